@@ -1,0 +1,169 @@
+"""Seeded synthetic inputs shared by the tests, the oracle runs and bench.py.
+
+This module holds NONE of the method's arithmetic (no tree, no draft, no
+sampling): it only produces token streams and logits that look like the
+paper's workloads, from explicit seeds.  Both the oracle (``oracle/``) and the
+CUDA path (``paper_2601_09083_b200``) consume what it returns; neither is
+imported here.
+
+Recipe (motivated by P:L97 long-tailed response
+lengths and P:L101 cross-epoch similarity):
+  * token ids: Zipf(1.1) ranks over V, mapped through a seeded permutation;
+  * per prompt p and epoch e a template R_{p,e}, length ~ LogNormal(median m,
+    sigma 0.9) clipped to [16, cap];
+  * sibling k's stream: copy of the template that forks with prob 0.03 per
+    position into a fresh Zipf segment (geometric length, mean 24) and re-joins
+    the template at a random offset within +-32;
+  * epoch drift: R_{p,e+1} = R_{p,e} with a 5% token edit rate;
+  * logits bulk x ~ N(0, 2^2); the row's head token gets mean + gap, where the
+    gap profile "rl-mix" draws 70% of rows from U[18,24] and 30% from U[12,18];
+    3 distractors at head - U[0.5, 4].
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["Workload", "zipf_tokens", "make_templates", "sibling_stream", "drift",
+           "make_workload", "random_logits_np", "bf16_bits", "gap_profile", "FIG3_VOCAB",
+           "fig3_sentences", "splitmix64"]
+
+
+def splitmix64(x: int) -> int:
+    """splitmix64 finaliser (Steele et al.), used for seeds and the prompt-owner hash."""
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def zipf_tokens(rng: np.random.Generator, n: int, V: int, perm: np.ndarray, s: float = 1.1):
+    r = rng.zipf(s, size=n)
+    r = np.minimum(r - 1, V - 1)
+    return perm[r].astype(np.int32)
+
+
+def _lengths(rng, n, median, cap, sigma=0.9):
+    L = np.exp(rng.normal(np.log(median), sigma, size=n))
+    return np.clip(L, 16, cap).astype(np.int64)
+
+
+def make_templates(rng, n_prompts, V, perm, median, cap):
+    lens = _lengths(rng, n_prompts, median, cap)
+    return [zipf_tokens(rng, int(l), V, perm) for l in lens]
+
+
+def sibling_stream(rng, template: np.ndarray, V: int, perm: np.ndarray, cap: int,
+                   fork_p: float = 0.03, fork_mean: int = 24, rejoin: int = 32):
+    out = []
+    i = 0
+    n = len(template)
+    while i < n and len(out) < cap:
+        if rng.random() < fork_p:
+            seg = int(rng.geometric(1.0 / fork_mean))
+            out.extend(zipf_tokens(rng, seg, V, perm).tolist())
+            i = max(0, min(n - 1, i + int(rng.integers(-rejoin, rejoin + 1))))
+        out.append(int(template[i]))
+        i += 1
+    return np.asarray(out[:cap], np.int32)
+
+
+def drift(rng, template: np.ndarray, V: int, perm: np.ndarray, rate: float = 0.05):
+    t = template.copy()
+    m = rng.random(len(t)) < rate
+    t[m] = zipf_tokens(rng, int(m.sum()), V, perm)
+    return t
+
+
+@dataclass
+class Workload:
+    """A synthetic rollout batch: prior-epoch rollouts (warm cache) and the
+    ground-truth streams of the active sequences."""
+    V: int
+    n_prompts: int
+    samples: int
+    prior: list = field(default_factory=list)       # list of (prompt, np.int32 tokens)
+    truth: list = field(default_factory=list)       # per active sequence: np.int32 tokens
+    seq_prompt: np.ndarray = None                   # prompt id per active sequence
+    seq_id: np.ndarray = None                       # u64 ids (epoch << 40 | p << 8 | k)
+
+
+def make_workload(seed: int, V: int, n_prompts: int, samples: int, median: int, cap: int,
+                  prior_epochs: int = 1, active: int | None = None) -> Workload:
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(V).astype(np.int32)
+    tmpl = make_templates(rng, n_prompts, V, perm, median, cap)
+    w = Workload(V=V, n_prompts=n_prompts, samples=samples)
+    for e in range(prior_epochs):
+        for p in range(n_prompts):
+            for k in range(samples):
+                w.prior.append((p, sibling_stream(rng, tmpl[p], V, perm, cap)))
+        tmpl = [drift(rng, t, V, perm) for t in tmpl]
+    n_act = n_prompts * samples if active is None else active
+    seq_prompt, seq_id, truth = [], [], []
+    for idx in range(n_act):
+        p, k = idx // samples, idx % samples
+        seq_prompt.append(p)
+        seq_id.append((prior_epochs << 40) | (p << 8) | k)
+        truth.append(sibling_stream(rng, tmpl[p], V, perm, cap))
+    w.truth = truth
+    w.seq_prompt = np.asarray(seq_prompt, np.int32)
+    w.seq_id = np.asarray(seq_id, np.uint64)
+    return w
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    """float32 -> bf16 bit patterns (uint16), round-to-nearest-even."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    rounded = (b + 0x7FFF + ((b >> 16) & 1)) >> 16
+    out = rounded.astype(np.uint16)
+    nan = np.isnan(x)
+    if nan.any():
+        out[nan] = 0x7FC0
+    return out
+
+
+def gap_profile(rng, n_rows: int, profile: str = "rl-mix") -> np.ndarray:
+    if profile == "rl-mix":
+        hi = rng.random(n_rows) < 0.7
+        return np.where(hi, rng.uniform(18, 24, n_rows), rng.uniform(12, 18, n_rows))
+    if profile == "peaked":
+        return np.full(n_rows, 26.0)
+    if profile == "moderate":
+        return np.full(n_rows, 18.0)
+    if profile == "flat":
+        return np.zeros(n_rows)
+    raise ValueError(profile)
+
+
+def random_logits_np(rng, n_rows: int, V: int, heads=None, profile: str = "rl-mix",
+                     sigma: float = 2.0) -> np.ndarray:
+    """float32 logits rows: bulk N(0, sigma^2), head token at +gap, 3 distractors."""
+    if profile == "flat":
+        return rng.random((n_rows, V), dtype=np.float32)
+    x = rng.normal(0.0, sigma, size=(n_rows, V)).astype(np.float32)
+    if heads is None:
+        heads = rng.integers(0, V, n_rows)
+    gaps = gap_profile(rng, n_rows, profile)
+    rows = np.arange(n_rows)
+    x[rows, heads] = gaps.astype(np.float32)
+    for _ in range(3):
+        d = rng.integers(0, V, n_rows)
+        x[rows, d] = (gaps - rng.uniform(0.5, 4.0, n_rows)).astype(np.float32)
+    x[rows, heads] = gaps.astype(np.float32)
+    return x
+
+
+# ---- the paper's Fig. 3 worked example, tokenised as in SPEC S:L76
+FIG3_VOCAB = {"the": 0, "cat": 1, "sit": 2, "on": 3, "mat": 4, "sofa": 5, "eat": 6, "fish": 7}
+
+
+def fig3_sentences():
+    """'the cat sit on the mat' x4, '... sofa' x1, 'the cat eat the fish' x2."""
+    s = []
+    s += ["the cat sit on the mat"] * 4
+    s += ["the cat sit on the sofa"] * 1
+    s += ["the cat eat the fish"] * 2
+    return [np.asarray([FIG3_VOCAB[w] for w in x.split()], np.int32) for x in s]
