@@ -1,0 +1,257 @@
+/*
+ * srt.h — C ABI of the B200-native SRT hot path (libsrt.so).
+ *
+ * SRT = "Speculative Rollout with Tree-Structured Cache" (arXiv 2601.09083).
+ * Citations: P:Lnn = line of PAPER.md (§3 "Method" unless noted); O1..O16 =
+ * the readings listed in DESIGN.md where the paper is silent or ambiguous.
+ *
+ * One step of the path (reading O14):
+ *     srt_draft   -> [policy forward on the drafted rows, outside this library]
+ *     srt_verify  -> srt_insert
+ *
+ * Conventions common to every call
+ * --------------------------------
+ *  - Every array argument is a DEVICE pointer owned by the caller (e.g. a torch
+ *    tensor's data_ptr()), in row-major layout, and must stay valid until the
+ *    work enqueued on `stream` has completed.  The library owns only the cache
+ *    pools, allocated in srt_cache_create and freed in srt_cache_destroy.
+ *  - All work is enqueued on the caller's `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream).  No call synchronises the stream,
+ *    except srt_cache_dump and srt_cache_status, which are documented blocking.
+ *    All calls on one cache must be ordered on one stream (no concurrent host
+ *    calls on the same cache).  Every call is CUDA-graph capturable except
+ *    srt_cache_create / destroy / dump / status.
+ *  - Errors: every call returns an srt_status.  SRT_ERR_INVALID_* are detected
+ *    on the host before anything is enqueued.  Problems only visible on the
+ *    device (out-of-vocabulary token, exhausted pool, NaN logit, bad prompt id)
+ *    set sticky bits in the cache's device status word, read by
+ *    srt_cache_status.  SRT_DEV_CAPACITY poisons the cache: recreate it.
+ *  - Sequence table: the caller's response tokens, seq_tok[s*stride + i] =
+ *    response token i of sequence s (int32), seq_len[s] = tokens committed so
+ *    far (t in the paper's y_{1:t}).  Prompt tokens are not part of it
+ *    (reading O2/O3: windows and matches are response-only).
+ *  - Token ids are int32 in [0, V).  Prompt ids are int32 in [0, P).
+ *
+ * Data layout in HBM (owned by the cache): a node pool shared by
+ * all prompts (node id p is the root of prompt p's tree T_p) as
+ * structure-of-arrays (token, count, child count, first child block), an
+ * open-addressing edge hash ((parent << 32) | token -> child id), and a pool of
+ * child-id blocks (4, 4, 8, 16, 32, 32, ... slots) for coalesced enumeration.
+ */
+#ifndef SRT_H_
+#define SRT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRT_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SRT_API __attribute__((visibility("default")))
+#else
+#define SRT_API
+#endif
+
+typedef enum {
+  SRT_OK = 0,
+  SRT_ERR_INVALID_CONFIG = 1, /* config violates a constraint below                   */
+  SRT_ERR_INVALID_ARG = 2,    /* null pointer, negative size, bad handle, T <= 0      */
+  SRT_ERR_CUDA = 3,           /* CUDA launch / allocation failure: srt_error_string() */
+  SRT_ERR_DEVICE = 4          /* a sticky device error is set: see srt_cache_status   */
+} srt_status;
+
+/* Sticky device error bits (srt_cache_status). */
+#define SRT_DEV_OOV 0x1u              /* a token >= V or < 0 was inserted/matched (window stops) */
+#define SRT_DEV_CAPACITY 0x2u         /* node / hash / slot pool exhausted: cache is poisoned    */
+#define SRT_DEV_BAD_PROMPT 0x4u       /* prompt id outside [0, P): the sequence is skipped       */
+#define SRT_DEV_NONFINITE_LOGIT 0x8u  /* a NaN logit was read (NaN is never sampled, O11)        */
+
+typedef enum { SRT_BF16 = 0, SRT_F32 = 1 } srt_dtype;
+
+typedef struct {
+  int32_t vocab_size;       /* V >= 2                                                      */
+  int32_t max_prompts;      /* P >= 1; prompt ids are dense in [0, P)                      */
+  int32_t max_depth;        /* D >= 1: window depth, every substring of length <= D is     */
+                            /*   indexed ("all substrings", reading O1/O2)           */
+  int32_t max_match_len;    /* L, 1 <= L <= min(D, 32): suffix-match cap (O3)      */
+  int32_t budget_max;       /* Bmax, 1 <= Bmax <= 64 (one u64 tree-mask word per node)     */
+  int32_t budget_base;      /* B(q) = min(Bmax, b0 + floor(q*num/den))  (O5)       */
+  int32_t budget_slope_num; /*   0 <= b0 <= Bmax, num >= 0, den >= 1                       */
+  int32_t budget_slope_den;
+  double min_path_score;    /* stop when the best frontier score is below this (O7); 0=off */
+  int64_t node_capacity;    /* node pool size, >= P + 1                                    */
+  int64_t hash_capacity;    /* edge-hash slots: a power of two >= 2*node_capacity          */
+  int64_t slot_capacity;    /* child-block words (4 B each), >= node_capacity              */
+  srt_dtype logits_dtype;   /* dtype of the logits passed to srt_verify                    */
+} srt_config;
+
+typedef struct srt_cache srt_cache; /* opaque */
+
+/* Device-side counters accumulated by srt_insert (optional, device pointer). */
+typedef struct {
+  unsigned long long windows;       /* window starts walked               */
+  unsigned long long increments;    /* count(u) += 1 operations (O1)      */
+  unsigned long long nodes_created; /* nodes created by this call         */
+} srt_insert_stats;
+
+/* Host-side snapshot returned by srt_cache_status (blocking). */
+typedef struct {
+  uint64_t nodes_used;     /* including the P roots                 */
+  uint64_t node_capacity;
+  uint64_t slots_used;     /* child-block words                     */
+  uint64_t slot_capacity;
+  uint64_t hash_capacity;
+} srt_cache_stats;
+
+/* One record of the canonical dump (SPEC S:L148-149 format). */
+typedef struct {
+  int32_t token;      /* -1 for the root                                   */
+  int32_t n_children;
+  uint64_t count;     /* root: sum of its children's counts                */
+} srt_dump_record;
+
+SRT_API int srt_abi_version(void);
+/* Human-readable text of the last SRT_ERR_CUDA on this host thread. */
+SRT_API const char* srt_error_string(void);
+
+/*
+ * srt_cache_create — allocate and initialise the trees of P prompts in HBM
+ * ("for each prompt p, a cache ... organized as a tree-structured cache
+ * T_p"; held in HBM rather than CPU memory, BJ:north_star (1)).
+ * Validates `cfg` (SRT_ERR_INVALID_CONFIG), allocates the pools with
+ * cudaMallocAsync on `stream`, initialises them, and builds the exact Gumbel
+ * noise bound tables used by srt_verify's pruning.  *out is set
+ * on success only.  Blocking only for the host-side bookkeeping.
+ */
+SRT_API srt_status srt_cache_create(const srt_config* cfg, void* stream, srt_cache** out);
+
+/* srt_cache_destroy — free the pools (stream-ordered).  NULL is a no-op. */
+SRT_API srt_status srt_cache_destroy(srt_cache* cache, void* stream);
+
+/*
+ * srt_insert — batched insertion of decoded / run-ahead spans ("decoded
+ * outputs of running rollouts are inserted online into T_p and node counts are
+ * updated"; run-ahead tokens "are inserted into T_p"; reading O1).
+ * For each span s < n: prompt prompt_id[s], tokens seq_tok[s*stride + i],
+ * new positions [from[s], to[s]), first allowed window start floor_[s]
+ * (floor_ may be NULL = 0).  Every window that ENDS at a new position gets +1:
+ * for each end j in [max(from,floor), to) and each d in [1, min(D, j-floor+1)],
+ * count(tokens[j-d+1 .. j]) += 1; missing nodes are created (lock-free CAS on
+ * the edge hash; atomic counts, so the result is independent of scheduling).
+ * stats_dev (device, nullable) is ACCUMULATED into.  n == 0 is a no-op.
+ */
+SRT_API srt_status srt_insert(srt_cache* cache, int32_t n, const int32_t* prompt_id,
+                      const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                      const int32_t* to, const int32_t* floor_, srt_insert_stats* stats_dev,
+                      void* stream);
+
+/*
+ * srt_draft — batched longest-suffix match + best-first draft + tree layout
+ * (P:L135-139).  For each sequence s < n (prompt prompt_id[s], response
+ * seq_tok[s*stride ...] of length t = seq_len[s]):
+ *  match   : q = largest q in [1, min(L, t)] such that the root walk along
+ *            y[t-q .. t-1] exists and has >= 1 child (O3); q = 0 = fallback,
+ *            empty draft ("revert to standard decoding for one step").
+ *  expand  : C(v) = count(v) / sum of the counts of v and its siblings,
+ *            score(v) = score(parent) * C(v), score(u_q) = 1 (fp64 RN, O6);
+ *            pop the best frontier node under the total order O8 (score desc,
+ *            depth asc, token asc, parent draft index asc) until B(q) nodes,
+ *            an empty frontier, or best score < min_path_score.
+ *  layout  : node i (pop order, 0 <= i < draft_len[s]) at [s*Bmax + i]:
+ *            draft_tok, draft_parent (-1 = the root = last committed token),
+ *            draft_depth (1 = child of the root), draft_pos = pos_base[s] + depth,
+ *            draft_mask = ancestor-or-self bitmask over draft indices (bit i).
+ *            Entries i >= draft_len[s] are tok=-1, parent=-1, depth=0, pos=-1,
+ *            mask=0.  match_len[s] = q.  row_offsets[n+1] (int64) = exclusive
+ *            scan of (draft_len + 1): the logits rows of sequence s are
+ *            [row_offsets[s], row_offsets[s+1]) in the order [root, node 0, ...].
+ * pos_base may be NULL (treated as 0).
+ */
+SRT_API srt_status srt_draft(srt_cache* cache, int32_t n, const int32_t* prompt_id,
+                     const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
+                     const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                     int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
+                     int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
+                     void* stream);
+
+/*
+ * srt_verify — lossless verification ("verifies and accepts drafted
+ * tokens up to the first mismatch"; "one decode pass ... verify
+ * multiple drafted tokens in parallel"; readings O10, O11, O13).
+ *  scan    : every logits row r of sequence s (row_offsets from srt_draft;
+ *            logits has row_offsets[n] rows of V elements of cfg.logits_dtype)
+ *            is sampled by Gumbel-max:  sampled[r] = argmax_v RN32(RN32(x_v/T)
+ *            + g_v), smallest v on ties, NaN never chosen, with
+ *            g_v = -log_det(-log_det(u)), u = (2(w>>9)+1) 2^-24, w = word (v&3)
+ *            of Philox4x32-10(ctr = (v>>2, pos, seq_id lo, hi), key = seed lo, hi),
+ *            pos = seq_len[s] for the root row, seq_len[s] + draft_depth for a
+ *            node row.  T == 1 skips the division.  T must be > 0.
+ *  walk    : from the root, accept the draft child whose token equals the
+ *            current row's sample, until none does; accept_len[s] = a,
+ *            accepted_nodes[s*Bmax + k] = draft index of the k-th accepted node
+ *            (rest -1).
+ *  commit  : the samples along the path (a accepted + 1 bonus token) are
+ *            written to commit_tok[s*(Bmax+1) + k] (rest -1), truncated after
+ *            the first eos_id (inclusive; eos_id < 0 = none) and at
+ *            max_new[s] - seq_len[s]; n_commit[s] = tokens committed; they are
+ *            appended to seq_tok (stride `stride`), seq_len[s] += n_commit[s],
+ *            finished[s] = EOS committed || seq_len[s] >= max_new[s].
+ * draft arrays are those srt_draft wrote (stride Bmax).  seq_tok must have
+ * room for seq_len[s] + Bmax + 1 tokens per row.
+ */
+SRT_API srt_status srt_verify(srt_cache* cache, int32_t n, const void* logits,
+                      const int64_t* row_offsets, const int32_t* draft_len,
+                      const int32_t* draft_tok, const int32_t* draft_parent,
+                      const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed,
+                      float temperature, int32_t eos_id, const int32_t* max_new,
+                      int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* sampled,
+                      int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+                      int32_t* accepted_nodes, uint8_t* finished, void* stream);
+
+/*
+ * srt_cache_dump — canonical serialization of T_p (BLOCKING; test path).
+ * Preorder records, children in ascending token order.
+ * host_buf (HOST pointer, capacity cap records) may be NULL to query the size;
+ * *n_records receives the total record count.  Returns SRT_ERR_DEVICE if the
+ * cache is poisoned.
+ */
+SRT_API srt_status srt_cache_dump(srt_cache* cache, int32_t prompt_id, srt_dump_record* host_buf,
+                          int64_t cap, int64_t* n_records, void* stream);
+
+/*
+ * srt_cache_status — BLOCKING: synchronises `stream`, returns the sticky
+ * device error bits (SRT_DEV_*) in *dev_error_bits and fills *stats (HOST
+ * pointers; either may be NULL).  Returns SRT_ERR_DEVICE iff any bit is set.
+ */
+SRT_API srt_status srt_cache_status(srt_cache* cache, uint32_t* dev_error_bits, srt_cache_stats* stats,
+                            void* stream);
+
+/* Clear the sticky error bits (not SRT_DEV_CAPACITY, which poisons). */
+SRT_API srt_status srt_cache_clear_errors(srt_cache* cache, void* stream);
+
+/*
+ * srt_noise_table — test support: out[r] = g(r) = -log_det(-log_det((2r+1) 2^-24))
+ * for all r in [0, 2^23) (DEVICE pointer, 2^23 floats), computed by the same
+ * device code srt_verify uses.  Lets a test compare the whole noise domain
+ * bitwise with the oracle (pin P9).
+ */
+SRT_API srt_status srt_noise_table(float* out, void* stream);
+
+/*
+ * srt_sample_rows_reference — test support: the UNPRUNED scan (every element's
+ * Philox + noise evaluated, one CTA per row) over the same rows as srt_verify's
+ * scan stage; writes sampled[].  Used to show the pruned scan changes no bit.
+ */
+SRT_API srt_status srt_sample_rows_reference(srt_cache* cache, int32_t n, const void* logits,
+                                     const int64_t* row_offsets, const int32_t* draft_depth,
+                                     const int32_t* seq_len, const uint64_t* seq_id,
+                                     uint64_t seed, float temperature, int32_t* sampled,
+                                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRT_H_ */

@@ -1,0 +1,339 @@
+// api.cu — host side of the C ABI declared in include/srt.h: validation,
+// pool allocation (cudaMallocAsync on the caller's stream), launches, status.
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <map>
+#include <vector>
+
+#include "srt_internal.cuh"
+
+using namespace srt;
+
+struct srt_cache {
+  srt_config cfg;
+  DevCache dev;
+  void* pool;           // one allocation holding every array below
+  long long* scratch;   // insert work offsets, grown on demand
+  int64_t scratch_cap;  // elements
+  int device;
+};
+
+namespace {
+
+thread_local char g_err[256] = "no error";
+
+srt_status cuda_fail(cudaError_t e, const char* what) {
+  snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+  return SRT_ERR_CUDA;
+}
+
+#define SRT_CUDA(call, what)                         \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+srt_status validate(const srt_config* c) {
+  if (!c) return SRT_ERR_INVALID_ARG;
+  if (c->vocab_size < 2 || c->max_prompts < 1 || c->max_depth < 1) return SRT_ERR_INVALID_CONFIG;
+  if (c->max_match_len < 1 || c->max_match_len > c->max_depth || c->max_match_len > 32)
+    return SRT_ERR_INVALID_CONFIG;
+  if (c->budget_max < 1 || c->budget_max > 64) return SRT_ERR_INVALID_CONFIG;
+  if (c->budget_base < 0 || c->budget_base > c->budget_max) return SRT_ERR_INVALID_CONFIG;
+  if (c->budget_slope_num < 0 || c->budget_slope_den < 1) return SRT_ERR_INVALID_CONFIG;
+  if (!(c->min_path_score >= 0.0)) return SRT_ERR_INVALID_CONFIG;
+  if (c->node_capacity < (int64_t)c->max_prompts + 1 || c->node_capacity >= (int64_t)BAD)
+    return SRT_ERR_INVALID_CONFIG;
+  if (!is_pow2(c->hash_capacity) || c->hash_capacity < 2 * c->node_capacity)
+    return SRT_ERR_INVALID_CONFIG;
+  if (c->slot_capacity < c->node_capacity || c->slot_capacity >= (int64_t)BAD)
+    return SRT_ERR_INVALID_CONFIG;
+  if (c->logits_dtype != SRT_BF16 && c->logits_dtype != SRT_F32) return SRT_ERR_INVALID_CONFIG;
+  return SRT_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+int srt_abi_version(void) { return SRT_ABI_VERSION; }
+
+const char* srt_error_string(void) { return g_err; }
+
+srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** out) {
+  if (!out) return SRT_ERR_INVALID_ARG;
+  srt_status st = validate(cfg);
+  if (st != SRT_OK) return st;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const size_t N = cfg->node_capacity, H = cfg->hash_capacity, W = cfg->slot_capacity;
+  size_t off = 0;
+  const size_t o_tok = off;     off = align_up(off + N * 4);
+  const size_t o_cnt = off;     off = align_up(off + N * 4);
+  const size_t o_nch = off;     off = align_up(off + N * 4);
+  const size_t o_blk = off;     off = align_up(off + N * 4);
+  const size_t o_hash = off;    off = align_up(off + H * sizeof(HashSlot));
+  const size_t o_slots = off;   off = align_up(off + W * 4);
+  const size_t o_ctr = off;     off = align_up(off + 2 * 8);
+  const size_t o_status = off;  off = align_up(off + 4);
+  const size_t o_gb = off;      off = align_up(off + (NOISE_BUCKETS + 1) * 4);
+  srt_cache* c = new srt_cache();
+  c->cfg = *cfg;
+  cudaGetDevice(&c->device);
+  cudaError_t e = cudaMallocAsync(&c->pool, off, stream);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMallocAsync(cache pools)");
+  }
+  char* b = (char*)c->pool;
+  DevCache& d = c->dev;
+  d.V = cfg->vocab_size; d.P = cfg->max_prompts; d.D = cfg->max_depth; d.L = cfg->max_match_len;
+  d.Bmax = cfg->budget_max; d.b0 = cfg->budget_base; d.snum = cfg->budget_slope_num;
+  d.sden = cfg->budget_slope_den; d.min_score = cfg->min_path_score;
+  d.N = N; d.H = H; d.W = W;
+  d.tok = (int32_t*)(b + o_tok);
+  d.cnt = (uint32_t*)(b + o_cnt);
+  d.nchild = (uint32_t*)(b + o_nch);
+  d.blk0 = (uint32_t*)(b + o_blk);
+  d.hash = (HashSlot*)(b + o_hash);
+  d.slots = (uint32_t*)(b + o_slots);
+  d.ctr = (unsigned long long*)(b + o_ctr);
+  d.status = (uint32_t*)(b + o_status);
+  d.gbound = (float*)(b + o_gb);
+  c->scratch = nullptr;
+  c->scratch_cap = 0;
+  if ((e = launch_init_cache(d, stream)) != cudaSuccess ||
+      (e = launch_noise_bounds(d, stream)) != cudaSuccess) {
+    cudaFreeAsync(c->pool, stream);
+    delete c;
+    return cuda_fail(e, "init kernels");
+  }
+  *out = c;
+  return SRT_OK;
+}
+
+srt_status srt_cache_destroy(srt_cache* c, void* stream) {
+  if (!c) return SRT_OK;
+  cudaFreeAsync(c->pool, (cudaStream_t)stream);
+  if (c->scratch) cudaFreeAsync(c->scratch, (cudaStream_t)stream);
+  delete c;
+  return SRT_OK;
+}
+
+srt_status srt_insert(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,
+                      int64_t stride, const int32_t* from, const int32_t* to,
+                      const int32_t* floor_, srt_insert_stats* stats_dev, void* stream_) {
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!prompt_id || !seq_tok || !from || !to) return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (c->scratch_cap < (int64_t)n + 1) {
+    if (c->scratch) SRT_CUDA(cudaFreeAsync(c->scratch, stream), "cudaFreeAsync(scratch)");
+    int64_t cap = std::max<int64_t>(4096, 2 * ((int64_t)n + 1));
+    SRT_CUDA(cudaMallocAsync(&c->scratch, cap * sizeof(long long), stream), "cudaMallocAsync(scratch)");
+    c->scratch_cap = cap;
+  }
+  SRT_CUDA(launch_insert(c->dev, n, prompt_id, seq_tok, stride, from, to, floor_, stats_dev,
+                         c->scratch, stream),
+           "insert kernels");
+  return SRT_OK;
+}
+
+srt_status srt_draft(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,
+                     int64_t stride, const int32_t* seq_len, const int32_t* pos_base,
+                     int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
+                     int32_t* draft_parent, int32_t* draft_depth, int32_t* draft_pos,
+                     uint64_t* draft_mask, int64_t* row_offsets, void* stream) {
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (!row_offsets) return SRT_ERR_INVALID_ARG;
+  if (n > 0 && (!prompt_id || !seq_tok || !seq_len || !match_len || !draft_len || !draft_tok ||
+                !draft_parent || !draft_depth || !draft_pos || !draft_mask))
+    return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(launch_draft(c->dev, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len,
+                        draft_len, draft_tok, draft_parent, draft_depth, draft_pos, draft_mask,
+                        row_offsets, (cudaStream_t)stream),
+           "draft kernels");
+  return SRT_OK;
+}
+
+srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t* row_offsets,
+                      const int32_t* draft_len, const int32_t* draft_tok,
+                      const int32_t* draft_parent, const int32_t* draft_depth,
+                      const uint64_t* seq_id, uint64_t seed, float temperature, int32_t eos_id,
+                      const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len,
+                      int32_t* sampled, int32_t* accept_len, int32_t* n_commit,
+                      int32_t* commit_tok, int32_t* accepted_nodes, uint8_t* finished,
+                      void* stream_) {
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!logits || !row_offsets || !draft_len || !draft_tok || !draft_parent || !draft_depth ||
+      !seq_id || !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit ||
+      !commit_tok || !accepted_nodes || !finished)
+    return SRT_ERR_INVALID_ARG;
+  VerifyArgs a{n,       logits,     (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
+               draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
+               seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
+               accepted_nodes, finished};
+  cudaStream_t stream = (cudaStream_t)stream_;
+  SRT_CUDA(launch_scan(c->dev, a, false, stream), "verify scan");
+  SRT_CUDA(launch_accept(c->dev, a, stream), "verify accept");
+  return SRT_OK;
+}
+
+srt_status srt_sample_rows_reference(srt_cache* c, int32_t n, const void* logits,
+                                     const int64_t* row_offsets, const int32_t* draft_depth,
+                                     const int32_t* seq_len, const uint64_t* seq_id,
+                                     uint64_t seed, float temperature, int32_t* sampled,
+                                     void* stream) {
+  if (!c || n < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!logits || !row_offsets || !draft_depth || !seq_len || !seq_id || !sampled)
+    return SRT_ERR_INVALID_ARG;
+  VerifyArgs a{};
+  a.n = n; a.logits = logits; a.dtype = (int)c->cfg.logits_dtype; a.row_offsets = row_offsets;
+  a.draft_depth = draft_depth; a.seq_id = seq_id; a.seed = seed; a.temperature = temperature;
+  a.seq_len = seq_len ? const_cast<int32_t*>(seq_len) : nullptr;
+  a.sampled = sampled;
+  SRT_CUDA(launch_scan(c->dev, a, true, (cudaStream_t)stream), "reference scan");
+  return SRT_OK;
+}
+
+srt_status srt_cache_status(srt_cache* c, uint32_t* bits, srt_cache_stats* stats, void* stream_) {
+  if (!c) return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint32_t h_status = 0;
+  unsigned long long h_ctr[2] = {0, 0};
+  SRT_CUDA(cudaMemcpyAsync(&h_status, c->dev.status, 4, cudaMemcpyDeviceToHost, stream), "status");
+  SRT_CUDA(cudaMemcpyAsync(h_ctr, c->dev.ctr, 16, cudaMemcpyDeviceToHost, stream), "status");
+  SRT_CUDA(cudaStreamSynchronize(stream), "status sync");
+  if (bits) *bits = h_status;
+  if (stats) {
+    stats->nodes_used = std::min<unsigned long long>(h_ctr[0], c->dev.N);
+    stats->node_capacity = c->dev.N;
+    stats->slots_used = std::min<unsigned long long>(h_ctr[1], c->dev.W);
+    stats->slot_capacity = c->dev.W;
+    stats->hash_capacity = c->dev.H;
+  }
+  return h_status ? SRT_ERR_DEVICE : SRT_OK;
+}
+
+srt_status srt_cache_clear_errors(srt_cache* c, void* stream_) {
+  if (!c) return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint32_t h_status = 0;
+  SRT_CUDA(cudaMemcpyAsync(&h_status, c->dev.status, 4, cudaMemcpyDeviceToHost, stream), "status");
+  SRT_CUDA(cudaStreamSynchronize(stream), "status sync");
+  h_status &= SRT_DEV_CAPACITY;
+  SRT_CUDA(cudaMemcpyAsync(c->dev.status, &h_status, 4, cudaMemcpyHostToDevice, stream), "status");
+  SRT_CUDA(cudaStreamSynchronize(stream), "status sync");
+  return SRT_OK;
+}
+
+srt_status srt_noise_table(float* out, void* stream) {
+  if (!out) return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(launch_noise_table(out, (cudaStream_t)stream), "noise table");
+  return SRT_OK;
+}
+
+srt_status srt_cache_dump(srt_cache* c, int32_t p, srt_dump_record* host_buf, int64_t cap,
+                          int64_t* n_records, void* stream_) {
+  if (!c || !n_records || p < 0 || p >= c->cfg.max_prompts || cap < 0) return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint32_t bits = 0;
+  srt_status st = srt_cache_status(c, &bits, nullptr, stream);
+  if (st == SRT_ERR_CUDA) return st;
+  if (bits & SRT_DEV_CAPACITY) return SRT_ERR_DEVICE;
+  // Breadth-first enumeration, one level per launch (<= D levels); the host
+  // then sorts siblings by token and emits the preorder.
+  struct HNode { int32_t tok; uint32_t cnt; std::vector<int64_t> kids; };
+  std::vector<HNode> nodes;
+  uint32_t root_nchild = 0;
+  SRT_CUDA(cudaMemcpyAsync(&root_nchild, c->dev.nchild + p, 4, cudaMemcpyDeviceToHost, stream), "dump");
+  SRT_CUDA(cudaStreamSynchronize(stream), "dump");
+  nodes.push_back(HNode{-1, 0, {}});
+  std::vector<uint32_t> frontier = {(uint32_t)p};
+  std::vector<int64_t> frontier_idx = {0};
+  std::vector<uint32_t> frontier_nch = {root_nchild};
+  while (!frontier.empty()) {
+    uint64_t total = 0;
+    for (uint32_t x : frontier_nch) total += x;
+    if (total == 0) break;
+    uint32_t *d_front = nullptr, *d_node = nullptr, *d_cnt = nullptr, *d_nch = nullptr;
+    int32_t *d_par = nullptr, *d_tok = nullptr;
+    unsigned int* d_n = nullptr;
+    const int32_t nf = (int32_t)frontier.size();
+    SRT_CUDA(cudaMallocAsync(&d_front, nf * 4, stream), "dump alloc");
+    SRT_CUDA(cudaMallocAsync(&d_node, total * 4, stream), "dump alloc");
+    SRT_CUDA(cudaMallocAsync(&d_cnt, total * 4, stream), "dump alloc");
+    SRT_CUDA(cudaMallocAsync(&d_nch, total * 4, stream), "dump alloc");
+    SRT_CUDA(cudaMallocAsync(&d_par, total * 4, stream), "dump alloc");
+    SRT_CUDA(cudaMallocAsync(&d_tok, total * 4, stream), "dump alloc");
+    SRT_CUDA(cudaMallocAsync(&d_n, 4, stream), "dump alloc");
+    SRT_CUDA(cudaMemsetAsync(d_n, 0, 4, stream), "dump");
+    SRT_CUDA(cudaMemcpyAsync(d_front, frontier.data(), nf * 4, cudaMemcpyHostToDevice, stream), "dump");
+    SRT_CUDA(launch_dump_level(c->dev, d_front, nf, d_node, d_par, d_tok, d_cnt, d_nch, d_n, stream),
+             "dump kernel");
+    std::vector<uint32_t> h_node(total), h_cnt(total), h_nch(total);
+    std::vector<int32_t> h_par(total), h_tok(total);
+    unsigned int h_n = 0;
+    SRT_CUDA(cudaMemcpyAsync(&h_n, d_n, 4, cudaMemcpyDeviceToHost, stream), "dump");
+    SRT_CUDA(cudaMemcpyAsync(h_node.data(), d_node, total * 4, cudaMemcpyDeviceToHost, stream), "dump");
+    SRT_CUDA(cudaMemcpyAsync(h_cnt.data(), d_cnt, total * 4, cudaMemcpyDeviceToHost, stream), "dump");
+    SRT_CUDA(cudaMemcpyAsync(h_nch.data(), d_nch, total * 4, cudaMemcpyDeviceToHost, stream), "dump");
+    SRT_CUDA(cudaMemcpyAsync(h_par.data(), d_par, total * 4, cudaMemcpyDeviceToHost, stream), "dump");
+    SRT_CUDA(cudaMemcpyAsync(h_tok.data(), d_tok, total * 4, cudaMemcpyDeviceToHost, stream), "dump");
+    SRT_CUDA(cudaStreamSynchronize(stream), "dump");
+    cudaFreeAsync(d_front, stream); cudaFreeAsync(d_node, stream); cudaFreeAsync(d_cnt, stream);
+    cudaFreeAsync(d_nch, stream); cudaFreeAsync(d_par, stream); cudaFreeAsync(d_tok, stream);
+    cudaFreeAsync(d_n, stream);
+    if (h_n != total) {
+      snprintf(g_err, sizeof g_err, "dump: child count mismatch (%u vs %llu)", h_n,
+               (unsigned long long)total);
+      return SRT_ERR_CUDA;
+    }
+    std::vector<uint32_t> nf_nodes;
+    std::vector<int64_t> nf_idx;
+    std::vector<uint32_t> nf_nch;
+    for (uint64_t k = 0; k < total; ++k) {
+      int64_t idx = (int64_t)nodes.size();
+      nodes.push_back(HNode{h_tok[k], h_cnt[k], {}});
+      nodes[frontier_idx[h_par[k]]].kids.push_back(idx);
+      nf_nodes.push_back(h_node[k]);
+      nf_idx.push_back(idx);
+      nf_nch.push_back(h_nch[k]);
+    }
+    frontier.swap(nf_nodes);
+    frontier_idx.swap(nf_idx);
+    frontier_nch.swap(nf_nch);
+  }
+  // preorder with children ascending by token
+  int64_t k = 0;
+  std::vector<int64_t> stack = {0};
+  while (!stack.empty()) {
+    int64_t i = stack.back();
+    stack.pop_back();
+    HNode& h = nodes[i];
+    std::sort(h.kids.begin(), h.kids.end(),
+              [&](int64_t a, int64_t b) { return nodes[a].tok < nodes[b].tok; });
+    if (host_buf && k < cap) {
+      uint64_t count = h.cnt;
+      if (i == 0) {
+        count = 0;
+        for (int64_t kid : h.kids) count += nodes[kid].cnt;
+      }
+      host_buf[k] = srt_dump_record{h.tok, (int32_t)h.kids.size(), count};
+    }
+    ++k;
+    for (auto it = h.kids.rbegin(); it != h.kids.rend(); ++it) stack.push_back(*it);
+  }
+  *n_records = k;
+  return SRT_OK;
+}
+
+}  // extern "C"

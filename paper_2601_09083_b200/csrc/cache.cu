@@ -1,0 +1,96 @@
+// cache.cu — cache initialisation, the exact noise-bound tables, the noise
+// table test hook and the dump enumeration kernel.
+#include "noise.cuh"
+#include "srt_internal.cuh"
+
+namespace srt {
+
+__global__ void k_init_counters(DevCache c) {
+  c.ctr[0] = (unsigned long long)c.P;  // node ids 0..P-1 are the roots
+  c.ctr[1] = 0;
+  *c.status = 0;
+}
+
+cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(c.tok, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.cnt, 0, c.N * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.nchild, 0, c.N * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.blk0, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.hash, 0xFF, c.H * sizeof(HashSlot), stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.slots, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
+  k_init_counters<<<1, 1, 0, stream>>>(c);
+  return cudaGetLastError();
+}
+
+// Bucket b covers r in [b << 13, (b+1) << 13): gbound[b] = max g(r) over the
+// bucket, gbound[1024] = max over all r.  Computed by enumeration, so the
+// bound is exact whatever the shape of g.
+__global__ void __launch_bounds__(256) k_noise_bucket_max(float* gbound) {
+  __shared__ float red[8];
+  const uint32_t b = blockIdx.x;
+  float m = -INFINITY;
+  for (uint32_t j = threadIdx.x; j < (1u << NOISE_BUCKET_SHIFT); j += blockDim.x)
+    m = fmaxf(m, gumbel_of_r((b << NOISE_BUCKET_SHIFT) | j));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+    gbound[b] = m;
+  }
+}
+
+__global__ void k_noise_global_max(float* gbound) {
+  float m = -INFINITY;
+  for (int b = threadIdx.x; b < NOISE_BUCKETS; b += 32) m = fmaxf(m, gbound[b]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x == 0) gbound[NOISE_BUCKETS] = m;
+}
+
+cudaError_t launch_noise_bounds(const DevCache& c, cudaStream_t stream) {
+  k_noise_bucket_max<<<NOISE_BUCKETS, 256, 0, stream>>>(c.gbound);
+  k_noise_global_max<<<1, 32, 0, stream>>>(c.gbound);
+  return cudaGetLastError();
+}
+
+__global__ void k_noise_table(float* out) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < (1u << 23)) out[r] = gumbel_of_r(r);
+}
+
+cudaError_t launch_noise_table(float* out, cudaStream_t stream) {
+  k_noise_table<<<(1u << 23) / 256, 256, 0, stream>>>(out);
+  return cudaGetLastError();
+}
+
+// One thread per frontier node: emit every child (test path only).
+__global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, uint32_t* out_node,
+                             int32_t* out_parent, int32_t* out_tok, uint32_t* out_cnt,
+                             uint32_t* out_nchild, unsigned int* out_n) {
+  const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const uint32_t u = frontier[f];
+  const uint32_t F = c.nchild[u];
+  const uint32_t b0 = c.blk0[u];
+  for (uint32_t k = 0; k < F; ++k) {
+    const uint32_t ch = c.slots[child_slot_word(c, u, b0, k)];
+    const unsigned int o = atomicAdd(out_n, 1u);
+    out_node[o] = ch;
+    out_parent[o] = f;
+    out_tok[o] = c.tok[ch];
+    out_cnt[o] = c.cnt[ch];
+    out_nchild[o] = c.nchild[ch];
+  }
+}
+
+cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
+                              uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,
+                              uint32_t* out_cnt, uint32_t* out_nchild, unsigned int* out_n,
+                              cudaStream_t stream) {
+  k_dump_level<<<(nf + 127) / 128, 128, 0, stream>>>(c, frontier, nf, out_node, out_parent,
+                                                      out_tok, out_cnt, out_nchild, out_n);
+  return cudaGetLastError();
+}
+
+}  // namespace srt

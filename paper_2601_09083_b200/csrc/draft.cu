@@ -1,0 +1,315 @@
+// draft.cu — srt_draft: batched longest-suffix match, best-first draft
+// expansion and tree-attention layout (readings O3-O9).
+//
+// One warp per sequence.  Match: lane q-1 walks the root along y[t-q .. t-1]
+// (q hash probes, all lanes in parallel) and a ballot keeps the largest q whose
+// node has a child.  Expansion: a frontier sorted under the total order O8 is
+// kept in shared memory (<= Bmax entries, truncated to B - popped, which is
+// exact because a child never outranks its parent); the children of each
+// popped node are enumerated 32 at a time from its child blocks (coalesced
+// block reads + count/token gathers) and inserted with warp ballots.
+// Roofline: latency-bound (L + ~3 B dependent loads per warp); us per batch.
+#include "srt_internal.cuh"
+
+namespace srt {
+
+namespace {
+
+constexpr int DRAFT_WARPS = 4;
+constexpr int FCAP = 64;
+
+struct FrontierSmem {
+  double score[FCAP];
+  int32_t depth[FCAP];
+  int32_t tok[FCAP];
+  int32_t parent[FCAP];
+  uint32_t node[FCAP];
+  unsigned long long mask[FCAP];  // ancestor-or-self masks of drafted nodes
+};
+
+struct Cand {
+  double score;
+  int32_t depth, tok, parent;
+  uint32_t node;
+};
+
+// O8: score desc, depth asc, token asc, parent draft index asc.
+__device__ __forceinline__ bool better(double s1, int32_t d1, int32_t t1, int32_t p1, double s2,
+                                       int32_t d2, int32_t t2, int32_t p2) {
+  if (s1 != s2) return s1 > s2;
+  if (d1 != d2) return d1 < d2;
+  if (t1 != t2) return t1 < t2;
+  return p1 < p2;
+}
+
+__device__ __forceinline__ bool entry_better(const FrontierSmem& F, int j, const Cand& c) {
+  return better(F.score[j], F.depth[j], F.tok[j], F.parent[j], c.score, c.depth, c.tok, c.parent);
+}
+
+// Insert c into the sorted frontier of current size `size`, keeping at most
+// `cap` entries.  Warp-collective; returns the new size.
+__device__ __forceinline__ int frontier_insert(FrontierSmem& F, int size, int cap, const Cand& c,
+                                               int lane) {
+  const bool b0 = lane < size && entry_better(F, lane, c);
+  const bool b1 = lane + 32 < size && entry_better(F, lane + 32, c);
+  const int pos = __popc(__ballot_sync(0xffffffffu, b0)) + __popc(__ballot_sync(0xffffffffu, b1));
+  if (pos >= cap) return size;
+  const int newsize = min(size + 1, cap);
+  Cand e0, e1;
+  const bool m0 = lane >= pos && lane < newsize - 1;
+  const bool m1 = lane + 32 >= pos && lane + 32 < newsize - 1;
+  if (m0) e0 = Cand{F.score[lane], F.depth[lane], F.tok[lane], F.parent[lane], F.node[lane]};
+  if (m1) e1 = Cand{F.score[lane + 32], F.depth[lane + 32], F.tok[lane + 32], F.parent[lane + 32],
+                    F.node[lane + 32]};
+  __syncwarp();
+  if (m0) {
+    F.score[lane + 1] = e0.score; F.depth[lane + 1] = e0.depth; F.tok[lane + 1] = e0.tok;
+    F.parent[lane + 1] = e0.parent; F.node[lane + 1] = e0.node;
+  }
+  if (m1) {
+    F.score[lane + 33] = e1.score; F.depth[lane + 33] = e1.depth; F.tok[lane + 33] = e1.tok;
+    F.parent[lane + 33] = e1.parent; F.node[lane + 33] = e1.node;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    F.score[pos] = c.score; F.depth[pos] = c.depth; F.tok[pos] = c.tok;
+    F.parent[pos] = c.parent; F.node[pos] = c.node;
+  }
+  __syncwarp();
+  return newsize;
+}
+
+__device__ __forceinline__ Cand frontier_pop(FrontierSmem& F, int size, int lane) {
+  const Cand top{F.score[0], F.depth[0], F.tok[0], F.parent[0], F.node[0]};
+  Cand e0, e1;
+  const bool m0 = lane >= 1 && lane < size;
+  const bool m1 = lane + 32 < size;
+  if (m0) e0 = Cand{F.score[lane], F.depth[lane], F.tok[lane], F.parent[lane], F.node[lane]};
+  if (m1) e1 = Cand{F.score[lane + 32], F.depth[lane + 32], F.tok[lane + 32], F.parent[lane + 32],
+                    F.node[lane + 32]};
+  __syncwarp();
+  if (m0) {
+    F.score[lane - 1] = e0.score; F.depth[lane - 1] = e0.depth; F.tok[lane - 1] = e0.tok;
+    F.parent[lane - 1] = e0.parent; F.node[lane - 1] = e0.node;
+  }
+  if (m1) {
+    F.score[lane + 31] = e1.score; F.depth[lane + 31] = e1.depth; F.tok[lane + 31] = e1.tok;
+    F.parent[lane + 31] = e1.parent; F.node[lane + 31] = e1.node;
+  }
+  __syncwarp();
+  return top;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Push the children of u (C(v) = count(v) / sum over u's children, P:L137;
+// score = score_u * C) into the frontier.
+__device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uint32_t u,
+                      double score_u, int32_t depth_u, int32_t parent_idx, int lane) {
+  const uint32_t nch = c.nchild[u];
+  if (nch == 0 || cap <= 0) return size;
+  const uint32_t b0 = c.blk0[u];
+  // pass 1: sibling sum (first 32 children kept in registers)
+  uint32_t ch0 = 0, cnt0 = 0;
+  int32_t tok0 = 0;
+  unsigned long long sum = 0;
+  for (uint32_t k = lane; k < nch; k += 32) {
+    const uint32_t ch = c.slots[child_slot_word(c, u, b0, k)];
+    const uint32_t cc = c.cnt[ch];
+    if (k < 32) {
+      ch0 = ch;
+      cnt0 = cc;
+      tok0 = c.tok[ch];
+    }
+    sum += cc;
+  }
+  sum = warp_sum_u64(sum);
+  const double dsum = (double)sum;  // exact: < 2^53
+  // pass 2: score every child and merge it into the frontier
+  for (uint32_t kb = 0; kb < nch; kb += 32) {
+    const uint32_t k = kb + lane;
+    const bool valid = k < nch;
+    Cand cd{0.0, depth_u + 1, 0, parent_idx, 0};
+    if (valid) {
+      uint32_t ch = ch0, cc = cnt0;
+      int32_t tk = tok0;
+      if (kb > 0) {
+        ch = c.slots[child_slot_word(c, u, b0, k)];
+        cc = c.cnt[ch];
+        tk = c.tok[ch];
+      }
+      const double C = sum ? __ddiv_rn((double)cc, dsum) : 0.0;
+      cd.score = __dmul_rn(score_u, C);
+      cd.tok = tk;
+      cd.node = ch;
+    }
+    // cheap prefilter against the current worst entry when full
+    bool want = valid;
+    if (want && size == cap) want = !entry_better(F, cap - 1, cd);
+    unsigned pending = __ballot_sync(0xffffffffu, want);
+    while (pending) {
+      const int src = __ffs(pending) - 1;
+      pending &= pending - 1;
+      Cand b;
+      b.score = __shfl_sync(0xffffffffu, cd.score, src);
+      b.depth = cd.depth;
+      b.tok = __shfl_sync(0xffffffffu, cd.tok, src);
+      b.parent = parent_idx;
+      b.node = __shfl_sync(0xffffffffu, cd.node, src);
+      size = frontier_insert(F, size, cap, b, lane);
+    }
+  }
+  return size;
+}
+
+__global__ void __launch_bounds__(DRAFT_WARPS * 32)
+k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
+        const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ seq_len,
+        const int32_t* __restrict__ pos_base, int32_t* __restrict__ match_len,
+        int32_t* __restrict__ draft_len, int32_t* __restrict__ draft_tok,
+        int32_t* __restrict__ draft_parent, int32_t* __restrict__ draft_depth,
+        int32_t* __restrict__ draft_pos, uint64_t* __restrict__ draft_mask) {
+  __shared__ FrontierSmem smem[DRAFT_WARPS];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int32_t s = blockIdx.x * DRAFT_WARPS + w;
+  if (s >= n) return;
+  FrontierSmem& F = smem[w];
+  const int32_t p = prompt_id[s];
+  const int32_t t = seq_len[s];
+  const int32_t* y = seq_tok + (int64_t)s * stride;
+  const int32_t Bmax = c.Bmax;
+  const int32_t pb = pos_base ? pos_base[s] : 0;
+  int32_t q = 0;
+  uint32_t uq = 0;
+  if (p < 0 || p >= c.P) {
+    if (lane == 0) set_error(c, SRT_DEV_BAD_PROMPT);
+  } else {
+    // ---- longest-suffix match (O3): lane handles q = lane + 1
+    const int32_t qmax = min(c.L, t);
+    const int32_t myq = lane + 1;
+    bool ok = myq <= qmax;
+    uint32_t node = (uint32_t)p;
+    if (ok) {
+      for (int32_t j = t - myq; j < t; ++j) {
+        const int32_t tk = y[j];
+        if (tk < 0 || tk >= c.V) {
+          set_error(c, SRT_DEV_OOV);
+          ok = false;
+          break;
+        }
+        node = child_of(c, node, tk);
+        if (node == NONE) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    const bool has = ok && c.nchild[node] > 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, has);
+    q = bal ? 32 - __clz(bal) : 0;
+    uq = __shfl_sync(0xffffffffu, node, q > 0 ? q - 1 : 0);
+  }
+  int32_t popped = 0;
+  if (q > 0) {
+    const long long bq = (long long)c.b0 + ((long long)q * c.snum) / c.sden;
+    const int32_t B = (int32_t)min((long long)Bmax, bq);
+    int size = expand(c, F, 0, B, uq, 1.0, 0, -1, lane);
+    while (popped < B && size > 0) {
+      __syncwarp();
+      if (F.score[0] < c.min_score) break;
+      const Cand top = frontier_pop(F, size, lane);
+      --size;
+      const int32_t i = popped++;
+      if (lane == 0) {
+        const unsigned long long m =
+            (top.parent >= 0 ? F.mask[top.parent] : 0ull) | (1ull << i);
+        F.mask[i] = m;
+        const int64_t o = (int64_t)s * Bmax + i;
+        draft_tok[o] = top.tok;
+        draft_parent[o] = top.parent;
+        draft_depth[o] = top.depth;
+        draft_pos[o] = pb + top.depth;
+        draft_mask[o] = m;
+      }
+      __syncwarp();
+      const int cap = B - popped;
+      if (size > cap) size = cap;
+      size = expand(c, F, size, cap, top.node, top.score, top.depth, i, lane);
+    }
+  }
+  for (int32_t i = popped + lane; i < Bmax; i += 32) {
+    const int64_t o = (int64_t)s * Bmax + i;
+    draft_tok[o] = -1;
+    draft_parent[o] = -1;
+    draft_depth[o] = 0;
+    draft_pos[o] = -1;
+    draft_mask[o] = 0;
+  }
+  if (lane == 0) {
+    match_len[s] = q;
+    draft_len[s] = popped;
+  }
+}
+
+constexpr int SCAN_THREADS = 1024;
+
+// row_offsets[s] = sum_{s' < s} (draft_len[s'] + 1)  (logits rows: root + nodes)
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_row_offsets(int32_t n, const int32_t* __restrict__ draft_len, int64_t* __restrict__ row_offsets) {
+  __shared__ long long warp_tot[SCAN_THREADS / 32];
+  __shared__ long long carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t base = 0; base < n; base += SCAN_THREADS) {
+    const int32_t s = base + threadIdx.x;
+    const long long w = s < n ? (long long)draft_len[s] + 1 : 0;
+    long long x = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long yv = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += yv;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      long long tt = warp_tot[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        long long yv = __shfl_up_sync(0xffffffffu, tt, o);
+        if (lane >= o) tt += yv;
+      }
+      warp_tot[lane] = tt;
+    }
+    __syncthreads();
+    const long long before = carry + (wid ? warp_tot[wid - 1] : 0) + x - w;
+    if (s < n) row_offsets[s] = before;
+    __syncthreads();
+    if (threadIdx.x == SCAN_THREADS - 1) carry = before + w;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row_offsets[n] = carry;
+}
+
+}  // namespace
+
+cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                         const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
+                         const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                         int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
+                         int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
+                         cudaStream_t stream) {
+  if (n > 0) {
+    k_draft<<<(n + DRAFT_WARPS - 1) / DRAFT_WARPS, DRAFT_WARPS * 32, 0, stream>>>(
+        c, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len, draft_len, draft_tok,
+        draft_parent, draft_depth, draft_pos, draft_mask);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_row_offsets<<<1, SCAN_THREADS, 0, stream>>>(n, draft_len, row_offsets);
+  return cudaGetLastError();
+}
+
+}  // namespace srt

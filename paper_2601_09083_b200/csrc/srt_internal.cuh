@@ -1,0 +1,183 @@
+// srt_internal.cuh — device-side data structures and primitives of libsrt.
+//
+// Layout of one cache in HBM.  All prompts share one node pool;
+// node id p (0 <= p < P) is the root of prompt p's tree T_p.
+//   tok[N]     i32  token labelling the edge into the node
+//   cnt[N]     u32  count(u) ("frequency statistics"; reading O1)
+//   nchild[N]  u32  number of children
+//   blk0[N]    u32  word offset of the node's first child block (NONE if none)
+//   hash[H]    16 B open-addressing edge hash: key (parent << 32) | token -> child id;
+//                   keys (node << 32) | 0x80000000 | i -> word offset of child block i >= 1
+//   slots[W]   u32  child-id blocks of 4, 4, 8, 16, 32, 32, ... slots
+// Concurrency: insertion creates nodes with a CAS on the hash key and publishes
+// the value with a release store; counts are atomic adds, so the logical tree
+// (set of (path, count)) does not depend on scheduling.  Node ids do, but no
+// output exposes them (draft order uses counts + tokens only; O8/O15).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/srt.h"
+
+namespace srt {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;  // "no block" / "value pending"
+constexpr uint32_t BAD = 0xFFFFFFFEu;   // creation failed (capacity): walk stops
+constexpr unsigned long long EMPTY_KEY = ~0ull;
+constexpr uint32_t BLOCK_TAG = 0x80000000u;  // tokens are < 2^31
+
+struct alignas(16) HashSlot {
+  unsigned long long key;
+  uint32_t val;
+  uint32_t pad;
+};
+
+// Exact noise bounds: g over the 2^23 noise inputs, bucketed by
+// r >> 13 (1024 buckets), plus the global max.
+constexpr int NOISE_BUCKETS = 1024;
+constexpr int NOISE_BUCKET_SHIFT = 13;
+
+struct DevCache {
+  int32_t V, P, D, L, Bmax, b0, snum, sden;
+  double min_score;
+  unsigned long long N, H, W;
+  int32_t* tok;
+  uint32_t* cnt;
+  uint32_t* nchild;
+  uint32_t* blk0;
+  HashSlot* hash;
+  uint32_t* slots;
+  unsigned long long* ctr;  // [0] next node id, [1] next slot word
+  uint32_t* status;         // sticky SRT_DEV_* bits
+  float* gbound;            // [NOISE_BUCKETS] bucket maxima, [NOISE_BUCKETS] = global max
+};
+
+// ---------------------------------------------------------------------------
+// memory-model helpers (gpu scope; L1 is not coherent, so polled words use
+// relaxed/acquire loads that go to L2)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void set_error(const DevCache& c, uint32_t bits) {
+  atomicOr(c.status, bits);
+}
+
+// splitmix64 finaliser as the hash mixer
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned long long edge_key(uint32_t parent, uint32_t tok) {
+  return ((unsigned long long)parent << 32) | tok;
+}
+__device__ __forceinline__ unsigned long long block_key(uint32_t node, uint32_t i) {
+  return ((unsigned long long)node << 32) | (BLOCK_TAG | i);
+}
+
+// ---- child-block geometry: blocks of 4, 4, 8, 16, then 32-slot blocks ----
+__device__ __forceinline__ uint32_t blk_index(uint32_t k) {
+  return k < 8 ? (k >> 2) : (k < 32 ? (uint32_t)(30 - __clz(k)) : 3u + (k >> 5));
+}
+__device__ __forceinline__ uint32_t blk_start(uint32_t i) {
+  return i < 2 ? 4u * i : (i < 4 ? (4u << (i - 1)) : 32u * (i - 3));
+}
+__device__ __forceinline__ uint32_t blk_size(uint32_t i) {
+  return i < 2 ? 4u : (i < 4 ? (4u << (i - 1)) : 32u);
+}
+
+// Read-only lookup (kernels that run after all insertion is complete).
+// Returns NONE if the key is absent.
+__device__ __forceinline__ uint32_t hash_find(const DevCache& c, unsigned long long key) {
+  unsigned long long mask = c.H - 1;
+  unsigned long long h = mix64(key) & mask;
+  for (unsigned long long probe = 0; probe <= mask; ++probe) {
+    const HashSlot* s = c.hash + h;
+    unsigned long long k = __ldg(&s->key);
+    if (k == key) return __ldg(&s->val);
+    if (k == EMPTY_KEY) return NONE;
+    h = (h + 1) & mask;
+  }
+  return NONE;
+}
+
+__device__ __forceinline__ uint32_t child_of(const DevCache& c, uint32_t u, int32_t tok) {
+  return hash_find(c, edge_key(u, (uint32_t)tok));
+}
+
+// word offset of child slot k of node u (read-only kernels)
+__device__ __forceinline__ uint32_t child_slot_word(const DevCache& c, uint32_t u, uint32_t blk0,
+                                                    uint32_t k) {
+  uint32_t i = blk_index(k);
+  uint32_t base = (i == 0) ? blk0 : hash_find(c, block_key(u, i));
+  return base + (k - blk_start(i));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// Launchers (defined in the .cu files; all enqueue on `stream`)
+// ---------------------------------------------------------------------------
+cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream);
+cudaError_t launch_noise_bounds(const DevCache& c, cudaStream_t stream);
+cudaError_t launch_noise_table(float* out, cudaStream_t stream);
+cudaError_t launch_insert(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                          const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                          const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
+                          long long* scratch, cudaStream_t stream);
+cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                         const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
+                         const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                         int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
+                         int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
+                         cudaStream_t stream);
+struct VerifyArgs {
+  int32_t n;
+  const void* logits;
+  int dtype;
+  const int64_t* row_offsets;
+  const int32_t* draft_len;
+  const int32_t* draft_tok;
+  const int32_t* draft_parent;
+  const int32_t* draft_depth;
+  const uint64_t* seq_id;
+  uint64_t seed;
+  float temperature;
+  int32_t eos_id;
+  const int32_t* max_new;
+  int32_t* seq_tok;
+  int64_t stride;
+  int32_t* seq_len;
+  int32_t* sampled;
+  int32_t* accept_len;
+  int32_t* n_commit;
+  int32_t* commit_tok;
+  int32_t* accepted_nodes;
+  uint8_t* finished;
+};
+cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference,
+                        cudaStream_t stream);
+cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, cudaStream_t stream);
+cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
+                              uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,
+                              uint32_t* out_cnt, uint32_t* out_nchild, unsigned int* out_n,
+                              cudaStream_t stream);
+
+}  // namespace srt

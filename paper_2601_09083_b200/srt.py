@@ -1,0 +1,213 @@
+"""Thin Python binding of libsrt's C ABI (include/srt.h) over torch tensors.
+
+torch is used for device memory and streams only: this module allocates
+output tensors (torch.empty) and passes data pointers + the current stream to
+the C ABI; every step of the SRT path runs inside libsrt's CUDA kernels.
+Names follow the paper: insert, draft, verify.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import SrtCacheStats, SrtConfig, SrtDumpRecord, SrtError, check
+
+__all__ = ["SrtCache", "DraftOut", "VerifyOut", "config", "noise_table", "SrtError"]
+
+_DT = {torch.bfloat16: _lib.SRT_BF16, torch.float32: _lib.SRT_F32}
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None, dtype=None, name: str = "") -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    if not t.is_cuda:
+        raise SrtError(f"{name}: expected a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise SrtError(f"{name}: expected a contiguous tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise SrtError(f"{name}: expected {dtype}, got {t.dtype}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def config(vocab_size: int, max_prompts: int, max_depth: int, max_match_len: int,
+           budget_max: int, budget_base: int | None = None, slope_num: int = 0,
+           slope_den: int = 1, min_path_score: float = 0.0, node_capacity: int = 1 << 20,
+           hash_capacity: int | None = None, slot_capacity: int | None = None,
+           logits_dtype: torch.dtype = torch.bfloat16) -> SrtConfig:
+    if budget_base is None:
+        budget_base = budget_max
+    if hash_capacity is None:
+        hash_capacity = 1 << max(1, (2 * node_capacity - 1).bit_length())
+    if slot_capacity is None:
+        slot_capacity = 2 * node_capacity
+    return SrtConfig(vocab_size, max_prompts, max_depth, max_match_len, budget_max, budget_base,
+                     slope_num, slope_den, float(min_path_score), node_capacity, hash_capacity,
+                     slot_capacity, _DT[logits_dtype])
+
+
+@dataclass
+class DraftOut:
+    match_len: torch.Tensor      # [n] i32
+    draft_len: torch.Tensor      # [n] i32
+    draft_tok: torch.Tensor      # [n, Bmax] i32
+    draft_parent: torch.Tensor   # [n, Bmax] i32
+    draft_depth: torch.Tensor    # [n, Bmax] i32
+    draft_pos: torch.Tensor      # [n, Bmax] i32
+    draft_mask: torch.Tensor     # [n, Bmax] i64 (u64 bit patterns)
+    row_offsets: torch.Tensor    # [n+1] i64
+
+    @staticmethod
+    def empty(n: int, Bmax: int, device) -> "DraftOut":
+        i32 = dict(dtype=torch.int32, device=device)
+        return DraftOut(torch.empty(n, **i32), torch.empty(n, **i32), torch.empty(n, Bmax, **i32),
+                        torch.empty(n, Bmax, **i32), torch.empty(n, Bmax, **i32),
+                        torch.empty(n, Bmax, **i32),
+                        torch.empty(n, Bmax, dtype=torch.int64, device=device),
+                        torch.empty(n + 1, dtype=torch.int64, device=device))
+
+
+@dataclass
+class VerifyOut:
+    sampled: torch.Tensor         # [rows] i32
+    accept_len: torch.Tensor      # [n] i32
+    n_commit: torch.Tensor        # [n] i32
+    commit_tok: torch.Tensor      # [n, Bmax+1] i32
+    accepted_nodes: torch.Tensor  # [n, Bmax] i32
+    finished: torch.Tensor        # [n] u8
+
+    @staticmethod
+    def empty(n: int, rows: int, Bmax: int, device) -> "VerifyOut":
+        i32 = dict(dtype=torch.int32, device=device)
+        return VerifyOut(torch.empty(rows, **i32), torch.empty(n, **i32), torch.empty(n, **i32),
+                         torch.empty(n, Bmax + 1, **i32), torch.empty(n, Bmax, **i32),
+                         torch.empty(n, dtype=torch.uint8, device=device))
+
+
+class SrtCache:
+    """The per-prompt tree caches T_p of P prompts, resident in HBM."""
+
+    def __init__(self, cfg: SrtConfig, device: int | torch.device | None = None):
+        self.L = _lib.load()
+        if not torch.cuda.is_available():
+            raise SrtError("SRT needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self.cfg = cfg
+        self.V, self.P, self.Bmax = cfg.vocab_size, cfg.max_prompts, cfg.budget_max
+        self.logits_dtype = torch.bfloat16 if cfg.logits_dtype == _lib.SRT_BF16 else torch.float32
+        self._h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(self.L.srt_cache_create(ctypes.byref(cfg), _stream(), ctypes.byref(self._h)),
+                  "srt_cache_create")
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            with torch.cuda.device(self.device):
+                self.L.srt_cache_destroy(self._h, _stream())
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- the hot path -------------------------------------------------------
+    def insert(self, prompt_id, seq_tok, frm, to, floor=None, stats=None) -> None:
+        n = prompt_id.shape[0]
+        i32 = torch.int32
+        check(self.L.srt_insert(self._h, n, _ptr(prompt_id, i32, "prompt_id"),
+                                _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+                                _ptr(frm, i32, "from"), _ptr(to, i32, "to"),
+                                _ptr(floor, i32, "floor"), _ptr(stats, torch.int64, "stats"),
+                                _stream()), "srt_insert")
+
+    def draft(self, prompt_id, seq_tok, seq_len, pos_base=None, out: DraftOut | None = None
+              ) -> DraftOut:
+        n = prompt_id.shape[0]
+        if out is None:
+            out = DraftOut.empty(n, self.Bmax, seq_tok.device)
+        i32 = torch.int32
+        check(self.L.srt_draft(self._h, n, _ptr(prompt_id, i32, "prompt_id"),
+                               _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+                               _ptr(seq_len, i32, "seq_len"), _ptr(pos_base, i32, "pos_base"),
+                               _ptr(out.match_len, i32), _ptr(out.draft_len, i32),
+                               _ptr(out.draft_tok, i32), _ptr(out.draft_parent, i32),
+                               _ptr(out.draft_depth, i32), _ptr(out.draft_pos, i32),
+                               _ptr(out.draft_mask, torch.int64), _ptr(out.row_offsets, torch.int64),
+                               _stream()), "srt_draft")
+        return out
+
+    def verify(self, logits, d: DraftOut, seq_id, seed: int, seq_tok, seq_len, max_new,
+               temperature: float = 1.0, eos_id: int = -1, out: VerifyOut | None = None,
+               rows: int | None = None) -> VerifyOut:
+        """Mutates seq_tok / seq_len (appends the committed tokens)."""
+        n = seq_len.shape[0]
+        if logits.dtype != self.logits_dtype:
+            raise SrtError(f"logits dtype {logits.dtype} != cache's {self.logits_dtype}")
+        if logits.shape[-1] != self.V:
+            raise SrtError("logits row length != V")
+        if out is None:
+            out = VerifyOut.empty(n, logits.shape[0] if rows is None else rows, self.Bmax,
+                                  seq_tok.device)
+        i32 = torch.int32
+        check(self.L.srt_verify(self._h, n, _ptr(logits, None, "logits"),
+                                _ptr(d.row_offsets, torch.int64), _ptr(d.draft_len, i32),
+                                _ptr(d.draft_tok, i32), _ptr(d.draft_parent, i32),
+                                _ptr(d.draft_depth, i32), _ptr(seq_id, torch.int64, "seq_id"),
+                                ctypes.c_uint64(seed & (2 ** 64 - 1)), float(temperature),
+                                int(eos_id), _ptr(max_new, i32, "max_new"),
+                                _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+                                _ptr(seq_len, i32, "seq_len"), _ptr(out.sampled, i32),
+                                _ptr(out.accept_len, i32), _ptr(out.n_commit, i32),
+                                _ptr(out.commit_tok, i32), _ptr(out.accepted_nodes, i32),
+                                _ptr(out.finished, torch.uint8), _stream()), "srt_verify")
+        return out
+
+    # ---- test / inspection support -----------------------------------------
+    def sample_rows_reference(self, logits, d: DraftOut, seq_len, seq_id, seed: int,
+                              temperature: float = 1.0, out=None) -> torch.Tensor:
+        n = seq_len.shape[0]
+        if out is None:
+            out = torch.empty(logits.shape[0], dtype=torch.int32, device=logits.device)
+        check(self.L.srt_sample_rows_reference(
+            self._h, n, _ptr(logits, None, "logits"), _ptr(d.row_offsets, torch.int64),
+            _ptr(d.draft_depth, torch.int32), _ptr(seq_len, torch.int32),
+            _ptr(seq_id, torch.int64), ctypes.c_uint64(seed & (2 ** 64 - 1)), float(temperature),
+            _ptr(out, torch.int32), _stream()), "srt_sample_rows_reference")
+        return out
+
+    def status(self):
+        bits = ctypes.c_uint32(0)
+        st = SrtCacheStats()
+        r = self.L.srt_cache_status(self._h, ctypes.byref(bits), ctypes.byref(st), _stream())
+        if r not in (_lib.SRT_OK, _lib.SRT_ERR_DEVICE):
+            check(r, "srt_cache_status")
+        return int(bits.value), {k: int(getattr(st, k)) for k, _ in SrtCacheStats._fields_}
+
+    def clear_errors(self):
+        check(self.L.srt_cache_clear_errors(self._h, _stream()), "srt_cache_clear_errors")
+
+    def dump(self, prompt_id: int):
+        """Canonical preorder records [(token, count, n_children), ...] (blocking)."""
+        n = ctypes.c_int64(0)
+        check(self.L.srt_cache_dump(self._h, prompt_id, None, 0, ctypes.byref(n), _stream()),
+              "srt_cache_dump")
+        buf = (SrtDumpRecord * max(1, n.value))()
+        check(self.L.srt_cache_dump(self._h, prompt_id, buf, n.value, ctypes.byref(n), _stream()),
+              "srt_cache_dump")
+        return [(buf[i].token, int(buf[i].count), buf[i].n_children) for i in range(n.value)]
+
+
+def noise_table(device=None) -> torch.Tensor:
+    L = _lib.load()
+    out = torch.empty(1 << 23, dtype=torch.float32, device=device or "cuda")
+    check(L.srt_noise_table(_ptr(out, torch.float32, "out"), _stream()), "srt_noise_table")
+    return out
