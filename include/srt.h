@@ -34,9 +34,10 @@
  *
  * Data layout in HBM (owned by the cache): a node pool shared by
  * all prompts (node id p is the root of prompt p's tree T_p) as
- * structure-of-arrays (token, count, child count, first child block), an
- * open-addressing edge hash ((parent << 32) | token -> child id), and a pool of
- * child-id blocks (4, 4, 8, 16, 32, 32, ... slots) for coalesced enumeration.
+ * structure-of-arrays (token, count, child count, first child inline, first
+ * child block), an open-addressing edge hash ((parent << 32) | token -> child
+ * id), and a pool of child-id blocks (4, 4, 8, 16, 32, 32, ... slots) holding
+ * children 1.. for coalesced enumeration.
  */
 #ifndef SRT_H_
 #define SRT_H_
@@ -250,6 +251,32 @@ SRT_API srt_status srt_sample_rows_reference(srt_cache* cache, int32_t n, const 
                                      const int32_t* seq_len, const uint64_t* seq_id,
                                      uint64_t seed, float temperature, int32_t* sampled,
                                      void* stream);
+
+/*
+ * Per-kernel device timing (measurement support).  When enabled, every kernel
+ * launched by srt_insert / srt_draft / srt_verify is bracketed by a pair of
+ * CUDA events recorded on the caller's stream (up to `capacity` launches;
+ * capacity 0 disables).  srt_profile_read (BLOCKING) synchronises `stream`,
+ * returns the (kernel id, milliseconds) records in launch order into host_buf
+ * (HOST, capacity cap) and clears them.
+ */
+typedef enum {
+  SRT_K_INSERT_PLAN = 0,
+  SRT_K_INSERT_WALK = 1,
+  SRT_K_DRAFT = 2,
+  SRT_K_ROW_OFFSETS = 3,
+  SRT_K_SCAN = 4,
+  SRT_K_ACCEPT = 5
+} srt_kernel_id;
+
+typedef struct {
+  int32_t kernel; /* srt_kernel_id */
+  float ms;
+} srt_profile_record;
+
+SRT_API srt_status srt_profile_enable(srt_cache* cache, int64_t capacity);
+SRT_API srt_status srt_profile_read(srt_cache* cache, srt_profile_record* host_buf, int64_t cap,
+                                    int64_t* n_records, void* stream);
 
 #ifdef __cplusplus
 }

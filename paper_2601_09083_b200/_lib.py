@@ -21,7 +21,10 @@ SRT_BF16, SRT_F32 = 0, 1
 # Every symbol include/srt.h declares (tests check the export table).
 EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache_destroy",
            "srt_insert", "srt_draft", "srt_verify", "srt_cache_dump", "srt_cache_status",
-           "srt_cache_clear_errors", "srt_noise_table", "srt_sample_rows_reference"]
+           "srt_cache_clear_errors", "srt_noise_table", "srt_sample_rows_reference",
+           "srt_profile_enable", "srt_profile_read"]
+KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
+                5: "accept"}
 
 
 class SrtConfig(ctypes.Structure):
@@ -43,6 +46,10 @@ class SrtCacheStats(ctypes.Structure):
 class SrtDumpRecord(ctypes.Structure):
     _fields_ = [("token", ctypes.c_int32), ("n_children", ctypes.c_int32),
                 ("count", ctypes.c_uint64)]
+
+
+class SrtProfileRecord(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("ms", ctypes.c_float)]
 
 
 class SrtError(RuntimeError):
@@ -78,6 +85,9 @@ def load() -> ctypes.CDLL:
     L.srt_cache_clear_errors.argtypes = [vp, vp]
     L.srt_noise_table.argtypes = [vp, vp]
     L.srt_sample_rows_reference.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, f32, vp, vp]
+    L.srt_profile_enable.argtypes = [vp, i64]
+    L.srt_profile_read.argtypes = [vp, ctypes.POINTER(SrtProfileRecord), i64,
+                                   ctypes.POINTER(ctypes.c_int64), vp]
     for name in EXPORTS:
         if name not in ("srt_abi_version", "srt_error_string"):
             getattr(L, name).restype = ctypes.c_int

@@ -17,6 +17,10 @@ struct srt_cache {
   long long* scratch;   // insert work offsets, grown on demand
   int64_t scratch_cap;  // elements
   int device;
+  // per-kernel timing (srt_profile_enable)
+  std::vector<cudaEvent_t> ev;
+  std::vector<int32_t> kid;
+  int64_t prof_cap = 0, prof_n = 0;
 };
 
 namespace {
@@ -57,6 +61,18 @@ srt_status validate(const srt_config* c) {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Launch `fn` (returns cudaError_t), bracketed by timing events if profiling.
+template <class F>
+cudaError_t timed(srt_cache* c, int32_t kernel, cudaStream_t stream, F fn) {
+  if (c->prof_n >= c->prof_cap) return fn();
+  const int64_t i = c->prof_n++;
+  cudaEventRecord(c->ev[2 * i], stream);
+  cudaError_t e = fn();
+  cudaEventRecord(c->ev[2 * i + 1], stream);
+  c->kid[i] = kernel;
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -76,6 +92,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_cnt = off;     off = align_up(off + N * 4);
   const size_t o_nch = off;     off = align_up(off + N * 4);
   const size_t o_blk = off;     off = align_up(off + N * 4);
+  const size_t o_ch0 = off;     off = align_up(off + N * 4);
   const size_t o_hash = off;    off = align_up(off + H * sizeof(HashSlot));
   const size_t o_slots = off;   off = align_up(off + W * 4);
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
@@ -99,6 +116,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.cnt = (uint32_t*)(b + o_cnt);
   d.nchild = (uint32_t*)(b + o_nch);
   d.blk0 = (uint32_t*)(b + o_blk);
+  d.child0 = (uint32_t*)(b + o_ch0);
   d.hash = (HashSlot*)(b + o_hash);
   d.slots = (uint32_t*)(b + o_slots);
   d.ctr = (unsigned long long*)(b + o_ctr);
@@ -118,6 +136,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
 
 srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   if (!c) return SRT_OK;
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFreeAsync(c->pool, (cudaStream_t)stream);
   if (c->scratch) cudaFreeAsync(c->scratch, (cudaStream_t)stream);
   delete c;
@@ -137,9 +156,18 @@ srt_status srt_insert(srt_cache* c, int32_t n, const int32_t* prompt_id, const i
     SRT_CUDA(cudaMallocAsync(&c->scratch, cap * sizeof(long long), stream), "cudaMallocAsync(scratch)");
     c->scratch_cap = cap;
   }
-  SRT_CUDA(launch_insert(c->dev, n, prompt_id, seq_tok, stride, from, to, floor_, stats_dev,
-                         c->scratch, stream),
-           "insert kernels");
+  SRT_CUDA(timed(c, SRT_K_INSERT_PLAN, stream,
+                 [&] {
+                   return launch_insert_plan(c->dev, n, prompt_id, from, to, floor_, c->scratch,
+                                             stream);
+                 }),
+           "insert plan");
+  SRT_CUDA(timed(c, SRT_K_INSERT_WALK, stream,
+                 [&] {
+                   return launch_insert_walk(c->dev, n, prompt_id, seq_tok, stride, from, to,
+                                             floor_, stats_dev, c->scratch, stream);
+                 }),
+           "insert walk");
   return SRT_OK;
 }
 
@@ -153,10 +181,18 @@ srt_status srt_draft(srt_cache* c, int32_t n, const int32_t* prompt_id, const in
   if (n > 0 && (!prompt_id || !seq_tok || !seq_len || !match_len || !draft_len || !draft_tok ||
                 !draft_parent || !draft_depth || !draft_pos || !draft_mask))
     return SRT_ERR_INVALID_ARG;
-  SRT_CUDA(launch_draft(c->dev, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len,
-                        draft_len, draft_tok, draft_parent, draft_depth, draft_pos, draft_mask,
-                        row_offsets, (cudaStream_t)stream),
-           "draft kernels");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n > 0)
+    SRT_CUDA(timed(c, SRT_K_DRAFT, st,
+                   [&] {
+                     return launch_draft(c->dev, n, prompt_id, seq_tok, stride, seq_len, pos_base,
+                                         match_len, draft_len, draft_tok, draft_parent,
+                                         draft_depth, draft_pos, draft_mask, st);
+                   }),
+             "draft");
+  SRT_CUDA(timed(c, SRT_K_ROW_OFFSETS, st,
+                 [&] { return launch_row_offsets(n, draft_len, row_offsets, st); }),
+           "row offsets");
   return SRT_OK;
 }
 
@@ -180,8 +216,10 @@ srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t
                seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
                accepted_nodes, finished};
   cudaStream_t stream = (cudaStream_t)stream_;
-  SRT_CUDA(launch_scan(c->dev, a, false, stream), "verify scan");
-  SRT_CUDA(launch_accept(c->dev, a, stream), "verify accept");
+  SRT_CUDA(timed(c, SRT_K_SCAN, stream, [&] { return launch_scan(c->dev, a, false, stream); }),
+           "verify scan");
+  SRT_CUDA(timed(c, SRT_K_ACCEPT, stream, [&] { return launch_accept(c->dev, a, stream); }),
+           "verify accept");
   return SRT_OK;
 }
 
@@ -232,6 +270,32 @@ srt_status srt_cache_clear_errors(srt_cache* c, void* stream_) {
   h_status &= SRT_DEV_CAPACITY;
   SRT_CUDA(cudaMemcpyAsync(c->dev.status, &h_status, 4, cudaMemcpyHostToDevice, stream), "status");
   SRT_CUDA(cudaStreamSynchronize(stream), "status sync");
+  return SRT_OK;
+}
+
+srt_status srt_profile_enable(srt_cache* c, int64_t capacity) {
+  if (!c || capacity < 0) return SRT_ERR_INVALID_ARG;
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  c->ev.assign(2 * capacity, nullptr);
+  for (auto& e : c->ev) SRT_CUDA(cudaEventCreate(&e), "cudaEventCreate");
+  c->kid.assign(capacity, -1);
+  c->prof_cap = capacity;
+  c->prof_n = 0;
+  return SRT_OK;
+}
+
+srt_status srt_profile_read(srt_cache* c, srt_profile_record* host_buf, int64_t cap,
+                            int64_t* n_records, void* stream) {
+  if (!c || !n_records || cap < 0) return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "profile sync");
+  const int64_t n = c->prof_n;
+  for (int64_t i = 0; i < n && i < cap && host_buf; ++i) {
+    float ms = 0.f;
+    SRT_CUDA(cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]), "cudaEventElapsedTime");
+    host_buf[i] = srt_profile_record{c->kid[i], ms};
+  }
+  *n_records = n;
+  c->prof_n = 0;
   return SRT_OK;
 }
 

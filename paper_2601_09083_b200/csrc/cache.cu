@@ -5,6 +5,17 @@
 
 namespace srt {
 
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
 __global__ void k_init_counters(DevCache c) {
   c.ctr[0] = (unsigned long long)c.P;  // node ids 0..P-1 are the roots
   c.ctr[1] = 0;
@@ -17,6 +28,7 @@ cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
   if ((e = cudaMemsetAsync(c.cnt, 0, c.N * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.nchild, 0, c.N * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.blk0, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.child0, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.hash, 0xFF, c.H * sizeof(HashSlot), stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.slots, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
   k_init_counters<<<1, 1, 0, stream>>>(c);
@@ -73,8 +85,9 @@ __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, u
   const uint32_t u = frontier[f];
   const uint32_t F = c.nchild[u];
   const uint32_t b0 = c.blk0[u];
+  const uint32_t c0 = c.child0[u];
   for (uint32_t k = 0; k < F; ++k) {
-    const uint32_t ch = c.slots[child_slot_word(c, u, b0, k)];
+    const uint32_t ch = child_at(c, u, c0, b0, k);
     const unsigned int o = atomicAdd(out_n, 1u);
     out_node[o] = ch;
     out_parent[o] = f;

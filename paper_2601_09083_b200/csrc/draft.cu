@@ -112,12 +112,13 @@ __device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uin
   const uint32_t nch = c.nchild[u];
   if (nch == 0 || cap <= 0) return size;
   const uint32_t b0 = c.blk0[u];
+  const uint32_t c0 = c.child0[u];
   // pass 1: sibling sum (first 32 children kept in registers)
   uint32_t ch0 = 0, cnt0 = 0;
   int32_t tok0 = 0;
   unsigned long long sum = 0;
   for (uint32_t k = lane; k < nch; k += 32) {
-    const uint32_t ch = c.slots[child_slot_word(c, u, b0, k)];
+    const uint32_t ch = child_at(c, u, c0, b0, k);
     const uint32_t cc = c.cnt[ch];
     if (k < 32) {
       ch0 = ch;
@@ -137,7 +138,7 @@ __device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uin
       uint32_t ch = ch0, cc = cnt0;
       int32_t tk = tok0;
       if (kb > 0) {
-        ch = c.slots[child_slot_word(c, u, b0, k)];
+        ch = child_at(c, u, c0, b0, k);
         cc = c.cnt[ch];
         tk = c.tok[ch];
       }
@@ -299,15 +300,16 @@ cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
                          const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
                          int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
-                         int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
-                         cudaStream_t stream) {
-  if (n > 0) {
-    k_draft<<<(n + DRAFT_WARPS - 1) / DRAFT_WARPS, DRAFT_WARPS * 32, 0, stream>>>(
-        c, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len, draft_len, draft_tok,
-        draft_parent, draft_depth, draft_pos, draft_mask);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
+                         int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  k_draft<<<(n + DRAFT_WARPS - 1) / DRAFT_WARPS, DRAFT_WARPS * 32, 0, stream>>>(
+      c, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len, draft_len, draft_tok,
+      draft_parent, draft_depth, draft_pos, draft_mask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_offsets(int32_t n, const int32_t* draft_len, int64_t* row_offsets,
+                               cudaStream_t stream) {
   k_row_offsets<<<1, SCAN_THREADS, 0, stream>>>(n, draft_len, row_offsets);
   return cudaGetLastError();
 }

@@ -143,7 +143,12 @@ __device__ uint32_t wait_block(const DevCache& c, uint32_t u, uint32_t i) {
 
 // Append child id `ch` to node u's child blocks.
 __device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch) {
-  const uint32_t k = atomicAdd(&c.nchild[u], 1u);
+  const uint32_t k0 = atomicAdd(&c.nchild[u], 1u);
+  if (k0 == 0) {  // the first child lives inline in the node
+    c.child0[u] = ch;
+    return;
+  }
+  const uint32_t k = k0 - 1;
   const uint32_t i = blk_index(k);
   const uint32_t off = k - blk_start(i);
   uint32_t base;
@@ -250,22 +255,19 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
 
 }  // namespace
 
-cudaError_t launch_insert(const DevCache& c, int32_t n, const int32_t* prompt_id,
-                          const int32_t* seq_tok, int64_t stride, const int32_t* from,
-                          const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
-                          long long* scratch, cudaStream_t stream) {
+cudaError_t launch_insert_plan(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                               const int32_t* from, const int32_t* to, const int32_t* floor_,
+                               long long* scratch, cudaStream_t stream) {
   k_insert_plan<<<1, PLAN_THREADS, 0, stream>>>(c, n, prompt_id, from, to, floor_, scratch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  k_insert_walk<<<sms * 8, 256, 0, stream>>>(c, n, prompt_id, seq_tok, stride, from, to, floor_,
-                                               scratch, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                               const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                               const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
+                               const long long* scratch, cudaStream_t stream) {
+  k_insert_walk<<<num_sms() * 8, 256, 0, stream>>>(c, n, prompt_id, seq_tok, stride, from, to,
+                                                   floor_, scratch, stats);
   return cudaGetLastError();
 }
 

@@ -5,10 +5,11 @@
 //   tok[N]     i32  token labelling the edge into the node
 //   cnt[N]     u32  count(u) ("frequency statistics"; reading O1)
 //   nchild[N]  u32  number of children
-//   blk0[N]    u32  word offset of the node's first child block (NONE if none)
+//   child0[N]  u32  the first child, inline (most trie nodes have exactly one)
+//   blk0[N]    u32  word offset of the block holding children 1..4 (NONE if none)
 //   hash[H]    16 B open-addressing edge hash: key (parent << 32) | token -> child id;
 //                   keys (node << 32) | 0x80000000 | i -> word offset of child block i >= 1
-//   slots[W]   u32  child-id blocks of 4, 4, 8, 16, 32, 32, ... slots
+//   slots[W]   u32  child-id blocks for children 1.. : 4, 4, 8, 16, 32, 32, ... slots
 // Concurrency: insertion creates nodes with a CAS on the hash key and publishes
 // the value with a release store; counts are atomic adds, so the logical tree
 // (set of (path, count)) does not depend on scheduling.  Node ids do, but no
@@ -44,6 +45,7 @@ struct DevCache {
   int32_t* tok;
   uint32_t* cnt;
   uint32_t* nchild;
+  uint32_t* child0;
   uint32_t* blk0;
   HashSlot* hash;
   uint32_t* slots;
@@ -118,12 +120,15 @@ __device__ __forceinline__ uint32_t child_of(const DevCache& c, uint32_t u, int3
   return hash_find(c, edge_key(u, (uint32_t)tok));
 }
 
-// word offset of child slot k of node u (read-only kernels)
-__device__ __forceinline__ uint32_t child_slot_word(const DevCache& c, uint32_t u, uint32_t blk0,
-                                                    uint32_t k) {
-  uint32_t i = blk_index(k);
-  uint32_t base = (i == 0) ? blk0 : hash_find(c, block_key(u, i));
-  return base + (k - blk_start(i));
+// Child k of node u (read-only kernels).  Child 0 is inline; child k >= 1 is
+// slot k-1 of the block geometry above (block 0 via blk0, blocks >= 1 via hash).
+__device__ __forceinline__ uint32_t child_at(const DevCache& c, uint32_t u, uint32_t child0,
+                                             uint32_t blk0, uint32_t k) {
+  if (k == 0) return child0;
+  const uint32_t j = k - 1;
+  const uint32_t i = blk_index(j);
+  const uint32_t base = (i == 0) ? blk0 : hash_find(c, block_key(u, i));
+  return c.slots[base + (j - blk_start(i))];
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -138,16 +143,21 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream);
 cudaError_t launch_noise_bounds(const DevCache& c, cudaStream_t stream);
 cudaError_t launch_noise_table(float* out, cudaStream_t stream);
-cudaError_t launch_insert(const DevCache& c, int32_t n, const int32_t* prompt_id,
-                          const int32_t* seq_tok, int64_t stride, const int32_t* from,
-                          const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
-                          long long* scratch, cudaStream_t stream);
+int num_sms();
+cudaError_t launch_insert_plan(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                               const int32_t* from, const int32_t* to, const int32_t* floor_,
+                               long long* scratch, cudaStream_t stream);
+cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                               const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                               const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
+                               const long long* scratch, cudaStream_t stream);
 cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
                          const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
                          int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
-                         int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
-                         cudaStream_t stream);
+                         int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream);
+cudaError_t launch_row_offsets(int32_t n, const int32_t* draft_len, int64_t* row_offsets,
+                               cudaStream_t stream);
 struct VerifyArgs {
   int32_t n;
   const void* logits;

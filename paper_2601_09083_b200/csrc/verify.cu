@@ -372,17 +372,6 @@ __global__ void __launch_bounds__(ACC_WARPS * 32) k_accept(DevCache c, VerifyArg
   }
 }
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
 }  // namespace
 
 cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference,

@@ -192,6 +192,19 @@ class SrtCache:
             check(r, "srt_cache_status")
         return int(bits.value), {k: int(getattr(st, k)) for k, _ in SrtCacheStats._fields_}
 
+    def profile_enable(self, capacity: int) -> None:
+        check(self.L.srt_profile_enable(self._h, int(capacity)), "srt_profile_enable")
+
+    def profile_read(self):
+        """[(kernel name, ms), ...] for every timed launch since the last read (blocking)."""
+        n = ctypes.c_int64(0)
+        cap = 1 << 16
+        buf = (_lib.SrtProfileRecord * cap)()
+        check(self.L.srt_profile_read(self._h, buf, cap, ctypes.byref(n), _stream()),
+              "srt_profile_read")
+        return [(_lib.KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms))
+                for i in range(min(n.value, cap))]
+
     def clear_errors(self):
         check(self.L.srt_cache_clear_errors(self._h, _stream()), "srt_cache_clear_errors")
 
