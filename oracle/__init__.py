@@ -62,6 +62,8 @@ def lib():
         L.orc_gumbel_from_word.argtypes = [ctypes.c_uint32]
         L.orc_gumbel_from_word.restype = ctypes.c_float
         L.orc_noise_table.argtypes = [_f32p]
+        L.orc_row_noise.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
+                                    ctypes.c_int32, _f32p]
         L.orc_sample_row.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
                                      ctypes.c_uint64, ctypes.c_int32, ctypes.c_float,
                                      ctypes.POINTER(ctypes.c_int)]
@@ -115,6 +117,13 @@ def gumbel_from_word(w: int) -> np.float32:
 def noise_table() -> np.ndarray:
     out = np.empty(1 << 23, np.float32)
     lib().orc_noise_table(out)
+    return out
+
+
+def row_noise(V: int, seed: int, seq_id: int, pos: int) -> np.ndarray:
+    """The sampler's Gumbel noise g_v for every v of one row key (O11)."""
+    out = np.empty(V, np.float32)
+    lib().orc_row_noise(V, seed, seq_id, pos, out)
     return out
 
 

@@ -167,24 +167,76 @@ float load_logit(const void* logits, int dtype, int64_t idx) {
   return ((const float*)logits)[idx];
 }
 
+// u(w) = (2 (w >> 9) + 1) 2^-24, exact in f32, in [2^-24, 1 - 2^-24]
+float uniform_from_word(uint32_t w) {
+  return (float)(2u * (w >> 9) + 1u) * f32_from_bits(0x33800000u);
+}
+
+// The Gumbel noise g_v of every element of one row (reading O11: the
+// top-down construction of iid Gumbel variables, Maddison, Tarlow & Minka,
+// "A* Sampling", NeurIPS 2014, §3 "Gumbel processes").  The vocabulary is cut
+// into blocks of BLK = 64 consecutive tokens (the last may be shorter, n_b).
+// For block b, one Philox4x32-10 call with counter (0x80000000 | (b >> 1),
+// pos, seq_lo, seq_hi) gives two words (wa, wb) = words (0,1) for even b,
+// (2,3) for odd b:
+//   a_b  = -log_det(u(wa))              ~ Exp(1)
+//   E_b  = RN(a_b / n_b)                ~ Exp(n_b): the first arrival in the block
+//   G_b  = -log_det(E_b)                ~ Gumbel(log n_b): the block's MAX noise
+//   p_b  = (wb * n_b) >> 32             uniform position of that maximum
+// Every other element v of the block gets a Gumbel truncated below G_b:
+//   A_v  = -log_det(u(w_v)),  w_v = word (v & 3) of Philox(v >> 2, pos, seq_lo, seq_hi)
+//   g_v  = min(G_b, -log_det(RN(E_b + A_v)))      (= -log(e^{-G_b} + Exp(1)))
+// and g_{p_b} = G_b.  (In exact arithmetic g_v < G_b already; the min makes the
+// block bound g_v <= G_b hold under rounding too.)  All counters depend on
+// (seed, seq_id, pos, v) only, so rows at the same position share noise.
+constexpr int64_t BLK = 64;
+
+void row_noise(int64_t V, uint64_t seed, uint64_t seq_id, int32_t pos, float* g) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const uint32_t slo = (uint32_t)seq_id, shi = (uint32_t)(seq_id >> 32);
+  const int64_t nblk = (V + BLK - 1) / BLK;
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t v0 = b * BLK;
+    const uint32_t n = (uint32_t)std::min<int64_t>(BLK, V - v0);
+    uint32_t bctr[4] = {0x80000000u | (uint32_t)(b >> 1), (uint32_t)pos, slo, shi};
+    uint32_t bw[4];
+    philox4x32_10(bctr, key, bw);
+    const uint32_t wa = (b & 1) ? bw[2] : bw[0];
+    const uint32_t wb = (b & 1) ? bw[3] : bw[1];
+    const float a = -log_det(uniform_from_word(wa));
+    const float E = a / (float)n;
+    const float G = -log_det(E);
+    const uint32_t p = (uint32_t)(((uint64_t)wb * n) >> 32);
+    for (uint32_t j = 0; j < n; ++j) {
+      const int64_t v = v0 + j;
+      if (j == p) {
+        g[v] = G;
+        continue;
+      }
+      uint32_t ctr[4] = {(uint32_t)(v >> 2), (uint32_t)pos, slo, shi};
+      uint32_t out[4];
+      philox4x32_10(ctr, key, out);
+      const float A = -log_det(uniform_from_word(out[v & 3]));
+      const float Tv = E + A;
+      const float gv = -log_det(Tv);
+      g[v] = gv > G ? G : gv;
+    }
+  }
+}
+
 // One logits row -> the sampled token (reading O11, BJ:north_star part 4):
-//   tau = argmax_v  RN32( RN32(x_v / T) + g(seed, seq_id, pos, v) ),
+//   tau = argmax_v  RN32( RN32(x_v / T) + g_v ),   g_v from row_noise above,
 //   first (smallest) index on ties; NaN logits are not candidates (flagged);
 //   if there is no candidate at all the result is 0.
-// The Philox counter is (v>>2, pos, seq_lo, seq_hi), key (seed_lo, seed_hi),
-// and v uses word (v & 3) of the output.
 int32_t sample_row(const void* row, int dtype, int64_t V, uint64_t seed, uint64_t seq_id,
                    int32_t pos, float temperature, int* nan_seen) {
-  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  std::vector<float> noise((size_t)V);
+  row_noise(V, seed, seq_id, pos, noise.data());
   int32_t best = 0;
   float best_z = 0.0f;
   bool have = false;
   for (int64_t v = 0; v < V; ++v) {
-    uint32_t ctr[4] = {(uint32_t)(v >> 2), (uint32_t)pos, (uint32_t)seq_id,
-                       (uint32_t)(seq_id >> 32)};
-    uint32_t out[4];
-    philox4x32_10(ctr, key, out);
-    float g = gumbel_from_word(out[v & 3]);
+    const float g = noise[(size_t)v];
     float x = load_logit(row, dtype, v);
     if (std::isnan(x)) {
       *nan_seen = 1;
@@ -324,6 +376,11 @@ float orc_gumbel_from_word(uint32_t w) { return gumbel_from_word(w); }
 void orc_noise_table(float* out) {
 #pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < (1 << 23); ++r) out[r] = gumbel_from_word((uint32_t)r << 9);
+}
+
+// g_v for every v of one row key (the noise of the sampler; test support).
+void orc_row_noise(int64_t V, uint64_t seed, uint64_t seq_id, int32_t pos, float* g) {
+  row_noise(V, seed, seq_id, pos, g);
 }
 
 int32_t orc_sample_row(const void* row, int dtype, int64_t V, uint64_t seed, uint64_t seq_id,

@@ -16,6 +16,9 @@ struct srt_cache {
   void* pool;           // one allocation holding every array below
   long long* scratch;   // insert work offsets, grown on demand
   int64_t scratch_cap;  // elements
+  int2* rowinfo = nullptr;      // verify: per-row (sequence, position)
+  unsigned long long* result = nullptr;  // verify: per-row packed winner (pack_cand)
+  int64_t row_cap = 0;          // rows the two buffers above can hold
   int device;
   // per-kernel timing (srt_profile_enable)
   std::vector<cudaEvent_t> ev;
@@ -97,7 +100,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_slots = off;   off = align_up(off + W * 4);
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
   const size_t o_status = off;  off = align_up(off + 4);
-  const size_t o_gb = off;      off = align_up(off + (NOISE_BUCKETS + 1) * 4);
+  const size_t o_gb = off;      off = align_up(off + (2 * NOISE_BUCKETS + 1) * 4);
   srt_cache* c = new srt_cache();
   c->cfg = *cfg;
   cudaGetDevice(&c->device);
@@ -139,6 +142,8 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFreeAsync(c->pool, (cudaStream_t)stream);
   if (c->scratch) cudaFreeAsync(c->scratch, (cudaStream_t)stream);
+  if (c->rowinfo) cudaFreeAsync(c->rowinfo, (cudaStream_t)stream);
+  if (c->result) cudaFreeAsync(c->result, (cudaStream_t)stream);
   delete c;
   return SRT_OK;
 }
@@ -216,9 +221,22 @@ srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t
                seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
                accepted_nodes, finished};
   cudaStream_t stream = (cudaStream_t)stream_;
-  SRT_CUDA(timed(c, SRT_K_SCAN, stream, [&] { return launch_scan(c->dev, a, false, stream); }),
+  // rows <= n * (Bmax + 1): size the scratch without reading row_offsets back
+  const int64_t rows_max = (int64_t)n * (c->cfg.budget_max + 1);
+  if (c->row_cap < rows_max) {
+    if (c->rowinfo) SRT_CUDA(cudaFreeAsync(c->rowinfo, stream), "cudaFreeAsync(rowinfo)");
+    if (c->result) SRT_CUDA(cudaFreeAsync(c->result, stream), "cudaFreeAsync(result)");
+    const int64_t cap = std::max<int64_t>(rows_max, 4096);
+    SRT_CUDA(cudaMallocAsync(&c->rowinfo, cap * sizeof(int2), stream), "cudaMallocAsync(rowinfo)");
+    SRT_CUDA(cudaMallocAsync(&c->result, cap * sizeof(unsigned long long), stream),
+             "cudaMallocAsync(result)");
+    c->row_cap = cap;
+  }
+  SRT_CUDA(timed(c, SRT_K_SCAN, stream,
+                 [&] { return launch_scan(c->dev, a, false, c->rowinfo, c->result, stream); }),
            "verify scan");
-  SRT_CUDA(timed(c, SRT_K_ACCEPT, stream, [&] { return launch_accept(c->dev, a, stream); }),
+  SRT_CUDA(timed(c, SRT_K_ACCEPT, stream,
+                 [&] { return launch_accept(c->dev, a, c->result, stream); }),
            "verify accept");
   return SRT_OK;
 }
@@ -238,7 +256,8 @@ srt_status srt_sample_rows_reference(srt_cache* c, int32_t n, const void* logits
   a.draft_depth = draft_depth; a.seq_id = seq_id; a.seed = seed; a.temperature = temperature;
   a.seq_len = seq_len ? const_cast<int32_t*>(seq_len) : nullptr;
   a.sampled = sampled;
-  SRT_CUDA(launch_scan(c->dev, a, true, (cudaStream_t)stream), "reference scan");
+  SRT_CUDA(launch_scan(c->dev, a, true, nullptr, nullptr, (cudaStream_t)stream),
+           "reference scan");
   return SRT_OK;
 }
 

@@ -69,6 +69,52 @@ __device__ __forceinline__ float gumbel_of_r(uint32_t r) {
   return -log_det(-log_det(u));
 }
 
+// ---- the top-down Gumbel construction of the sampler (O11) ------
+// Blocks of NOISE_BLK = 64 tokens; block b's maximum noise is drawn first from
+// one Philox call shared by blocks 2m and 2m+1, the others are truncated below.
+constexpr int NOISE_BLK = 64;
+
+// tokens in block b of a V-token row (0 past the end)
+__device__ __forceinline__ int block_len(int64_t V, int64_t b) {
+  const int64_t rem = V - b * NOISE_BLK;
+  return rem <= 0 ? 0 : (rem < NOISE_BLK ? (int)rem : NOISE_BLK);
+}
+
+__device__ __forceinline__ float uniform_of_word(uint32_t w) {
+  return __fmul_rn((float)(2u * (w >> 9) + 1u), __uint_as_float(0x33800000u));  // exact
+}
+
+// Philox words (wa, wb) of block b
+__device__ __forceinline__ void block_words(uint32_t b, uint32_t pos, uint32_t s_lo, uint32_t s_hi,
+                                            uint32_t k0, uint32_t k1, uint32_t& wa,
+                                            uint32_t& wb) {
+  const Philox4 w = philox4x32_10(0x80000000u | (b >> 1), pos, s_lo, s_hi, k0, k1);
+  wa = (b & 1) ? w.z : w.x;
+  wb = (b & 1) ? w.w : w.y;
+}
+
+struct BlockNoise {
+  float E;     // e^{-G}: the block's first "arrival" ~ Exp(n)/1
+  float G;     // the block's maximum noise
+  uint32_t p;  // its position in the block
+};
+
+__device__ __forceinline__ BlockNoise block_noise(uint32_t wa, uint32_t wb, uint32_t n) {
+  const float a = -log_det(uniform_of_word(wa));
+  const float E = __fdiv_rn(a, (float)n);
+  const float G = -log_det(E);
+  const uint32_t p = __umulhi(wb, n);
+  return BlockNoise{E, G, p};
+}
+
+// g_v for element v at offset j of its block (j != bn.p):
+// min(G, -log_det(RN(E + A_v))), A_v = -log_det(u(word (v&3) of Philox(v>>2, ...)))
+__device__ __forceinline__ float element_noise_from_word(uint32_t w, const BlockNoise& bn) {
+  const float A = -log_det(uniform_of_word(w));
+  const float g = -log_det(__fadd_rn(bn.E, A));
+  return g > bn.G ? bn.G : g;
+}
+
 // z = RN(RN(x / T) + g); T == 1 skips the division (O11).
 __device__ __forceinline__ float perturbed(float x, float g, float temperature, bool unit_t) {
   const float xs = unit_t ? x : __fdiv_rn(x, temperature);

@@ -1,0 +1,501 @@
+// scan.cu — the roofline kernel of srt_verify: the exact Gumbel-max sample of
+// every drafted logits row (BJ:north_star part 4; O11 and §5).
+//
+// The noise is the top-down construction of O11: per block of 64 tokens the
+// block's MAXIMUM noise G_b is drawn first (one Philox call per two blocks),
+// the other 63 are Gumbels truncated below it.  So
+//     U_b = RN(RN(max_{v in b} x_v / T) + G_b)  >=  z_v  for every v in b,
+// and with the bucket bound G_b <= TAB[r_b >> 13] (the max of G over the
+// block word's bucket, enumerated over all 2^23 words at cache creation) the
+// block bound needs no logarithm at all.  A block can hold the row's winner
+// only if U_b >= M for M any ACHIEVED z of the row; M = z(i*) of the row's
+// largest logit is exact and strong.  Everything else is streaming.
+//
+// Persistent, warp-specialised kernel; one CTA per SM owns whole rows
+// (rows b, b+G, b+2G, ...), so no row ever waits on another SM:
+//  * producer warp: 1-D TMA bulk copies (cp.async.bulk + mbarrier) stream each
+//    row through a ring of NST 32 KB shared-memory stages (~7.4 TB/s
+//    read-only on this B200 in isolation, tools/stream_probe.cu);
+//  * stream warps: each lane takes a PAIR of blocks (128 logits) per step —
+//    packed bf16x2 maxima from conflict-free swizzled 16-byte shared loads,
+//    one Philox call for the pair, the bucket-bounded U_b into the row summary
+//    (4 B per block), and the row's largest logit;
+//  * tail warps, one row behind: M = z(i*) exactly, then every block with
+//    U_b >= M (the head's block and a few others) is evaluated element by
+//    element from L2 with the exact noise; each warp's best (z, v) goes to the
+//    row's packed atomicMax word (larger z, then smaller v).
+// Nothing observable depends on scheduling: the result is the argmax of the
+// plain definition (k_scan_reference; the tests compare both bit for bit).
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_bf16.h>
+
+#include "noise.cuh"
+#include "srt_internal.cuh"
+
+namespace srt {
+
+namespace {
+
+// ---- PTX helpers: mbarriers, 1-D TMA bulk copy ------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ __nv_bfloat162 as_bf2(uint32_t w) {
+  return *reinterpret_cast<const __nv_bfloat162*>(&w);
+}
+// order-preserving key of a non-NaN float (never 0, which means "none")
+__device__ __forceinline__ uint32_t fkey(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_value(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+template <int DT>
+__device__ __forceinline__ float load_x(const unsigned char* rowp, int64_t v) {
+  if (DT == SRT_BF16) return __uint_as_float((uint32_t)((const uint16_t*)rowp)[v] << 16);
+  return ((const float*)rowp)[v];
+}
+
+// NaN-propagating max of the 16-byte vectors of one block held in shared
+// memory: vector index (k + rot) & (NV - 1) at step k, so the 8 lanes of an
+// LDS.128 phase hit distinct bank groups.
+template <int DT>
+__device__ __forceinline__ float block_max_nan(const unsigned char* blk, int rot) {
+  constexpr int NV = DT == SRT_BF16 ? 8 : 16;  // 16-byte vectors per 64-token block
+  const uint4* v = reinterpret_cast<const uint4*>(blk);
+  if (DT == SRT_BF16) {
+    __nv_bfloat162 m0 = as_bf2(0xFF80FF80u), m1 = m0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const uint4 q = v[(k + rot) & (NV - 1)];
+      m0 = __hmax2_nan(m0, __hmax2_nan(as_bf2(q.x), as_bf2(q.y)));
+      m1 = __hmax2_nan(m1, __hmax2_nan(as_bf2(q.z), as_bf2(q.w)));
+    }
+    const __nv_bfloat162 m = __hmax2_nan(m0, m1);
+    return max_nan(__low2float(m), __high2float(m));
+  } else {
+    float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const uint4 q = v[(k + rot) & (NV - 1)];
+      m0 = max_nan(m0, max_nan(__uint_as_float(q.x), __uint_as_float(q.y)));
+      m1 = max_nan(m1, max_nan(__uint_as_float(q.z), __uint_as_float(q.w)));
+    }
+    return max_nan(m0, m1);
+  }
+}
+
+// non-NaN max of the first n elements of a block in shared memory (-inf if none)
+template <int DT>
+__device__ __forceinline__ float block_max_scalar(const unsigned char* blk, int n) {
+  float m = -INFINITY;
+  for (int j = 0; j < n; ++j) {
+    const float x = load_x<DT>(blk, j);
+    if (x > m) m = x;
+  }
+  return m;
+}
+
+constexpr uint32_t CHUNK = 32768;  // TMA chunk (bytes); a multiple of a block pair
+
+struct ScanParams {
+  const void* logits;
+  const int2* rowinfo;         // per row: (seq, pos)
+  const int64_t* total;        // -> row_offsets[n]
+  const uint64_t* seq_id;
+  uint64_t seed;
+  float temperature;
+  unsigned long long* result;  // per row: packed best candidate (atomicMax)
+  int32_t V;
+  int32_t nblk;                // ceil(V / 64)
+  uint32_t sum_bytes;          // row summary bytes (nblk floats, 128-aligned)
+  uint32_t debug;              // development only (SRT_SCAN_DEBUG=8 prints the launch)
+};
+
+// Warp roles: warp 0 = producer, warps 1..NSW = stream, the rest = tail.
+template <int DT, int NSW, int NT, int NST, int NS>
+__global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c, ScanParams a) {
+  constexpr int ESZ = DT == SRT_BF16 ? 2 : 4;
+  constexpr int BLKB = NOISE_BLK * ESZ;  // bytes per block
+  constexpr int PAIRB = 2 * BLKB;
+  constexpr int PAIRS_PER_CHUNK = CHUNK / PAIRB;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* ring = smem;                                            // [NST][CHUNK]
+  unsigned char* sums = ring + NST * CHUNK;                              // [NS][sum_bytes]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sums + NS * a.sum_bytes);
+  uint64_t* ring_full = bars;                                            // [NST]
+  uint64_t* ring_empty = ring_full + NST;                                // [NST]
+  uint64_t* sum_ready = ring_empty + NST;                                // [NS]
+  uint64_t* sum_free = sum_ready + NS;                                   // [NS]
+  unsigned long long* p1key = reinterpret_cast<unsigned long long*>(sum_free + NS);  // [NS]
+  unsigned long long* rowhdr = p1key + NS;                               // [NS]
+  uint32_t* p1cnt = reinterpret_cast<uint32_t*>(rowhdr + NS);            // [NS]
+  float* tab = reinterpret_cast<float*>(p1cnt + ((NS + 3) & ~3));        // [1024]
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t total = *a.total;
+  const int64_t row_bytes = (int64_t)a.V * ESZ;
+  const uint32_t nch = (uint32_t)((row_bytes + CHUNK - 1) / CHUNK);
+  const float T = a.temperature;
+  const bool unit_t = T == 1.0f;
+  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+
+  for (int i = tid; i < NOISE_BUCKETS; i += blockDim.x) tab[i] = c.gbound[i];
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&ring_full[s], 1);
+      mbar_init(&ring_empty[s], NSW);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sum_ready[s], 1);
+      mbar_init(&sum_free[s], NT);
+      p1key[s] = 0;
+      p1cnt[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (wid == 0) {
+    // ===================== producer: the rows' chunks into the ring ========
+    if (lane == 0) {
+      uint64_t kc = 0;
+      for (int64_t row = blockIdx.x; row < total; row += gridDim.x) {
+        const char* base = (const char*)a.logits + row * row_bytes;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
+          const int s = (int)(kc % NST);
+          const uint32_t use = (uint32_t)(kc / NST);
+          if (use > 0) mbar_wait(&ring_empty[s], (use - 1) & 1);
+          const int64_t left = row_bytes - (int64_t)ch * CHUNK;
+          const uint32_t nb = (uint32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
+          mbar_arrive_expect_tx(&ring_full[s], nb);
+          tma_load_1d(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  if (wid <= NSW) {
+    // ===================== stream: block bounds U_b, the row's max logit ====
+    const int w = wid - 1;
+    uint64_t kc = 0;
+    int64_t u = 0;
+    for (int64_t row = blockIdx.x; row < total; row += gridDim.x, ++u) {
+      const int sb = (int)(u % NS);
+      const uint32_t suse = (uint32_t)(u / NS);
+      if (suse > 0) mbar_wait(&sum_free[sb], (suse - 1) & 1);
+      float* U = reinterpret_cast<float*>(sums + sb * a.sum_bytes);
+      const int2 ri = a.rowinfo[row];
+      const uint64_t sid = a.seq_id[ri.x];
+      const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+      float tmax = -INFINITY;
+      uint32_t tblk = 0xFFFFFFFFu;
+      bool nan = false;
+      for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
+        const int s = (int)(kc % NST);
+        mbar_wait(&ring_full[s], (uint32_t)((kc / NST) & 1));
+        const int64_t left = row_bytes - (int64_t)ch * CHUNK;
+        const int32_t nb = (int32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
+        const int32_t npairs = (nb + PAIRB - 1) / PAIRB;
+        const unsigned char* st = ring + s * CHUNK;
+        for (int32_t pi = w * 32 + lane; pi < npairs; pi += NSW * 32) {
+          const uint32_t gp = ch * PAIRS_PER_CHUNK + (uint32_t)pi;  // pair index in the row
+          const int64_t e0 = (int64_t)gp * 2 * NOISE_BLK;             // first element
+          const int nA = block_len(a.V, 2 * (int64_t)gp);
+          const int nB = block_len(a.V, 2 * (int64_t)gp + 1);
+          (void)e0;
+          const unsigned char* pa = st + pi * PAIRB;
+          float mA, mB;
+          if (nA == NOISE_BLK && nB == NOISE_BLK) {
+            mA = block_max_nan<DT>(pa, lane);
+            mB = block_max_nan<DT>(pa + BLKB, lane);
+            if (mA != mA) { nan = true; mA = block_max_scalar<DT>(pa, NOISE_BLK); }
+            if (mB != mB) { nan = true; mB = block_max_scalar<DT>(pa + BLKB, NOISE_BLK); }
+          } else {  // the row's last, partial pair
+            mA = block_max_scalar<DT>(pa, nA);
+            mB = nB ? block_max_scalar<DT>(pa + BLKB, nB) : -INFINITY;
+            for (int j = 0; j < nA; ++j) nan |= load_x<DT>(pa, j) != load_x<DT>(pa, j);
+            for (int j = 0; j < nB; ++j)
+              nan |= load_x<DT>(pa + BLKB, j) != load_x<DT>(pa + BLKB, j);
+          }
+          const Philox4 pw = philox4x32_10(0x80000000u | gp, pos, s_lo, s_hi, k0, k1);
+          const float xa = unit_t ? mA : __fdiv_rn(mA, T);
+          float GA;
+          if (nA == NOISE_BLK) GA = tab[pw.x >> 22];  // bucket bound of G_b (r >> 13)
+          else GA = block_noise(pw.x, pw.y, (uint32_t)nA).G;
+          U[2 * gp] = __fadd_rn(xa, GA);
+          if (mA > tmax || (tblk == 0xFFFFFFFFu && mA == mA)) { tmax = mA; tblk = 2 * gp; }
+          if (nB) {
+            const float xb = unit_t ? mB : __fdiv_rn(mB, T);
+            float GB;
+            if (nB == NOISE_BLK) GB = tab[pw.z >> 22];
+            else GB = block_noise(pw.z, pw.w, (uint32_t)nB).G;
+            U[2 * gp + 1] = __fadd_rn(xb, GB);
+            if (mB > tmax) { tmax = mB; tblk = 2 * gp + 1; }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring_empty[s]);
+      }
+      if (__any_sync(0xffffffffu, nan) && lane == 0) set_error(c, SRT_DEV_NONFINITE_LOGIT);
+      // (max logit desc, block asc) -> the CTA's packed row header
+      const uint32_t mykey = tblk == 0xFFFFFFFFu ? 0u : fkey(tmax);
+      const uint32_t wkey = __reduce_max_sync(0xffffffffu, mykey);
+      const uint32_t wblk =
+          __reduce_min_sync(0xffffffffu, (wkey && mykey == wkey) ? tblk : 0xFFFFFFFFu);
+      __syncwarp();
+      if (lane == 0) {
+        if (wkey) atomicMax(&p1key[sb], ((unsigned long long)wkey << 32) | (0xFFFFFFFFu - wblk));
+        __threadfence_block();
+        if (atomicAdd(&p1cnt[sb], 1u) == NSW - 1) {  // the last stream warp publishes
+          rowhdr[sb] = atomicExch(&p1key[sb], 0ull);
+          p1cnt[sb] = 0;
+          mbar_arrive(&sum_ready[sb]);  // release: the summary is complete
+        }
+      }
+    }
+    return;
+  }
+
+  // ======================= tail: M, then the surviving blocks ==============
+  const int t = wid - 1 - NSW;
+  int64_t u = 0;
+  for (int64_t row = blockIdx.x; row < total; row += gridDim.x, ++u) {
+    const int sb = (int)(u % NS);
+    mbar_wait(&sum_ready[sb], (uint32_t)((u / NS) & 1));
+    const unsigned long long hdr = rowhdr[sb];
+    const float* U = reinterpret_cast<const float*>(sums + sb * a.sum_bytes);
+    float bz = -INFINITY;
+    int32_t bv = INT_MAX;
+    if (hdr != 0) {  // else every logit of the row is NaN: no candidate
+      const int2 ri = a.rowinfo[row];
+      const uint64_t sid = a.seq_id[ri.x];
+      const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+      const unsigned char* rowp = (const unsigned char*)a.logits + row * row_bytes;
+      const float X = key_value((uint32_t)(hdr >> 32));
+      const uint32_t bX = 0xFFFFFFFFu - (uint32_t)hdr;
+      // i* = the first element of block bX equal to X; M = z(i*), exactly
+      const int nX = block_len(a.V, bX);
+      const int64_t vX = (int64_t)bX * NOISE_BLK;
+      uint32_t first = 0xFFFFFFFFu;
+      if (2 * lane < nX && load_x<DT>(rowp, vX + 2 * lane) == X) first = 2 * lane;
+      else if (2 * lane + 1 < nX && load_x<DT>(rowp, vX + 2 * lane + 1) == X) first = 2 * lane + 1;
+      const uint32_t jstar = __reduce_min_sync(0xffffffffu, first);
+      float M;
+      {
+        uint32_t wa, wb;
+        block_words(bX, pos, s_lo, s_hi, k0, k1, wa, wb);
+        const BlockNoise bn = block_noise(wa, wb, (uint32_t)nX);
+        float g = bn.G;
+        const int64_t vs = vX + jstar;
+        if (jstar != bn.p) {
+          const Philox4 pw = philox4x32_10((uint32_t)(vs >> 2), pos, s_lo, s_hi, k0, k1);
+          const uint32_t k = (uint32_t)(vs & 3);
+          g = element_noise_from_word(k == 0 ? pw.x : k == 1 ? pw.y : k == 2 ? pw.z : pw.w, bn);
+        }
+        M = perturbed(X, g, T, unit_t);
+      }
+      // every block whose bound reaches M is evaluated exactly by the whole
+      // warp (lane = 2 consecutive tokens, coalesced), BATCH blocks at a time
+      // so their L2 loads overlap
+      constexpr int BATCH = 4;
+      const int32_t nchunk = (a.nblk + 31) / 32;
+      for (int32_t cb = t; cb < nchunk; cb += NT) {
+        const int32_t b = cb * 32 + lane;
+        unsigned surv = __ballot_sync(0xffffffffu, b < a.nblk && U[b] >= M);
+        while (surv) {
+          int32_t bb[BATCH];
+          float2 xx[BATCH];
+#pragma unroll
+          for (int i = 0; i < BATCH; ++i) {  // pop up to BATCH blocks, issue their loads
+            bb[i] = -1;
+            if (surv) {
+              bb[i] = cb * 32 + __ffs(surv) - 1;
+              surv &= surv - 1;
+              const int n = block_len(a.V, bb[i]);
+              const int64_t v = (int64_t)bb[i] * NOISE_BLK + 2 * lane;
+              xx[i].x = 2 * lane < n ? load_x<DT>(rowp, v) : NAN;
+              xx[i].y = 2 * lane + 1 < n ? load_x<DT>(rowp, v + 1) : NAN;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < BATCH; ++i) {
+            if (bb[i] < 0) continue;
+            const int n = block_len(a.V, bb[i]);
+            uint32_t wa, wb;
+            block_words((uint32_t)bb[i], pos, s_lo, s_hi, k0, k1, wa, wb);
+            const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+            const float xs0 = unit_t ? xx[i].x : __fdiv_rn(xx[i].x, T);
+            const float xs1 = unit_t ? xx[i].y : __fdiv_rn(xx[i].y, T);
+            // g_v <= G_b: skip a token if even the block maximum cannot reach M
+            const bool n0 = __fadd_rn(xs0, bn.G) >= M, n1 = __fadd_rn(xs1, bn.G) >= M;
+            if (!(n0 || n1)) continue;  // (NaN fails both tests)
+            const int64_t v = (int64_t)bb[i] * NOISE_BLK + 2 * lane;
+            const Philox4 pw = philox4x32_10((uint32_t)(v >> 2), pos, s_lo, s_hi, k0, k1);
+            const bool hi = (lane & 1) != 0;  // tokens 2l, 2l+1 are words 0,1 or 2,3
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              if (!(k ? n1 : n0)) continue;
+              const uint32_t j = 2 * lane + k;
+              const uint32_t wd = hi ? (k ? pw.w : pw.z) : (k ? pw.y : pw.x);
+              const float g = j == bn.p ? bn.G : element_noise_from_word(wd, bn);
+              const float z = __fadd_rn(k ? xs1 : xs0, g);
+              if (cand_better(z, (int32_t)(v + k), bz, bv)) {
+                bz = z;
+                bv = (int32_t)(v + k);
+                M = fmaxf(M, z);
+              }
+            }
+          }
+        }
+      }
+    }
+    const unsigned long long mine = bv == INT_MAX ? 0ull : pack_cand(bz, bv);
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(mine >> 32));
+    const uint32_t lo32 =
+        __reduce_max_sync(0xffffffffu, (uint32_t)(mine >> 32) == hi ? (uint32_t)mine : 0u);
+    const unsigned long long wbest = ((unsigned long long)hi << 32) | lo32;
+    __syncwarp();
+    if (lane == 0) {
+      if (wbest) atomicMax(&a.result[row], wbest);
+      mbar_arrive(&sum_free[sb]);
+    }
+  }
+}
+
+// per row: (sequence, position) — rows of sequence s are [row_offsets[s],
+// row_offsets[s+1]); also clears the row's packed result.
+__global__ void k_rowinfo(VerifyArgs a, int32_t Bmax, int2* rowinfo,
+                          unsigned long long* result) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.n) return;
+  const int64_t r0 = a.row_offsets[s];
+  const int32_t t = a.seq_len[s];
+  const int32_t nd = (int32_t)(a.row_offsets[s + 1] - r0 - 1);
+  rowinfo[r0] = make_int2(s, t);
+  result[r0] = 0;
+  for (int32_t i = 0; i < nd; ++i) {
+    rowinfo[r0 + 1 + i] = make_int2(s, t + a.draft_depth[(int64_t)s * Bmax + i]);
+    result[r0 + 1 + i] = 0;
+  }
+}
+
+template <int DT, int NSW, int NT, int NST, int NS>
+cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
+  constexpr int THREADS = (1 + NSW + NT) * 32;
+  const size_t smem = (size_t)NST * CHUNK + (size_t)NS * p.sum_bytes +
+                      (2 * NST + 2 * NS) * 8 + 2 * NS * 8 + ((NS + 3) & ~3) * 4 +
+                      NOISE_BUCKETS * 4;
+  auto kern = k_scan_rows<DT, NSW, NT, NST, NS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  static int blocks = 0;
+  if (!blocks) {
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+    if (e != cudaSuccess || per_sm <= 0) per_sm = 1;
+    blocks = per_sm * num_sms();
+    if (p.debug & 8)
+      fprintf(stderr, "[srt scan] rows: NSW=%d NT=%d NST=%d NS=%d smem=%zu -> %d CTAs\n", NSW,
+              NT, NST, NS, smem, blocks);
+  }
+  k_scan_rows<DT, NSW, NT, NST, NS><<<blocks, THREADS, smem, stream>>>(c, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// The rows kernel serves every V whose rows are 16-byte multiples (TMA) and
+// whose block summaries fit in shared memory; the rest takes the reference.
+int scan_cluster_size(int32_t V, int dtype) {
+  if ((int64_t)V * (dtype == SRT_BF16 ? 2 : 4) % 16) return 0;
+  const int64_t nblk = ((int64_t)V + NOISE_BLK - 1) / NOISE_BLK;
+  return nblk * 4 <= 16 * 1024 ? 1 : 0;
+}
+
+cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
+                                unsigned long long* result, cudaStream_t stream) {
+  if (!scan_cluster_size(c.V, a.dtype)) return cudaErrorInvalidValue;
+  k_rowinfo<<<(a.n + 127) / 128, 128, 0, stream>>>(a, c.Bmax, rowinfo, result);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ScanParams p;
+  p.logits = a.logits;
+  p.rowinfo = rowinfo;
+  p.total = a.row_offsets + a.n;
+  p.seq_id = a.seq_id;
+  p.seed = a.seed;
+  p.temperature = a.temperature;
+  p.result = result;
+  p.V = c.V;
+  p.nblk = (c.V + NOISE_BLK - 1) / NOISE_BLK;
+  p.sum_bytes = (uint32_t)(((int64_t)p.nblk * 4 + 127) / 128 * 128);
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* s = getenv("SRT_SCAN_DEBUG");
+    dbg = s ? atoi(s) : 0;
+  }
+  p.debug = (uint32_t)dbg;
+  static int nsw = -1, nt = -1;
+  if (nsw < 0) {  // SRT_SCAN_ROWS="NSW,NT" picks another instantiated split (dev knob)
+    nsw = 4;
+    nt = 12;
+    if (const char* s = getenv("SRT_SCAN_ROWS")) {
+      int x = 0, y = 0;
+      if (sscanf(s, "%d,%d", &x, &y) == 2) { nsw = x; nt = y; }
+    }
+  }
+#define SRT_ROWS_CASE(A, B)                                                      \
+  if (nsw == A && nt == B)                                                       \
+    return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, A, B, 4, 4>(c, p, stream) \
+                               : launch_rows<SRT_F32, A, B, 4, 4>(c, p, stream);
+  SRT_ROWS_CASE(4, 8)
+  SRT_ROWS_CASE(6, 8)
+  SRT_ROWS_CASE(6, 10)
+  SRT_ROWS_CASE(8, 8)
+#undef SRT_ROWS_CASE
+  return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, 4, 12, 4, 4>(c, p, stream)
+                             : launch_rows<SRT_F32, 4, 12, 4, 4>(c, p, stream);
+}
+
+}  // namespace srt

@@ -51,8 +51,25 @@ struct DevCache {
   uint32_t* slots;
   unsigned long long* ctr;  // [0] next node id, [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
-  float* gbound;            // [NOISE_BUCKETS] bucket maxima, [NOISE_BUCKETS] = global max
+  float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima
 };
+
+// Candidate (z, v) packed so that a larger u64 is the better candidate under
+// "larger z, then smaller v" (first maximum): order-preserving float key in the
+// high word (-0 folded onto +0, which compare equal), ~v in the low word.
+// 0 is "no candidate".  z must not be NaN.
+__device__ __forceinline__ unsigned long long pack_cand(float z, int32_t v) {
+  uint32_t b = __float_as_uint(z == 0.0f ? 0.0f : z);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((unsigned long long)b << 32) | (0xFFFFFFFFu - (uint32_t)v);
+}
+__device__ __forceinline__ int32_t unpack_index(unsigned long long k) {
+  return k ? (int32_t)(0xFFFFFFFFu - (uint32_t)k) : 0;
+}
+__device__ __forceinline__ float unpack_value(unsigned long long k) {
+  const uint32_t b = (uint32_t)(k >> 32);
+  return __uint_as_float((b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b);
+}
 
 // ---------------------------------------------------------------------------
 // memory-model helpers (gpu scope; L1 is not coherent, so polled words use
@@ -182,9 +199,15 @@ struct VerifyArgs {
   int32_t* accepted_nodes;
   uint8_t* finished;
 };
-cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference,
-                        cudaStream_t stream);
-cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, cudaStream_t stream);
+int scan_cluster_size(int32_t V, int dtype);
+cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
+                                unsigned long long* result, cudaStream_t stream);
+// reference = the unpruned kernel writing sampled[] directly; otherwise the
+// product scan writing each row's packed winner (pack_cand) to result[].
+cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference, int2* rowinfo,
+                        unsigned long long* result, cudaStream_t stream);
+cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, const unsigned long long* result,
+                          cudaStream_t stream);
 cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
                               uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,
                               uint32_t* out_cnt, uint32_t* out_nchild, unsigned int* out_n,

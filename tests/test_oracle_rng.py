@@ -87,23 +87,76 @@ def test_noise_table_range_and_monotone(orc):
     assert abs(g[-1] - (-np.log(-np.log(u_hi)))) < 2e-5
 
 
-def test_gumbel_max_matches_softmax(orc):
-    """P9: argmax(x + g) ~ softmax(x).  16-way row, 40k independent keys."""
-    x = np.array([0.0, 1.0, 2.0, -1.0, 0.5, 3.0, -2.0, 1.5,
-                  0.25, -0.5, 2.5, 0.0, -3.0, 1.0, 0.75, 2.0], np.float32)
+def _softmax_chi2(orc, x, n, seed=12345, pos=7):
     p = np.exp(x.astype(np.float64) - x.max())
     p /= p.sum()
-    n = 40000
-    counts = np.zeros(16)
+    counts = np.zeros(len(x))
     for i in range(n):
-        tok, _ = orc.sample_row(x, seed=12345, seq_id=i, pos=7)
+        tok, _ = orc.sample_row(x, seed=seed, seq_id=i, pos=pos)
         counts[tok] += 1
-    expect = n * p
-    chi2 = float(((counts - expect) ** 2 / expect).sum())
-    # 15 dof: P(chi2 > 37.7) = 0.001
-    assert chi2 < 37.7, (chi2, counts, expect)
-    sigma = np.sqrt(n * p * (1 - p))
-    assert np.all(np.abs(counts - expect) < 4.5 * sigma)
+    keep = n * p >= 5          # chi-square cells with enough mass; pool the rest
+    obs = np.append(counts[keep], counts[~keep].sum())
+    exp = np.append(n * p[keep], n * p[~keep].sum())
+    if exp[-1] < 5:
+        obs, exp = obs[:-1], exp[:-1]
+    return float(((obs - exp) ** 2 / exp).sum()), len(obs) - 1, counts, n * p
+
+
+def test_gumbel_max_matches_softmax(orc):
+    """P9: argmax_v(x_v + g_v) ~ softmax(x): the defining property of Gumbel-max
+    sampling.  16-way row (one partial block), 40k independent keys."""
+    x = np.array([0.0, 1.0, 2.0, -1.0, 0.5, 3.0, -2.0, 1.5,
+                  0.25, -0.5, 2.5, 0.0, -3.0, 1.0, 0.75, 2.0], np.float32)
+    chi2, dof, counts, expect = _softmax_chi2(orc, x, 40000)
+    assert dof == 15 and chi2 < 37.7, (chi2, counts, expect)  # P(chi2_15 > 37.7) = 0.001
+
+
+def test_gumbel_max_matches_softmax_across_blocks(orc):
+    """Same property for a row spanning several 64-token noise blocks (the
+    top-down construction, O11): mass spread inside one block, across blocks
+    and on the partial last block."""
+    V = 150  # blocks of 64, 64, 22
+    x = np.full(V, -6.0, np.float32)
+    for v, val in [(3, 2.0), (10, 1.5), (63, 1.0), (64, 2.2), (100, 0.5), (127, 1.7),
+                   (128, 2.1), (140, 1.2), (149, 0.8), (5, 1.9)]:
+        x[v] = val
+    chi2, dof, counts, expect = _softmax_chi2(orc, x, 40000, seed=99, pos=3)
+    # dof ~ 11: P(chi2_11 > 31.3) = 0.001
+    assert chi2 < 31.3 + 2 * (dof - 11), (chi2, dof)
+
+
+def _gumbel_cdf(g, loc=0.0):
+    return np.exp(-np.exp(-(g - loc)))
+
+
+def _ks(samples, cdf):
+    s = np.sort(np.asarray(samples, np.float64))
+    n = len(s)
+    F = cdf(s)
+    return max(np.max(np.arange(1, n + 1) / n - F), np.max(F - np.arange(0, n) / n))
+
+
+def test_noise_marginals_are_gumbel(orc):
+    """Every element's noise is Gumbel(0,1) (Kolmogorov-Smirnov), the block
+    maximum is Gumbel(log n) and sits at the position p_b, elements of a block
+    are uncorrelated: the top-down construction yields iid Gumbel noise."""
+    V = 130  # blocks 64, 64, 2
+    keys = 1500
+    G = np.stack([orc.row_noise(V, 777, k, 5) for k in range(keys)])
+    assert np.all(np.isfinite(G))
+    n = G.size
+    assert _ks(G.ravel(), _gumbel_cdf) < 1.63 / np.sqrt(n)      # alpha = 0.01
+    bm = G[:, :64].max(axis=1)
+    assert _ks(bm, lambda g: _gumbel_cdf(g, np.log(64.0))) < 1.63 / np.sqrt(keys)
+    # argmax position of a full block is uniform over its 64 slots
+    pos = np.argmax(G[:, 64:128], axis=1)
+    cnt = np.bincount(pos, minlength=64)
+    chi2 = ((cnt - keys / 64) ** 2 / (keys / 64)).sum()
+    assert chi2 < 110  # 63 dof: P(chi2 > 110) ~ 1e-4
+    c = np.corrcoef(G[:, 0], G[:, 1])[0, 1]
+    assert abs(c) < 4 / np.sqrt(keys)
+    # the partial block of 2 elements: max ~ Gumbel(log 2)
+    assert _ks(G[:, 128:].max(axis=1), lambda g: _gumbel_cdf(g, np.log(2.0))) < 1.63 / np.sqrt(keys)
 
 
 def test_sampler_special_cases(orc):
@@ -124,9 +177,9 @@ def test_sampler_special_cases(orc):
     x[30] = 50.0
     tok, nan = orc.sample_row(x, 1, 2, 3)
     assert nan and tok == 30
-    # a huge gap always wins (g range is < 19.5 wide)
+    # a huge gap always wins (the noise spans < 24 for blocks of <= 64)
     x = np.zeros(V, np.float32)
-    x[11] = 19.5
+    x[11] = 24.0
     for s in range(50):
         assert orc.sample_row(x, s, s + 1, s + 2)[0] == 11
 
@@ -144,28 +197,46 @@ def test_sampler_keying(orc):
     assert base != [orc.sample_row(x, 7, 11, pos + 1)[0] for pos in range(40)]
 
 
-def test_sampler_matches_explicit_philox_gumbel(orc):
-    """The row sampler equals argmax over an explicit per-element evaluation
-    built from the pinned pieces (Philox KAT-checked, table-checked g)."""
+def _noise_by_steps(orc, V, seed, sid, pos):
+    """O11's construction re-derived step by step from the separately pinned
+    pieces (Philox: KATs; log_det: accuracy pins) in numpy float32 (IEEE RN)."""
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    lo, hi = sid & 0xFFFFFFFF, sid >> 32
+    u = lambda w: np.float32((2 * (int(w) >> 9) + 1) * 2.0 ** -24)
+    ld = lambda v: orc.log_det_array(np.asarray([v], np.float32))[0]
+    g = np.empty(V, np.float32)
+    for b in range((V + 63) // 64):
+        n = min(64, V - 64 * b)
+        w = orc.philox4x32_10([0x80000000 | (b >> 1), pos, lo, hi], key)
+        wa, wb = (w[2], w[3]) if b & 1 else (w[0], w[1])
+        a = -ld(u(wa))
+        E = np.float32(a / np.float32(n))
+        G = -ld(E)
+        p = (int(wb) * n) >> 32
+        for j in range(n):
+            v = 64 * b + j
+            if j == p:
+                g[v] = G
+                continue
+            A = -ld(u(orc.philox4x32_10([v >> 2, pos, lo, hi], key)[v & 3]))
+            gv = -ld(np.float32(E + A))
+            g[v] = min(G, gv)
+    return g
+
+
+def test_sampler_noise_by_steps(orc):
+    """The oracle's noise and sample equal the construction evaluated step by
+    step; z = RN(RN(x/T) + g), first maximum."""
     rng = np.random.default_rng(3)
-    V = 203
+    V = 203  # blocks 64, 64, 64, 11
     x = rng.normal(0, 2, V).astype(np.float32)
-    seed, sid, pos = 0x1234567890ABCDEF, (5 << 40) | 77, 19
-    g = orc.noise_table()
-    z = np.empty(V, np.float32)
-    for v in range(V):
-        w = orc.philox4x32_10([v >> 2, pos, sid & 0xFFFFFFFF, sid >> 32],
-                              [seed & 0xFFFFFFFF, seed >> 32])[v & 3]
-        z[v] = np.float32(x[v] + g[int(w) >> 9])
-    want = int(np.argmax(z))
-    assert orc.sample_row(x, seed, sid, pos)[0] == want
-    # temperature: z = RN(RN(x/T) + g)
-    T = np.float32(0.7)
-    gw = np.array([g[int(orc.philox4x32_10([v >> 2, pos, sid & 0xFFFFFFFF, sid >> 32],
-                                           [seed & 0xFFFFFFFF, seed >> 32])[v & 3]) >> 9]
-                   for v in range(V)], np.float32)
-    zt = ((x / T).astype(np.float32) + gw).astype(np.float32)
-    assert orc.sample_row(x, seed, sid, pos, float(T))[0] == int(np.argmax(zt))
+    for seed, sid, pos in [(0x1234567890ABCDEF, (5 << 40) | 77, 19), (1, 2, 0), (2**64 - 1, 2**63, 4095)]:
+        g = _noise_by_steps(orc, V, seed, sid, pos)
+        assert np.array_equal(g.view(np.uint32), orc.row_noise(V, seed, sid, pos).view(np.uint32))
+        assert orc.sample_row(x, seed, sid, pos)[0] == int(np.argmax((x + g).astype(np.float32)))
+        T = np.float32(0.7)
+        zt = ((x / T).astype(np.float32) + g).astype(np.float32)
+        assert orc.sample_row(x, seed, sid, pos, float(T))[0] == int(np.argmax(zt))
 
 
 def test_sampler_bf16_equals_f32_of_same_values(orc):
