@@ -83,7 +83,7 @@ class ClockSampler:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -369,7 +369,7 @@ def cpu_cores_used(n_units: int) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="grpo", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="srt", choices=["srt", "reference"])
@@ -502,7 +502,7 @@ def main():
         "committed_tokens_per_s": world * com / (max_ms / 1000.0),
         "mean_accepted_per_seq_step": acc / (K * cfg["active"]),
         "mean_rows_per_step": float(rows.mean()),
-        "roofline": {"bound": "hbm", "kernel": "scan (k_scan_pruned)",
+        "roofline": {"bound": "hbm", "kernel": "scan (k_scan_rows + k_rowinfo)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind,
