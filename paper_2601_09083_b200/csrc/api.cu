@@ -93,9 +93,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   size_t off = 0;
   const size_t o_tok = off;     off = align_up(off + N * 4);
   const size_t o_cnt = off;     off = align_up(off + N * 4);
-  const size_t o_nch = off;     off = align_up(off + N * 4);
-  const size_t o_blk = off;     off = align_up(off + N * 4);
-  const size_t o_ch0 = off;     off = align_up(off + N * 4);
+  const size_t o_rec = off;     off = align_up(off + N * 16);
   const size_t o_hash = off;    off = align_up(off + H * sizeof(HashSlot));
   const size_t o_slots = off;   off = align_up(off + W * 4);
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
@@ -117,9 +115,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.N = N; d.H = H; d.W = W;
   d.tok = (int32_t*)(b + o_tok);
   d.cnt = (uint32_t*)(b + o_cnt);
-  d.nchild = (uint32_t*)(b + o_nch);
-  d.blk0 = (uint32_t*)(b + o_blk);
-  d.child0 = (uint32_t*)(b + o_ch0);
+  d.rec = (uint4*)(b + o_rec);
   d.hash = (HashSlot*)(b + o_hash);
   d.slots = (uint32_t*)(b + o_slots);
   d.ctr = (unsigned long long*)(b + o_ctr);
@@ -337,7 +333,7 @@ srt_status srt_cache_dump(srt_cache* c, int32_t p, srt_dump_record* host_buf, in
   struct HNode { int32_t tok; uint32_t cnt; std::vector<int64_t> kids; };
   std::vector<HNode> nodes;
   uint32_t root_nchild = 0;
-  SRT_CUDA(cudaMemcpyAsync(&root_nchild, c->dev.nchild + p, 4, cudaMemcpyDeviceToHost, stream), "dump");
+  SRT_CUDA(cudaMemcpyAsync(&root_nchild, &c->dev.rec[p].x, 4, cudaMemcpyDeviceToHost, stream), "dump");
   SRT_CUDA(cudaStreamSynchronize(stream), "dump");
   nodes.push_back(HNode{-1, 0, {}});
   std::vector<uint32_t> frontier = {(uint32_t)p};

@@ -26,9 +26,8 @@ cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(c.tok, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.cnt, 0, c.N * 4, stream)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(c.nchild, 0, c.N * 4, stream)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(c.blk0, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(c.child0, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
+  // rec = {nchild 0, child0 -, token -, csum 0}: child0 is read only if nchild >= 1
+  if ((e = cudaMemsetAsync(c.rec, 0, c.N * 16, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.hash, 0xFF, c.H * sizeof(HashSlot), stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.slots, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
   k_init_counters<<<1, 1, 0, stream>>>(c);
@@ -101,17 +100,16 @@ __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, u
   const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const uint32_t u = frontier[f];
-  const uint32_t F = c.nchild[u];
-  const uint32_t b0 = c.blk0[u];
-  const uint32_t c0 = c.child0[u];
+  const uint4 r = c.rec[u];
+  const uint32_t F = r.x;
   for (uint32_t k = 0; k < F; ++k) {
-    const uint32_t ch = child_at(c, u, c0, b0, k);
+    const uint32_t ch = child_at(c, u, r.y, k);
     const unsigned int o = atomicAdd(out_n, 1u);
     out_node[o] = ch;
     out_parent[o] = f;
     out_tok[o] = c.tok[ch];
     out_cnt[o] = c.cnt[ch];
-    out_nchild[o] = c.nchild[ch];
+    out_nchild[o] = c.rec[ch].x;
   }
 }
 

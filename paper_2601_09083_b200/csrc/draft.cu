@@ -100,67 +100,72 @@ __device__ __forceinline__ Cand frontier_pop(FrontierSmem& F, int size, int lane
   return top;
 }
 
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
-  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
-// Push the children of u (C(v) = count(v) / sum over u's children, P:L137;
-// score = score_u * C) into the frontier.
+// Push the children of u (C(v) = count(v) / csum(u), csum = the sum of the
+// counts of u's children; score = score_u * C) into the
+// frontier.  rec[u] is one 16-byte load; a single child needs nothing else
+// (its C is exactly 1); more children are enumerated 32 x UNR at a time with
+// every load of a round issued before any is used.
 __device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uint32_t u,
                       double score_u, int32_t depth_u, int32_t parent_idx, int lane) {
-  const uint32_t nch = c.nchild[u];
-  if (nch == 0 || cap <= 0) return size;
-  const uint32_t b0 = c.blk0[u];
-  const uint32_t c0 = c.child0[u];
-  // pass 1: sibling sum (first 32 children kept in registers)
-  uint32_t ch0 = 0, cnt0 = 0;
-  int32_t tok0 = 0;
-  unsigned long long sum = 0;
-  for (uint32_t k = lane; k < nch; k += 32) {
-    const uint32_t ch = child_at(c, u, c0, b0, k);
-    const uint32_t cc = c.cnt[ch];
-    if (k < 32) {
-      ch0 = ch;
-      cnt0 = cc;
-      tok0 = c.tok[ch];
-    }
-    sum += cc;
+  if (cap <= 0) return size;
+  const uint4 r = ld_rec(c, u);
+  const uint32_t nch = r.x;
+  if (nch == 0) return size;
+  if (nch == 1) {
+    // C = cnt(child0) / csum(u) = 1 exactly when csum > 0 (0/0 -> 0, O6)
+    const Cand b{r.w ? __dmul_rn(score_u, 1.0) : 0.0, depth_u + 1, (int32_t)r.z, parent_idx, r.y};
+    if (size == cap && !better(b.score, b.depth, b.tok, b.parent, F.score[cap - 1],
+                               F.depth[cap - 1], F.tok[cap - 1], F.parent[cap - 1]))
+      return size;
+    return frontier_insert(F, size, cap, b, lane);
   }
-  sum = warp_sum_u64(sum);
-  const double dsum = (double)sum;  // exact: < 2^53
-  // pass 2: score every child and merge it into the frontier
-  for (uint32_t kb = 0; kb < nch; kb += 32) {
-    const uint32_t k = kb + lane;
-    const bool valid = k < nch;
-    Cand cd{0.0, depth_u + 1, 0, parent_idx, 0};
-    if (valid) {
-      uint32_t ch = ch0, cc = cnt0;
-      int32_t tk = tok0;
-      if (kb > 0) {
-        ch = child_at(c, u, c0, b0, k);
-        cc = c.cnt[ch];
-        tk = c.tok[ch];
-      }
-      const double C = sum ? __ddiv_rn((double)cc, dsum) : 0.0;
-      cd.score = __dmul_rn(score_u, C);
-      cd.tok = tk;
-      cd.node = ch;
+  const double dsum = (double)r.w;  // exact (< 2^32)
+  // block bases of blocks 0..nb-1 (children 1..nch-1), one lane each
+  const uint32_t nb = blk_index(nch - 2) + 1;
+  const uint32_t mybase = lane < (int)nb ? hash_find(c, block_key(u, lane)) : 0u;
+  constexpr int UNR = 8;
+  for (uint32_t kr = 0; kr < nch; kr += 32 * UNR) {
+    uint32_t ch[UNR], cc[UNR];
+    int32_t tk[UNR];
+#pragma unroll
+    for (int m = 0; m < UNR; ++m) {  // child ids
+      const uint32_t k = kr + m * 32 + lane;
+      const uint32_t jj = k >= 1 ? k - 1 : 0;
+      const uint32_t bi = blk_index(jj);
+      const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
+      ch[m] = NONE;
+      if (k < nch) ch[m] = k == 0 ? r.y : c.slots[base + (jj - blk_start(bi))];
     }
-    // cheap prefilter against the current worst entry when full
-    bool want = valid;
-    if (want && size == cap) want = !entry_better(F, cap - 1, cd);
-    unsigned pending = __ballot_sync(0xffffffffu, want);
-    while (pending) {
-      const int src = __ffs(pending) - 1;
-      pending &= pending - 1;
-      Cand b;
-      b.score = __shfl_sync(0xffffffffu, cd.score, src);
-      b.depth = cd.depth;
-      b.tok = __shfl_sync(0xffffffffu, cd.tok, src);
-      b.parent = parent_idx;
-      b.node = __shfl_sync(0xffffffffu, cd.node, src);
-      size = frontier_insert(F, size, cap, b, lane);
+#pragma unroll
+    for (int m = 0; m < UNR; ++m) {  // their counts and tokens
+      cc[m] = 0;
+      tk[m] = 0;
+      if (ch[m] != NONE) {
+        cc[m] = __ldg(&c.cnt[ch[m]]);
+        tk[m] = kr + m * 32 + lane == 0 ? (int32_t)r.z : __ldg(&c.tok[ch[m]]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < UNR; ++m) {
+      if (kr + m * 32 >= nch) break;
+      const bool valid = ch[m] != NONE;
+      Cand cd{0.0, depth_u + 1, tk[m], parent_idx, ch[m]};
+      if (valid) cd.score = __dmul_rn(score_u, r.w ? __ddiv_rn((double)cc[m], dsum) : 0.0);
+      // cheap prefilter against the current worst entry when full
+      bool want = valid;
+      if (want && size == cap) want = !entry_better(F, cap - 1, cd);
+      unsigned pending = __ballot_sync(0xffffffffu, want);
+      while (pending) {
+        const int src = __ffs(pending) - 1;
+        pending &= pending - 1;
+        Cand b;
+        b.score = __shfl_sync(0xffffffffu, cd.score, src);
+        b.depth = cd.depth;
+        b.tok = __shfl_sync(0xffffffffu, cd.tok, src);
+        b.parent = parent_idx;
+        b.node = __shfl_sync(0xffffffffu, cd.node, src);
+        size = frontier_insert(F, size, cap, b, lane);
+      }
     }
   }
   return size;
@@ -209,7 +214,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         }
       }
     }
-    const bool has = ok && c.nchild[node] > 0;
+    const bool has = ok && ld_rec(c, node).x > 0;
     const unsigned bal = __ballot_sync(0xffffffffu, has);
     q = bal ? 32 - __clz(bal) : 0;
     uq = __shfl_sync(0xffffffffu, node, q > 0 ? q - 1 : 0);

@@ -90,25 +90,42 @@ __device__ __forceinline__ uint32_t bump_alloc(unsigned long long* ctr, unsigned
   return (id + amount <= limit) ? (uint32_t)id : BAD;
 }
 
+// One 16-byte relaxed load of a hash slot: key and value together, so the
+// common case (an existing edge) costs one round trip per hop.
+__device__ __forceinline__ void ld_slot(const HashSlot* s, unsigned long long& key,
+                                        uint32_t& val) {
+  unsigned long long k, v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(v) : "l"(s)
+               : "memory");
+  key = k;
+  val = (uint32_t)v;
+}
+
 // Probe for `key`; if absent, claim the first EMPTY slot with a CAS.
 // Returns the slot index (or -1 if the table is full); *created tells whether
-// this thread inserted the key (its value is then still NONE = pending).
+// this thread inserted the key (its value is then still NONE = pending);
+// *val is the slot's value as read (NONE if pending or created).
 __device__ __forceinline__ long long hash_acquire(const DevCache& c, unsigned long long key,
-                                                  bool* created) {
+                                                  bool* created, uint32_t* val) {
   const unsigned long long mask = c.H - 1;
   unsigned long long h = mix64(key) & mask;
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
     HashSlot* s = c.hash + h;
-    unsigned long long k = ld_relaxed_u64(&s->key);
+    unsigned long long k;
+    uint32_t v;
+    ld_slot(s, k, v);
     if (k == EMPTY_KEY) {
       k = atomicCAS(&s->key, EMPTY_KEY, key);
       if (k == EMPTY_KEY) {
         *created = true;
+        *val = NONE;
         return (long long)h;
       }
+      v = NONE;  // another thread claimed this slot: re-read its value later
     }
     if (k == key) {
       *created = false;
+      *val = v;
       return (long long)h;
     }
     h = (h + 1) & mask;
@@ -141,11 +158,14 @@ __device__ uint32_t wait_block(const DevCache& c, uint32_t u, uint32_t i) {
   }
 }
 
-// Append child id `ch` to node u's child blocks.
-__device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch) {
-  const uint32_t k0 = atomicAdd(&c.nchild[u], 1u);
-  if (k0 == 0) {  // the first child lives inline in the node
-    c.child0[u] = ch;
+// Append child `ch` (token tk) to node u's children.  Child 0 lives inline in
+// rec[u]; child k >= 1 goes to slot k-1 of the geometric blocks, each created
+// by the thread that claims its first slot and published through the hash.
+__device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch, int32_t tk) {
+  const uint32_t k0 = atomicAdd(&c.rec[u].x, 1u);
+  if (k0 == 0) {  // read only by later kernels
+    c.rec[u].y = ch;
+    c.rec[u].z = (uint32_t)tk;
     return;
   }
   const uint32_t k = k0 - 1;
@@ -157,19 +177,14 @@ __device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch) {
     const unsigned long long b = atomicAdd(&c.ctr[1], (unsigned long long)sz);
     base = (b + sz <= c.W) ? (uint32_t)b : BAD;
     if (base == BAD) set_error(c, SRT_DEV_CAPACITY);
-    if (i == 0) {
-      st_release_u32(&c.blk0[u], base);
-    } else {
-      bool created = false;
-      const long long h = hash_acquire(c, block_key(u, i), &created);
-      if (h < 0) {
-        set_error(c, SRT_DEV_CAPACITY);
-        return;  // waiters poll the status word
-      }
-      st_release_u32(&c.hash[h].val, base);
+    bool created = false;
+    uint32_t unused;
+    const long long h = hash_acquire(c, block_key(u, i), &created, &unused);
+    if (h < 0) {
+      set_error(c, SRT_DEV_CAPACITY);
+      return;  // waiters poll the status word
     }
-  } else if (i == 0) {
-    while ((base = ld_acquire_u32(&c.blk0[u])) == NONE) __nanosleep(32);
+    st_release_u32(&c.hash[h].val, base);
   } else {
     base = wait_block(c, u, i);
   }
@@ -181,13 +196,14 @@ __device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch) {
 __device__ __forceinline__ uint32_t get_or_create(const DevCache& c, uint32_t u, int32_t tk,
                                                   unsigned& created_ctr) {
   bool created = false;
-  const long long h = hash_acquire(c, edge_key(u, (uint32_t)tk), &created);
+  uint32_t v = NONE;
+  const long long h = hash_acquire(c, edge_key(u, (uint32_t)tk), &created, &v);
   if (h < 0) {
     set_error(c, SRT_DEV_CAPACITY);
     return BAD;
   }
   HashSlot* s = c.hash + h;
-  if (!created) return wait_value(&s->val);
+  if (!created) return v != NONE ? v : wait_value(&s->val);
   const uint32_t id = bump_alloc(&c.ctr[0], 1, c.N);
   if (id == BAD) {
     set_error(c, SRT_DEV_CAPACITY);
@@ -195,7 +211,7 @@ __device__ __forceinline__ uint32_t get_or_create(const DevCache& c, uint32_t u,
     return BAD;
   }
   c.tok[id] = tk;
-  attach_child(c, u, id);
+  attach_child(c, u, id, tk);
   st_release_u32(&s->val, id);
   ++created_ctr;
   return id;
@@ -231,8 +247,9 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       }
       const uint32_t ch = get_or_create(c, u, tk, created);
       if (ch >= BAD) break;
-      if (j >= f) {
+      if (j >= f) {  // a window ends at a new position: count it (and its parent's csum)
         atomicAdd(&c.cnt[ch], 1u);
+        atomicAdd(&c.rec[u].w, 1u);
         ++incs;
       }
       u = ch;

@@ -4,12 +4,13 @@
 // node id p (0 <= p < P) is the root of prompt p's tree T_p.
 //   tok[N]     i32  token labelling the edge into the node
 //   cnt[N]     u32  count(u) ("frequency statistics"; reading O1)
-//   nchild[N]  u32  number of children
-//   child0[N]  u32  the first child, inline (most trie nodes have exactly one)
-//   blk0[N]    u32  word offset of the block holding children 1..4 (NONE if none)
+//   rec[N]     16 B {nchild, child0, token of child0, csum}: one load per pop;
+//                   csum = sum of the children's counts (the denominator of
+//                   C(v)), maintained by insert alongside cnt
 //   hash[H]    16 B open-addressing edge hash: key (parent << 32) | token -> child id;
-//                   keys (node << 32) | 0x80000000 | i -> word offset of child block i >= 1
-//   slots[W]   u32  child-id blocks for children 1.. : 4, 4, 8, 16, 32, 32, ... slots
+//                   keys (node << 32) | 0x80000000 | i -> word offset of child block i
+//   slots[W]   u32  child-id blocks for children 1.. : 4, 4, 8, 16, 32, 64, ...
+//                   (geometric, so a hub node with F children has O(log F) blocks)
 // Concurrency: insertion creates nodes with a CAS on the hash key and publishes
 // the value with a release store; counts are atomic adds, so the logical tree
 // (set of (path, count)) does not depend on scheduling.  Node ids do, but no
@@ -44,9 +45,7 @@ struct DevCache {
   unsigned long long N, H, W;
   int32_t* tok;
   uint32_t* cnt;
-  uint32_t* nchild;
-  uint32_t* child0;
-  uint32_t* blk0;
+  uint4* rec;  // .x nchild, .y child0, .z token of child0, .w csum
   HashSlot* hash;
   uint32_t* slots;
   unsigned long long* ctr;  // [0] next node id, [1] next slot word
@@ -107,16 +106,13 @@ __device__ __forceinline__ unsigned long long block_key(uint32_t node, uint32_t 
   return ((unsigned long long)node << 32) | (BLOCK_TAG | i);
 }
 
-// ---- child-block geometry: blocks of 4, 4, 8, 16, then 32-slot blocks ----
-__device__ __forceinline__ uint32_t blk_index(uint32_t k) {
-  return k < 8 ? (k >> 2) : (k < 32 ? (uint32_t)(30 - __clz(k)) : 3u + (k >> 5));
+// ---- child-block geometry for children 1.. (slot j = child j+1):
+//      blocks of 4, 4, 8, 16, 32, 64, ... slots (block i >= 2 holds [2^(i+1), 2^(i+2)))
+__device__ __forceinline__ uint32_t blk_index(uint32_t j) {
+  return j < 8 ? (j >> 2) : (uint32_t)(30 - __clz(j));
 }
-__device__ __forceinline__ uint32_t blk_start(uint32_t i) {
-  return i < 2 ? 4u * i : (i < 4 ? (4u << (i - 1)) : 32u * (i - 3));
-}
-__device__ __forceinline__ uint32_t blk_size(uint32_t i) {
-  return i < 2 ? 4u : (i < 4 ? (4u << (i - 1)) : 32u);
-}
+__device__ __forceinline__ uint32_t blk_start(uint32_t i) { return i < 2 ? 4u * i : (4u << (i - 1)); }
+__device__ __forceinline__ uint32_t blk_size(uint32_t i) { return i < 2 ? 4u : (4u << (i - 1)); }
 
 // Read-only lookup (kernels that run after all insertion is complete).
 // Returns NONE if the key is absent.
@@ -137,15 +133,16 @@ __device__ __forceinline__ uint32_t child_of(const DevCache& c, uint32_t u, int3
   return hash_find(c, edge_key(u, (uint32_t)tok));
 }
 
-// Child k of node u (read-only kernels).  Child 0 is inline; child k >= 1 is
-// slot k-1 of the block geometry above (block 0 via blk0, blocks >= 1 via hash).
+__device__ __forceinline__ uint4 ld_rec(const DevCache& c, uint32_t u) { return __ldg(&c.rec[u]); }
+
+// Child k of node u (read-only kernels; slow path — enumeration loops look the
+// block bases up once).  Child 0 is inline in rec; child k >= 1 is slot k-1.
 __device__ __forceinline__ uint32_t child_at(const DevCache& c, uint32_t u, uint32_t child0,
-                                             uint32_t blk0, uint32_t k) {
+                                             uint32_t k) {
   if (k == 0) return child0;
   const uint32_t j = k - 1;
   const uint32_t i = blk_index(j);
-  const uint32_t base = (i == 0) ? blk0 : hash_find(c, block_key(u, i));
-  return c.slots[base + (j - blk_start(i))];
+  return c.slots[hash_find(c, block_key(u, i)) + (j - blk_start(i))];
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
