@@ -228,9 +228,10 @@ class GpuRun:
             else:
                 self.logits[r0:r1].normal_(0.0, 2.0, generator=g)
         rg = np.random.default_rng(seed + 3)
-        from synth import gap_profile
-        gaps = gap_profile(rg, self.rows_max + 1, profile if profile != "flat" else "moderate")
+        from synth import head_profile
+        gaps, offs = head_profile(rg, self.rows_max + 1, profile if profile != "flat" else "moderate")
         self.gaps = torch.from_numpy(gaps.astype(np.float32)).to(dev)
+        self.offs = torch.from_numpy(offs.astype(np.float32)).to(dev)  # [rows, 3]
         self.profile = profile
         self.flat_logits = self.logits.view(-1)
         self.mod_idx = None
@@ -264,12 +265,14 @@ class GpuRun:
         valid = self.slot[None, :] <= d.draft_len.to(torch.int64)[:, None]
         row = d.row_offsets[:-1, None] + self.slot[None, :]
         row = torch.where(valid, row, torch.full_like(row, self.rows_max))         # dummy row
-        gap = self.gaps[row.clamp(max=self.rows_max)]
+        rc = row.clamp(max=self.rows_max)
+        gap = self.gaps[rc]
+        off = self.offs[rc]  # [n, B+1, 3]
         idx = [row * V + head]
         val = [gap]
-        for k, off in enumerate((0.7, 1.9, 3.4)):
+        for k in range(3):
             idx.append(row * V + (head + 1 + 7919 * (k + 1) + row * 31) % V)
-            val.append(gap - off)
+            val.append(gap - off[..., k])
         idx = torch.stack(idx, -1).reshape(-1)
         val = torch.stack(val, -1).reshape(-1).to(self.ldtype)
         self.mod_idx = idx

@@ -278,6 +278,15 @@ SRT_API srt_status srt_profile_enable(srt_cache* cache, int64_t capacity);
 SRT_API srt_status srt_profile_read(srt_cache* cache, srt_profile_record* host_buf, int64_t cap,
                                     int64_t* n_records, void* stream);
 
+/*
+ * srt_debug_draft_profile — development support: when dev_buf (DEVICE,
+ * 4 int64 per sequence of the next srt_draft calls) is non-NULL, srt_draft
+ * writes per sequence {cycles spent in the match, total cycles, children
+ * enumerated, max children of one expanded node}.  NULL disables (default).
+ * Process-wide; not for concurrent use.
+ */
+SRT_API srt_status srt_debug_draft_profile(int64_t* dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ SRT_BF16, SRT_F32 = 0, 1
 EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache_destroy",
            "srt_insert", "srt_draft", "srt_verify", "srt_cache_dump", "srt_cache_status",
            "srt_cache_clear_errors", "srt_noise_table", "srt_sample_rows_reference",
-           "srt_profile_enable", "srt_profile_read"]
+           "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
                 5: "accept"}
 
@@ -86,6 +86,7 @@ def load() -> ctypes.CDLL:
     L.srt_noise_table.argtypes = [vp, vp]
     L.srt_sample_rows_reference.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, f32, vp, vp]
     L.srt_profile_enable.argtypes = [vp, i64]
+    L.srt_debug_draft_profile.argtypes = [vp]
     L.srt_profile_read.argtypes = [vp, ctypes.POINTER(SrtProfileRecord), i64,
                                    ctypes.POINTER(ctypes.c_int64), vp]
     for name in EXPORTS:

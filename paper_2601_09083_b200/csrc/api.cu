@@ -314,6 +314,11 @@ srt_status srt_profile_read(srt_cache* c, srt_profile_record* host_buf, int64_t 
   return SRT_OK;
 }
 
+srt_status srt_debug_draft_profile(int64_t* dev_buf) {
+  SRT_CUDA(set_draft_profile((long long*)dev_buf), "set_draft_profile");
+  return SRT_OK;
+}
+
 srt_status srt_noise_table(float* out, void* stream) {
   if (!out) return SRT_ERR_INVALID_ARG;
   SRT_CUDA(launch_noise_table(out, (cudaStream_t)stream), "noise table");

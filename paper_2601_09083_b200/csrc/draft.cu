@@ -16,6 +16,11 @@ namespace srt {
 namespace {
 
 constexpr int DRAFT_WARPS = 4;
+
+// Development-only per-sequence profile (srt_debug_draft_profile): when set,
+// k_draft writes {match cycles, total cycles, children scanned, max children
+// of one node} per sequence.
+__device__ long long* g_draft_prof = nullptr;
 constexpr int FCAP = 64;
 
 struct FrontierSmem {
@@ -184,6 +189,8 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   const int32_t s = blockIdx.x * DRAFT_WARPS + w;
   if (s >= n) return;
   FrontierSmem& F = smem[w];
+  const long long t_start = clock64();
+  long long t_match = 0, scanned = 0, maxch = 0;
   const int32_t p = prompt_id[s];
   const int32_t t = seq_len[s];
   const int32_t* y = seq_tok + (int64_t)s * stride;
@@ -219,10 +226,16 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     q = bal ? 32 - __clz(bal) : 0;
     uq = __shfl_sync(0xffffffffu, node, q > 0 ? q - 1 : 0);
   }
+  t_match = clock64() - t_start;
   int32_t popped = 0;
   if (q > 0) {
     const long long bq = (long long)c.b0 + ((long long)q * c.snum) / c.sden;
     const int32_t B = (int32_t)min((long long)Bmax, bq);
+    if (g_draft_prof) {
+      const long long nc = ld_rec(c, uq).x;
+      scanned += nc;
+      maxch = max(maxch, nc);
+    }
     int size = expand(c, F, 0, B, uq, 1.0, 0, -1, lane);
     while (popped < B && size > 0) {
       __syncwarp();
@@ -244,6 +257,11 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       __syncwarp();
       const int cap = B - popped;
       if (size > cap) size = cap;
+      if (g_draft_prof) {
+        const long long nc = ld_rec(c, top.node).x;
+        scanned += nc;
+        maxch = max(maxch, nc);
+      }
       size = expand(c, F, size, cap, top.node, top.score, top.depth, i, lane);
     }
   }
@@ -258,6 +276,13 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   if (lane == 0) {
     match_len[s] = q;
     draft_len[s] = popped;
+    if (g_draft_prof) {
+      long long* o = g_draft_prof + 4 * (int64_t)s;
+      o[0] = t_match;
+      o[1] = clock64() - t_start;
+      o[2] = scanned;
+      o[3] = maxch;
+    }
   }
 }
 
@@ -300,6 +325,10 @@ k_row_offsets(int32_t n, const int32_t* __restrict__ draft_len, int64_t* __restr
 }
 
 }  // namespace
+
+cudaError_t set_draft_profile(long long* buf) {
+  return cudaMemcpyToSymbol(g_draft_prof, &buf, sizeof(buf));
+}
 
 cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,

@@ -126,16 +126,25 @@ def bf16_bits(x: np.ndarray) -> np.ndarray:
 
 
 def gap_profile(rng, n_rows: int, profile: str = "rl-mix") -> np.ndarray:
+    return head_profile(rng, n_rows, profile)[0]
+
+
+def head_profile(rng, n_rows: int, profile: str = "rl-mix"):
+    """Per row: the head's gap above the bulk mean and the 3 distractors'
+    offsets below the head.  rl-mix = low-entropy reasoning with occasional
+    forks: 70% "confident" rows (gap U[18,24], distractors U[5,9] below,
+    p_head > 0.97) and 30% "uncertain" rows (gap U[12,18], distractors
+    U[0.5,4] below)."""
     if profile == "rl-mix":
-        hi = rng.random(n_rows) < 0.7
-        return np.where(hi, rng.uniform(18, 24, n_rows), rng.uniform(12, 18, n_rows))
-    if profile == "peaked":
-        return np.full(n_rows, 26.0)
-    if profile == "moderate":
-        return np.full(n_rows, 18.0)
-    if profile == "flat":
-        return np.zeros(n_rows)
-    raise ValueError(profile)
+        conf = rng.random(n_rows) < 0.7
+        gap = np.where(conf, rng.uniform(18, 24, n_rows), rng.uniform(12, 18, n_rows))
+        off = np.where(conf[:, None], rng.uniform(5, 9, (n_rows, 3)),
+                       rng.uniform(0.5, 4, (n_rows, 3)))
+        return gap, off
+    gap = {"peaked": 26.0, "moderate": 18.0, "flat": 0.0}.get(profile)
+    if gap is None:
+        raise ValueError(profile)
+    return np.full(n_rows, gap), rng.uniform(0.5, 4, (n_rows, 3))
 
 
 def random_logits_np(rng, n_rows: int, V: int, heads=None, profile: str = "rl-mix",
