@@ -69,6 +69,8 @@ typedef enum {
 #define SRT_DEV_CAPACITY 0x2u         /* node / hash / slot pool exhausted: cache is poisoned    */
 #define SRT_DEV_BAD_PROMPT 0x4u       /* prompt id outside [0, P): the sequence is skipped       */
 #define SRT_DEV_NONFINITE_LOGIT 0x8u  /* a NaN logit was read (NaN is never sampled, O11)        */
+#define SRT_DEV_INCONSISTENT 0x10u    /* srt_cache_dump found a child-slot mirror (token/count)
+                                         that disagrees with the node arrays: a library bug   */
 
 typedef enum { SRT_BF16 = 0, SRT_F32 = 1 } srt_dtype;
 
@@ -280,9 +282,10 @@ SRT_API srt_status srt_profile_read(srt_cache* cache, srt_profile_record* host_b
 
 /*
  * srt_debug_draft_profile — development support: when dev_buf (DEVICE,
- * 4 int64 per sequence of the next srt_draft calls) is non-NULL, srt_draft
+ * 8 int64 per sequence of the next srt_draft calls) is non-NULL, srt_draft
  * writes per sequence {cycles spent in the match, total cycles, children
- * enumerated, max children of one expanded node}.  NULL disables (default).
+ * enumerated, max children of one expanded node, cycles in record loads,
+ * block lookups, child loads, frontier inserts}.  NULL disables (default).
  * Process-wide; not for concurrent use.
  */
 SRT_API srt_status srt_debug_draft_profile(int64_t* dev_buf);

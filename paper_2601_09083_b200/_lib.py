@@ -16,6 +16,7 @@ SRT_OK, SRT_ERR_INVALID_CONFIG, SRT_ERR_INVALID_ARG, SRT_ERR_CUDA, SRT_ERR_DEVIC
 STATUS_NAMES = {0: "SRT_OK", 1: "SRT_ERR_INVALID_CONFIG", 2: "SRT_ERR_INVALID_ARG",
                 3: "SRT_ERR_CUDA", 4: "SRT_ERR_DEVICE"}
 SRT_DEV_OOV, SRT_DEV_CAPACITY, SRT_DEV_BAD_PROMPT, SRT_DEV_NONFINITE_LOGIT = 1, 2, 4, 8
+SRT_DEV_INCONSISTENT = 0x10
 SRT_BF16, SRT_F32 = 0, 1
 
 # Every symbol include/srt.h declares (tests check the export table).

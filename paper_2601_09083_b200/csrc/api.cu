@@ -96,6 +96,8 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_rec = off;     off = align_up(off + N * 16);
   const size_t o_hash = off;    off = align_up(off + H * sizeof(HashSlot));
   const size_t o_slots = off;   off = align_up(off + W * 4);
+  const size_t o_stok = off;    off = align_up(off + W * 4);
+  const size_t o_scnt = off;    off = align_up(off + W * 4);
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
   const size_t o_status = off;  off = align_up(off + 4);
   const size_t o_gb = off;      off = align_up(off + (2 * NOISE_BUCKETS + 1) * 4);
@@ -118,6 +120,8 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.rec = (uint4*)(b + o_rec);
   d.hash = (HashSlot*)(b + o_hash);
   d.slots = (uint32_t*)(b + o_slots);
+  d.stok = (int32_t*)(b + o_stok);
+  d.scnt = (uint32_t*)(b + o_scnt);
   d.ctr = (unsigned long long*)(b + o_ctr);
   d.status = (uint32_t*)(b + o_status);
   d.gbound = (float*)(b + o_gb);

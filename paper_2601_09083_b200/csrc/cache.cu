@@ -30,6 +30,8 @@ cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
   if ((e = cudaMemsetAsync(c.rec, 0, c.N * 16, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.hash, 0xFF, c.H * sizeof(HashSlot), stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.slots, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.stok, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.scnt, 0, c.W * 4, stream)) != cudaSuccess) return e;
   k_init_counters<<<1, 1, 0, stream>>>(c);
   return cudaGetLastError();
 }
@@ -93,7 +95,9 @@ cudaError_t launch_noise_table(float* out, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// One thread per frontier node: emit every child (test path only).
+// One thread per frontier node: emit every child (test path only).  Children
+// k >= 1 are read through their slot mirrors (stok, scnt: what srt_draft
+// enumerates) and checked against the node arrays (tok, cnt).
 __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, uint32_t* out_node,
                              int32_t* out_parent, int32_t* out_tok, uint32_t* out_cnt,
                              uint32_t* out_nchild, unsigned int* out_n) {
@@ -103,12 +107,26 @@ __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, u
   const uint4 r = c.rec[u];
   const uint32_t F = r.x;
   for (uint32_t k = 0; k < F; ++k) {
-    const uint32_t ch = child_at(c, u, r.y, k);
+    uint32_t ch;
+    int32_t tk;
+    uint32_t n;
+    if (k == 0) {
+      ch = r.y;
+      tk = (int32_t)r.z;
+      n = c.cnt[ch];
+    } else {
+      const uint32_t j = k - 1, i = blk_index(j);
+      const uint32_t pos = hash_find(c, block_key(u, i)) + (j - blk_start(i));
+      ch = c.slots[pos];
+      tk = c.stok[pos];
+      n = c.scnt[pos];
+    }
+    if (tk != c.tok[ch] || n != c.cnt[ch]) set_error(c, SRT_DEV_INCONSISTENT);
     const unsigned int o = atomicAdd(out_n, 1u);
     out_node[o] = ch;
     out_parent[o] = f;
-    out_tok[o] = c.tok[ch];
-    out_cnt[o] = c.cnt[ch];
+    out_tok[o] = tk;
+    out_cnt[o] = n;
     out_nchild[o] = c.rec[ch].x;
   }
 }

@@ -7,7 +7,8 @@
 // kept in shared memory (<= Bmax entries, truncated to B - popped, which is
 // exact because a child never outranks its parent); the children of each
 // popped node are enumerated 32 at a time from its child blocks (coalesced
-// block reads + count/token gathers) and inserted with warp ballots.
+// reads of the child ids and their token / count mirrors) and inserted with
+// warp ballots.
 // Roofline: latency-bound (L + ~3 B dependent loads per warp); us per batch.
 #include "srt_internal.cuh"
 
@@ -19,8 +20,12 @@ constexpr int DRAFT_WARPS = 4;
 
 // Development-only per-sequence profile (srt_debug_draft_profile): when set,
 // k_draft writes {match cycles, total cycles, children scanned, max children
-// of one node} per sequence.
+// of one node, cycles in: record loads, block lookups, child loads,
+// frontier inserts} per sequence.
 __device__ long long* g_draft_prof = nullptr;
+struct ExpandProf {
+  long long rec = 0, blk = 0, ld = 0, ins = 0;
+};
 constexpr int FCAP = 64;
 
 struct FrontierSmem {
@@ -105,16 +110,38 @@ __device__ __forceinline__ Cand frontier_pop(FrontierSmem& F, int size, int lane
   return top;
 }
 
+
+// ---- register frontier (cap <= 32): lane i holds entry i while a node's
+// children stream past, so each candidate costs one compare against the
+// current bar (entry cap-1) and an entering one a ballot and a lane shift.
+constexpr int32_t IMAX = 0x7FFFFFFF;
+__device__ __forceinline__ Cand cand_shfl(const Cand& e, int src) {
+  return Cand{__shfl_sync(0xffffffffu, e.score, src), __shfl_sync(0xffffffffu, e.depth, src),
+              __shfl_sync(0xffffffffu, e.tok, src), __shfl_sync(0xffffffffu, e.parent, src),
+              __shfl_sync(0xffffffffu, e.node, src)};
+}
+__device__ __forceinline__ Cand cand_shfl_up1(const Cand& e) {
+  return Cand{__shfl_up_sync(0xffffffffu, e.score, 1), __shfl_up_sync(0xffffffffu, e.depth, 1),
+              __shfl_up_sync(0xffffffffu, e.tok, 1), __shfl_up_sync(0xffffffffu, e.parent, 1),
+              __shfl_up_sync(0xffffffffu, e.node, 1)};
+}
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
+  return better(a.score, a.depth, a.tok, a.parent, b.score, b.depth, b.tok, b.parent);
+}
+
 // Push the children of u (C(v) = count(v) / csum(u), csum = the sum of the
 // counts of u's children; score = score_u * C) into the
 // frontier.  rec[u] is one 16-byte load; a single child needs nothing else
 // (its C is exactly 1); more children are enumerated 32 x UNR at a time with
 // every load of a round issued before any is used.
 __device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uint32_t u,
-                      double score_u, int32_t depth_u, int32_t parent_idx, int lane) {
+                      double score_u, int32_t depth_u, int32_t parent_idx, int lane,
+                      ExpandProf& pf) {
   if (cap <= 0) return size;
+  long long t0 = clock64();
   const uint4 r = ld_rec(c, u);
   const uint32_t nch = r.x;
+  pf.rec += clock64() - t0;
   if (nch == 0) return size;
   if (nch == 1) {
     // C = cnt(child0) / csum(u) = 1 exactly when csum > 0 (0/0 -> 0, O6)
@@ -127,29 +154,100 @@ __device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uin
   const double dsum = (double)r.w;  // exact (< 2^32)
   // block bases of blocks 0..nb-1 (children 1..nch-1), one lane each
   const uint32_t nb = blk_index(nch - 2) + 1;
+  t0 = clock64();
   const uint32_t mybase = lane < (int)nb ? hash_find(c, block_key(u, lane)) : 0u;
+  __syncwarp();
+  pf.blk += clock64() - t0;
   constexpr int UNR = 8;
+  if (cap <= 32) {
+    const Cand SENT{-1.0, IMAX, IMAX, IMAX, NONE};  // worse than every real entry (scores >= 0)
+    Cand fr = SENT;
+    if (lane < size) fr = Cand{F.score[lane], F.depth[lane], F.tok[lane], F.parent[lane], F.node[lane]};
+    Cand worst = cand_shfl(fr, cap - 1);  // the bar to enter
+    for (uint32_t kr = 0; kr < nch; kr += 32 * UNR) {
+      Cand cd[UNR];
+      uint32_t cc[UNR];
+      t0 = clock64();
+#pragma unroll
+      for (int m = 0; m < UNR; ++m) {  // child id, token and count mirror: coalesced
+        const uint32_t k = kr + m * 32 + lane;
+        const uint32_t jj = k >= 1 ? k - 1 : 0;
+        const uint32_t bi = blk_index(jj);
+        const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
+        const uint32_t pos = base + (jj - blk_start(bi));
+        cd[m] = Cand{-1.0, depth_u + 1, IMAX, parent_idx, NONE};
+        cc[m] = 0;
+        if (k == 0) {
+          cd[m].node = r.y;
+          cd[m].tok = (int32_t)r.z;
+          cc[m] = __ldg(&c.cnt[r.y]);
+        } else if (k < nch) {
+          cd[m].node = __ldg(&c.slots[pos]);
+          cd[m].tok = __ldg(&c.stok[pos]);
+          cc[m] = __ldg(&c.scnt[pos]);
+        }
+      }
+      __syncwarp();
+      pf.ld += clock64() - t0;
+      t0 = clock64();
+#pragma unroll
+      for (int m = 0; m < UNR; ++m)  // independent: the divisions pipeline
+        if (cd[m].node != NONE)
+          cd[m].score = __dmul_rn(score_u, r.w ? __ddiv_rn((double)cc[m], dsum) : 0.0);
+#pragma unroll
+      for (int m = 0; m < UNR; ++m) {
+        if (kr + m * 32 >= nch) break;
+        unsigned pending = __ballot_sync(0xffffffffu, cand_better(cd[m], worst));
+        while (pending) {
+          const int src = __ffs(pending) - 1;
+          pending &= pending - 1;
+          const Cand b = cand_shfl(cd[m], src);
+          if (!cand_better(b, worst)) continue;  // an earlier insertion raised the bar
+          const int at = __popc(__ballot_sync(0xffffffffu, cand_better(fr, b)));
+          const Cand prev = cand_shfl_up1(fr);
+          if (lane > at) fr = prev;
+          if (lane == at) fr = b;
+          worst = cand_shfl(fr, cap - 1);
+        }
+      }
+      pf.ins += clock64() - t0;
+    }
+    const int nsize = __popc(__ballot_sync(0xffffffffu, lane < cap && fr.score >= 0.0));
+    __syncwarp();
+    if (lane < nsize) {
+      F.score[lane] = fr.score; F.depth[lane] = fr.depth; F.tok[lane] = fr.tok;
+      F.parent[lane] = fr.parent; F.node[lane] = fr.node;
+    }
+    __syncwarp();
+    return nsize;
+  }
   for (uint32_t kr = 0; kr < nch; kr += 32 * UNR) {
     uint32_t ch[UNR], cc[UNR];
     int32_t tk[UNR];
+    t0 = clock64();
 #pragma unroll
-    for (int m = 0; m < UNR; ++m) {  // child ids
+    for (int m = 0; m < UNR; ++m) {  // child id, token and count mirror: coalesced
       const uint32_t k = kr + m * 32 + lane;
       const uint32_t jj = k >= 1 ? k - 1 : 0;
       const uint32_t bi = blk_index(jj);
       const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
+      const uint32_t pos = base + (jj - blk_start(bi));
       ch[m] = NONE;
-      if (k < nch) ch[m] = k == 0 ? r.y : c.slots[base + (jj - blk_start(bi))];
-    }
-#pragma unroll
-    for (int m = 0; m < UNR; ++m) {  // their counts and tokens
       cc[m] = 0;
       tk[m] = 0;
-      if (ch[m] != NONE) {
-        cc[m] = __ldg(&c.cnt[ch[m]]);
-        tk[m] = kr + m * 32 + lane == 0 ? (int32_t)r.z : __ldg(&c.tok[ch[m]]);
+      if (k == 0) {
+        ch[m] = r.y;
+        tk[m] = (int32_t)r.z;
+        cc[m] = __ldg(&c.cnt[r.y]);
+      } else if (k < nch) {
+        ch[m] = __ldg(&c.slots[pos]);
+        tk[m] = __ldg(&c.stok[pos]);
+        cc[m] = __ldg(&c.scnt[pos]);
       }
     }
+    __syncwarp();
+    pf.ld += clock64() - t0;
+    t0 = clock64();
 #pragma unroll
     for (int m = 0; m < UNR; ++m) {
       if (kr + m * 32 >= nch) break;
@@ -169,9 +267,12 @@ __device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uin
         b.tok = __shfl_sync(0xffffffffu, cd.tok, src);
         b.parent = parent_idx;
         b.node = __shfl_sync(0xffffffffu, cd.node, src);
+        // re-check: earlier insertions of this round may have raised the worst entry
+        if (size == cap && entry_better(F, cap - 1, b)) continue;
         size = frontier_insert(F, size, cap, b, lane);
       }
     }
+    pf.ins += clock64() - t0;
   }
   return size;
 }
@@ -191,6 +292,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   FrontierSmem& F = smem[w];
   const long long t_start = clock64();
   long long t_match = 0, scanned = 0, maxch = 0;
+  ExpandProf pf;
   const int32_t p = prompt_id[s];
   const int32_t t = seq_len[s];
   const int32_t* y = seq_tok + (int64_t)s * stride;
@@ -236,7 +338,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       scanned += nc;
       maxch = max(maxch, nc);
     }
-    int size = expand(c, F, 0, B, uq, 1.0, 0, -1, lane);
+    int size = expand(c, F, 0, B, uq, 1.0, 0, -1, lane, pf);
     while (popped < B && size > 0) {
       __syncwarp();
       if (F.score[0] < c.min_score) break;
@@ -262,7 +364,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         scanned += nc;
         maxch = max(maxch, nc);
       }
-      size = expand(c, F, size, cap, top.node, top.score, top.depth, i, lane);
+      size = expand(c, F, size, cap, top.node, top.score, top.depth, i, lane, pf);
     }
   }
   for (int32_t i = popped + lane; i < Bmax; i += 32) {
@@ -277,11 +379,15 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     match_len[s] = q;
     draft_len[s] = popped;
     if (g_draft_prof) {
-      long long* o = g_draft_prof + 4 * (int64_t)s;
+      long long* o = g_draft_prof + 8 * (int64_t)s;
       o[0] = t_match;
       o[1] = clock64() - t_start;
       o[2] = scanned;
       o[3] = maxch;
+      o[4] = pf.rec;
+      o[5] = pf.blk;
+      o[6] = pf.ld;
+      o[7] = pf.ins;
     }
   }
 }

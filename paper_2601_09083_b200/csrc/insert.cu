@@ -90,35 +90,37 @@ __device__ __forceinline__ uint32_t bump_alloc(unsigned long long* ctr, unsigned
   return (id + amount <= limit) ? (uint32_t)id : BAD;
 }
 
-// One 16-byte relaxed load of a hash slot: key and value together, so the
-// common case (an existing edge) costs one round trip per hop.
+// One 16-byte relaxed load of a hash slot: key and (val, aux) together, so
+// the common case (an existing edge) costs one round trip per hop.
 __device__ __forceinline__ void ld_slot(const HashSlot* s, unsigned long long& key,
-                                        uint32_t& val) {
+                                        uint32_t& val, uint32_t& aux) {
   unsigned long long k, v;
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(v) : "l"(s)
                : "memory");
   key = k;
   val = (uint32_t)v;
+  aux = (uint32_t)(v >> 32);
 }
 
 // Probe for `key`; if absent, claim the first EMPTY slot with a CAS.
 // Returns the slot index (or -1 if the table is full); *created tells whether
 // this thread inserted the key (its value is then still NONE = pending);
-// *val is the slot's value as read (NONE if pending or created).
+// *val / *aux are the slot's words as read (val NONE if pending or created).
 __device__ __forceinline__ long long hash_acquire(const DevCache& c, unsigned long long key,
-                                                  bool* created, uint32_t* val) {
+                                                  bool* created, uint32_t* val, uint32_t* aux) {
   const unsigned long long mask = c.H - 1;
   unsigned long long h = mix64(key) & mask;
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
     HashSlot* s = c.hash + h;
     unsigned long long k;
-    uint32_t v;
-    ld_slot(s, k, v);
+    uint32_t v, a;
+    ld_slot(s, k, v, a);
     if (k == EMPTY_KEY) {
       k = atomicCAS(&s->key, EMPTY_KEY, key);
       if (k == EMPTY_KEY) {
         *created = true;
         *val = NONE;
+        *aux = NONE;
         return (long long)h;
       }
       v = NONE;  // another thread claimed this slot: re-read its value later
@@ -126,6 +128,7 @@ __device__ __forceinline__ long long hash_acquire(const DevCache& c, unsigned lo
     if (k == key) {
       *created = false;
       *val = v;
+      *aux = a;
       return (long long)h;
     }
     h = (h + 1) & mask;
@@ -133,10 +136,12 @@ __device__ __forceinline__ long long hash_acquire(const DevCache& c, unsigned lo
   return -1;
 }
 
-__device__ __forceinline__ uint32_t wait_value(const uint32_t* val) {
-  uint32_t v;
-  while ((v = ld_acquire_u32(val)) == NONE) __nanosleep(32);
-  return v;
+// Wait for a pending slot's publication; returns val, *aux gets aux.
+__device__ __forceinline__ uint32_t wait_value(const HashSlot* s, uint32_t* aux) {
+  unsigned long long v;
+  while ((uint32_t)(v = ld_acquire_u64(&s->val)) == NONE) __nanosleep(32);
+  *aux = (uint32_t)(v >> 32);
+  return (uint32_t)v;
 }
 
 // Wait until block i of node u has been published (its unique creator is the
@@ -149,7 +154,8 @@ __device__ uint32_t wait_block(const DevCache& c, uint32_t u, uint32_t i) {
     for (unsigned long long probe = 0; probe <= mask; ++probe) {
       HashSlot* s = c.hash + h;
       const unsigned long long k = ld_relaxed_u64(&s->key);
-      if (k == key) return wait_value(&s->val);
+      uint32_t unused;
+      if (k == key) return wait_value(s, &unused);
       if (k == EMPTY_KEY) break;
       h = (h + 1) & mask;
     }
@@ -161,12 +167,13 @@ __device__ uint32_t wait_block(const DevCache& c, uint32_t u, uint32_t i) {
 // Append child `ch` (token tk) to node u's children.  Child 0 lives inline in
 // rec[u]; child k >= 1 goes to slot k-1 of the geometric blocks, each created
 // by the thread that claims its first slot and published through the hash.
-__device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch, int32_t tk) {
+// Returns the child's slot word (NONE for the inline child 0, BAD on failure).
+__device__ uint32_t attach_child(const DevCache& c, uint32_t u, uint32_t ch, int32_t tk) {
   const uint32_t k0 = atomicAdd(&c.rec[u].x, 1u);
   if (k0 == 0) {  // read only by later kernels
     c.rec[u].y = ch;
     c.rec[u].z = (uint32_t)tk;
-    return;
+    return NONE;
   }
   const uint32_t k = k0 - 1;
   const uint32_t i = blk_index(k);
@@ -178,41 +185,44 @@ __device__ void attach_child(const DevCache& c, uint32_t u, uint32_t ch, int32_t
     base = (b + sz <= c.W) ? (uint32_t)b : BAD;
     if (base == BAD) set_error(c, SRT_DEV_CAPACITY);
     bool created = false;
-    uint32_t unused;
-    const long long h = hash_acquire(c, block_key(u, i), &created, &unused);
+    uint32_t unused, unused2;
+    const long long h = hash_acquire(c, block_key(u, i), &created, &unused, &unused2);
     if (h < 0) {
       set_error(c, SRT_DEV_CAPACITY);
-      return;  // waiters poll the status word
+      return BAD;  // waiters poll the status word
     }
-    st_release_u32(&c.hash[h].val, base);
+    publish_slot(c.hash + h, base, NONE);
   } else {
     base = wait_block(c, u, i);
   }
-  if (base == BAD) return;
+  if (base == BAD) return BAD;
   c.slots[base + off] = ch;
+  c.stok[base + off] = tk;
+  return base + off;
 }
 
-// Child of u labelled tk, created if missing.  BAD if a pool is exhausted.
+// Child of u labelled tk, created if missing; *pos = its slot word (NONE for
+// an inline child 0).  BAD if a pool is exhausted.
 __device__ __forceinline__ uint32_t get_or_create(const DevCache& c, uint32_t u, int32_t tk,
-                                                  unsigned& created_ctr) {
+                                                  uint32_t* pos, unsigned& created_ctr) {
   bool created = false;
   uint32_t v = NONE;
-  const long long h = hash_acquire(c, edge_key(u, (uint32_t)tk), &created, &v);
+  const long long h = hash_acquire(c, edge_key(u, (uint32_t)tk), &created, &v, pos);
   if (h < 0) {
     set_error(c, SRT_DEV_CAPACITY);
     return BAD;
   }
   HashSlot* s = c.hash + h;
-  if (!created) return v != NONE ? v : wait_value(&s->val);
+  if (!created) return v != NONE ? v : wait_value(s, pos);
   const uint32_t id = bump_alloc(&c.ctr[0], 1, c.N);
   if (id == BAD) {
     set_error(c, SRT_DEV_CAPACITY);
-    st_release_u32(&s->val, BAD);
+    publish_slot(s, BAD, NONE);
     return BAD;
   }
   c.tok[id] = tk;
-  attach_child(c, u, id, tk);
-  st_release_u32(&s->val, id);
+  *pos = attach_child(c, u, id, tk);
+  publish_slot(s, id, *pos);
   ++created_ctr;
   return id;
 }
@@ -245,10 +255,12 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         set_error(c, SRT_DEV_OOV);
         break;
       }
-      const uint32_t ch = get_or_create(c, u, tk, created);
+      uint32_t pos;
+      const uint32_t ch = get_or_create(c, u, tk, &pos, created);
       if (ch >= BAD) break;
       if (j >= f) {  // a window ends at a new position: count it (and its parent's csum)
         atomicAdd(&c.cnt[ch], 1u);
+        if (pos < BAD) atomicAdd(&c.scnt[pos], 1u);
         atomicAdd(&c.rec[u].w, 1u);
         ++incs;
       }

@@ -11,6 +11,8 @@
 //                   keys (node << 32) | 0x80000000 | i -> word offset of child block i
 //   slots[W]   u32  child-id blocks for children 1.. : 4, 4, 8, 16, 32, 64, ...
 //                   (geometric, so a hub node with F children has O(log F) blocks)
+//   stok[W], scnt[W]  the token and a mirror of the count of the child in each
+//                   slot, so a node's children enumerate with coalesced loads
 // Concurrency: insertion creates nodes with a CAS on the hash key and publishes
 // the value with a release store; counts are atomic adds, so the logical tree
 // (set of (path, count)) does not depend on scheduling.  Node ids do, but no
@@ -28,10 +30,14 @@ constexpr uint32_t BAD = 0xFFFFFFFEu;   // creation failed (capacity): walk stop
 constexpr unsigned long long EMPTY_KEY = ~0ull;
 constexpr uint32_t BLOCK_TAG = 0x80000000u;  // tokens are < 2^31
 
+// val and aux are published together by one 64-bit release store (pending =
+// both NONE).  Edge entries: val = child id, aux = the child's slot word in its
+// parent's child blocks (NONE for the inline child 0).  Block entries: val =
+// the block's first slot word.
 struct alignas(16) HashSlot {
   unsigned long long key;
   uint32_t val;
-  uint32_t pad;
+  uint32_t aux;
 };
 
 // Exact noise bounds: g over the 2^23 noise inputs, bucketed by
@@ -47,7 +53,9 @@ struct DevCache {
   uint32_t* cnt;
   uint4* rec;  // .x nchild, .y child0, .z token of child0, .w csum
   HashSlot* hash;
-  uint32_t* slots;
+  uint32_t* slots;  // child ids (children 1.. of a node, in its blocks)
+  int32_t* stok;    // their tokens (immutable)
+  uint32_t* scnt;   // mirrors of their counts, contiguous for enumeration
   unsigned long long* ctr;  // [0] next node id, [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
   float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima
@@ -87,6 +95,16 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Publish a hash slot's (val, aux) pair with one release store.
+__device__ __forceinline__ void publish_slot(HashSlot* s, uint32_t val, uint32_t aux) {
+  const unsigned long long v = ((unsigned long long)aux << 32) | val;
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&s->val), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ void set_error(const DevCache& c, uint32_t bits) {
   atomicOr(c.status, bits);
@@ -121,7 +139,7 @@ __device__ __forceinline__ uint32_t hash_find(const DevCache& c, unsigned long l
   unsigned long long h = mix64(key) & mask;
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
     const HashSlot* s = c.hash + h;
-    unsigned long long k = __ldg(&s->key);
+    const unsigned long long k = __ldg(&s->key);
     if (k == key) return __ldg(&s->val);
     if (k == EMPTY_KEY) return NONE;
     h = (h + 1) & mask;

@@ -53,6 +53,8 @@ class Pair:
             o = [tuple(int(v) for v in r) for r in self.orc.dump(p)]
             g = [(t, c, n) for (t, c, n) in g]
             assert g == o, f"tree of prompt {p} differs ({len(g)} vs {len(o)} records)"
+        bits, _ = self.gpu.status()
+        assert not bits & 0x10, "child-slot mirrors disagree with the node arrays"
 
     # -- draft on both -------------------------------------------------------
     def draft(self, prompt_id, seq_tok, seq_len, pos_base=None):

@@ -115,6 +115,26 @@ def test_draft_parity(orc, seed):
     assert od["draft_len"].sum() > 0
 
 
+@pytest.mark.parametrize("Bmax", [7, 32, 64])
+def test_draft_parity_hubs(orc, Bmax):
+    """Hub nodes with thousands of children (several 256-child enumeration
+    rounds), Zipf counts with many ties (resolved by token, O8), and both the
+    register top-K path (budget <= 32) and the serial path (> 32)."""
+    from synth import zipf_tokens
+    rng = np.random.default_rng(7000 + Bmax)
+    V, D, L = 6000, 6, 3
+    pair = Pair(orc, V, 2, D, L, Bmax, node_capacity=1 << 20)
+    perm = rng.permutation(V).astype(np.int32)
+    seqs = [(k % 2, zipf_tokens(rng, 400, V, perm, s=1.05), [(0, 400)]) for k in range(60)]
+    _insert_all(pair, seqs)
+    n = 96
+    ctx = zipf_tokens(rng, n * 20, V, perm, s=1.05).reshape(n, 20)
+    seq_len = rng.integers(1, 21, n).astype(np.int32)
+    od, gd = pair.draft(rng.integers(0, 2, n).astype(np.int32), ctx, seq_len)
+    pair.compare_drafts(od, gd)
+    assert od["draft_len"].sum() > n
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("seed", range(4))
 def test_verify_parity_random(orc, dtype, seed):

@@ -29,7 +29,7 @@ def main():
     for k in range(3):
         run.step(bench.step_seed(0, k))
     n = run.n
-    prof = torch.zeros(n, 4, dtype=torch.int64, device="cuda")
+    prof = torch.zeros(n, 8, dtype=torch.int64, device="cuda")
     L = _lib.load()
     L.srt_debug_draft_profile(ctypes.c_void_p(prof.data_ptr()))
     for k in range(a.steps):
@@ -48,7 +48,8 @@ def main():
               f"max {sc.max()}; max fan-out p50 {np.percentile(mx, 50):.0f} p99 {np.percentile(mx, 99):.0f} max {mx.max()}")
         slow = np.argsort(-tot)[:8]
         for s in slow:
-            print(f"   slow seq {s}: cycles {tot[s]} match {mt[s]} q {q[s]} len {dl[s]} scanned {sc[s]} maxfan {mx[s]}")
+            print(f"   slow seq {s}: cycles {tot[s]} match {mt[s]} q {q[s]} len {dl[s]} scanned {sc[s]} "
+                  f"maxfan {mx[s]} rec {p[s,4]} blk {p[s,5]} ld {p[s,6]} ins {p[s,7]}")
         run.standin(0)
         run.cache.verify(run.logits, run.d, run.seq_id, bench.step_seed(0, 100 + k), run.seq_tok,
                          run.seq_len, run.max_new, out=run.v)
