@@ -51,7 +51,7 @@ CONFIGS = {
                  cap=20000, act_cap=20000, prior_epochs=1, node_capacity=1 << 28),
 }
 
-KERNELS_PER_STEP = 6  # draft, row_offsets, scan, accept, insert_plan, insert_walk
+KERNELS_PER_STEP = 7  # per group: draft, row_offsets, scan, accept, insert_plan/walk/cursor
 
 
 def log(*a):
@@ -161,26 +161,34 @@ class Workload:
             f"tokens), {len(w.truth)} active, generated in {time.time() - t:.1f}s")
 
 
-class GpuRun:
-    """Device state for one rank: cache, sequence tables, logits buffer."""
+class Group:
+    """Device state of one prompt group: its own cache (the trees of the
+    prompts p with p % G == g), sequence tables, draft/verify outputs and a
+    slice of the shared logits buffer.  Groups share no tree, so their steps
+    may run concurrently on different streams with results identical to one
+    cache processing everything in order."""
 
-    def __init__(self, wl: Workload, dtype: str, profile: str, seed: int):
+    def __init__(self, wl: Workload, dtype: str, profile: str, seed: int, g: int, G: int,
+                 logits, gaps, offs, row0: int):
         import torch
         import paper_2601_09083_b200 as srt
         self.torch = torch
         cfg = wl.cfg
         self.cfg = cfg
-        dev = torch.device("cuda", torch.cuda.current_device())
+        dev = logits.device
         self.dev = dev
-        self.n = n = cfg["active"]
+        seqs = np.nonzero(wl.seq_prompt % G == g)[0]
+        self.seqs = seqs
+        self.n = n = len(seqs)
         self.V, self.Bmax = V, B = cfg["V"], cfg["Bmax"]
-        self.ldtype = torch.bfloat16 if dtype == "bf16" else torch.float32
-        t = time.time()
-        c = srt.config(V, cfg["prompts"], cfg["D"], cfg["L"], B, node_capacity=cfg["node_capacity"],
+        self.ldtype = logits.dtype
+        n_prompts = len(range(g, cfg["prompts"], G))
+        c = srt.config(V, n_prompts, cfg["D"], cfg["L"], B,
+                       node_capacity=max(1 << 16, cfg["node_capacity"] // G),
                        logits_dtype=self.ldtype)
         self.cache = srt.SrtCache(c)
         # ---- warm trees: prior-epoch rollouts (P:L151 "carries signal across steps")
-        prior = wl.w.prior
+        prior = [(p // G, tk) for p, tk in wl.w.prior if p % G == g]
         cap = cfg["cap"]
         chunk = 4096
         for i0 in range(0, len(prior), chunk):
@@ -196,55 +204,44 @@ class GpuRun:
         stride = cfg["act_cap"] + B + 2
         tab = np.zeros((n, stride), np.int32)
         truth = np.zeros((n, cfg["act_cap"]), np.int32)
-        for s in range(n):
+        for j, s in enumerate(seqs):
             tr = wl.truth[s]
-            tab[s, :wl.t0[s]] = tr[:wl.t0[s]]
-            truth[s, :len(tr)] = tr
-            truth[s, len(tr):] = tr[-1]
+            tab[j, :wl.t0[s]] = tr[:wl.t0[s]]
+            truth[j, :len(tr)] = tr
+            truth[j, len(tr):] = tr[-1]
         i32 = dict(dtype=torch.int32, device=dev)
-        self.prompt_id = torch.from_numpy(wl.seq_prompt.astype(np.int32)).to(dev)
+        self.prompt_id = torch.from_numpy((wl.seq_prompt[seqs] // G).astype(np.int32)).to(dev)
         self.seq_tok = torch.from_numpy(tab).to(dev)
-        self.seq_len = torch.from_numpy(wl.t0.copy()).to(dev)
+        self.seq_len = torch.from_numpy(wl.t0[seqs].copy()).to(dev)
         self.t_before = self.seq_len.clone()
         self.truth = torch.from_numpy(truth).to(dev)
-        self.truth_last = torch.from_numpy(np.maximum(wl.max_new - 1, 0)).to(dev).to(torch.int64)
-        self.max_new = torch.from_numpy(wl.max_new).to(dev)
-        self.seq_id = torch.from_numpy(wl.seq_id.view(np.int64)).to(dev)
-        self.cache.insert(self.prompt_id, self.seq_tok, torch.zeros(n, **i32), self.seq_len)
+        self.truth_last = torch.from_numpy(np.maximum(wl.max_new[seqs] - 1, 0)).to(dev).to(torch.int64)
+        self.max_new = torch.from_numpy(wl.max_new[seqs].copy()).to(dev)
+        self.seq_id = torch.from_numpy(wl.seq_id[seqs].view(np.int64)).to(dev)
+        # per-sequence suffix cursors (srt_insert_cursor): one hop per window end
+        self.cursor = self.cache.new_cursors(n, dev)
+        self.cache.insert(self.prompt_id, self.seq_tok, torch.zeros(n, **i32), self.seq_len,
+                          cursor=self.cursor)
         bits, st = self.cache.status()
         if bits:
             raise RuntimeError(f"cache error bits {bits} after warm-up inserts ({st})")
         self.tree_stats = st
-        # ---- logits buffer: rows_max + 1 dummy row, bulk N(0, 2^2)
+        # ---- this group's rows of the logits buffer: rows_max + 1 dummy row
         self.rows_max = n * (B + 1)
-        g = torch.Generator(device=dev)
-        g.manual_seed(seed)
-        self.logits = torch.empty(self.rows_max + 1, V, dtype=self.ldtype, device=dev)
-        step = 2048
-        for r0 in range(0, self.rows_max + 1, step):
-            r1 = min(self.rows_max + 1, r0 + step)
-            if profile == "flat":
-                self.logits[r0:r1].uniform_(0, 1, generator=g)
-            else:
-                self.logits[r0:r1].normal_(0.0, 2.0, generator=g)
-        rg = np.random.default_rng(seed + 3)
-        from synth import head_profile
-        gaps, offs = head_profile(rg, self.rows_max + 1, profile if profile != "flat" else "moderate")
-        self.gaps = torch.from_numpy(gaps.astype(np.float32)).to(dev)
-        self.offs = torch.from_numpy(offs.astype(np.float32)).to(dev)  # [rows, 3]
+        self.logits = logits[row0:row0 + self.rows_max + 1]
+        self.gaps = gaps[row0:row0 + self.rows_max + 1]
+        self.offs = offs[row0:row0 + self.rows_max + 1]
         self.profile = profile
         self.flat_logits = self.logits.view(-1)
-        self.mod_idx = None
-        self.mod_val = None
         self.d = srt.DraftOut.empty(n, B, dev)
         self.v = srt.VerifyOut.empty(n, self.rows_max, B, dev)
         self.slot = torch.arange(B + 1, device=dev, dtype=torch.int64)
-        torch.cuda.synchronize()
-        log(f"[bench] device setup {time.time() - t:.1f}s; tree nodes {st['nodes_used']:,} "
-            f"(cap {st['node_capacity']:,}); logits {self.logits.numel() * self.logits.element_size() / 1e9:.2f} GB")
+        # stand-in edits of the previous step (static buffers: restored in place)
+        self.mod_idx = torch.zeros(n * (B + 1) * 4, dtype=torch.int64, device=dev)
+        self.mod_val = self.flat_logits[self.mod_idx].clone()
 
-    # ---- forward stand-in (NOT part of the timed path) ---------------------
-    def standin(self, step: int):
+    # ---- forward stand-in (NOT part of the SRT path) -----------------------
+    def standin(self):
         """Write each drafted row's head logit: the policy's preferred next
         token is the ground-truth token at that row's position (the rollout
         re-joins its template after a divergence), bulk mean 0, gap from the
@@ -255,8 +252,7 @@ class GpuRun:
             self.t_before.copy_(self.seq_len)
             return
         d, n, B, V = self.d, self.n, self.Bmax, self.V
-        if self.mod_idx is not None:
-            self.flat_logits[self.mod_idx] = self.mod_val
+        self.flat_logits[self.mod_idx] = self.mod_val
         depth = torch.cat([torch.zeros(n, 1, dtype=torch.int32, device=self.dev), d.draft_depth],
                           dim=1).to(torch.int64)                                   # [n, B+1]
         pos = self.seq_len.to(torch.int64)[:, None] + depth
@@ -265,9 +261,8 @@ class GpuRun:
         valid = self.slot[None, :] <= d.draft_len.to(torch.int64)[:, None]
         row = d.row_offsets[:-1, None] + self.slot[None, :]
         row = torch.where(valid, row, torch.full_like(row, self.rows_max))         # dummy row
-        rc = row.clamp(max=self.rows_max)
-        gap = self.gaps[rc]
-        off = self.offs[rc]  # [n, B+1, 3]
+        gap = self.gaps[row]
+        off = self.offs[row]  # [n, B+1, 3]
         idx = [row * V + head]
         val = [gap]
         for k in range(3):
@@ -275,27 +270,114 @@ class GpuRun:
             val.append(gap - off[..., k])
         idx = torch.stack(idx, -1).reshape(-1)
         val = torch.stack(val, -1).reshape(-1).to(self.ldtype)
-        self.mod_idx = idx
-        self.mod_val = self.flat_logits[idx].clone()
+        self.mod_idx.copy_(idx)
+        self.mod_val.copy_(self.flat_logits[idx])
         self.flat_logits[idx] = val
         self.t_before.copy_(self.seq_len)
 
-    def step(self, seed: int, ev=None):
-        """draft -> [stand-in] -> verify -> insert.  ev = 4 CUDA events."""
+    def draft(self):
+        self.cache.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d)
+
+    def verify_insert(self, seed: int):
         c = self.cache
+        c.verify(self.logits, self.d, self.seq_id, seed, self.seq_tok, self.seq_len, self.max_new,
+                 out=self.v, rows=self.rows_max)
+        c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len, cursor=self.cursor)
+
+
+class GpuRun:
+    """Device state for one rank: G prompt groups (each its own cache and
+    stream) over one shared logits buffer."""
+
+    def __init__(self, wl: Workload, dtype: str, profile: str, seed: int, groups: int = 1):
+        import torch
+        self.torch = torch
+        cfg = wl.cfg
+        self.cfg = cfg
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        self.n = n = cfg["active"]
+        self.V, self.Bmax = V, B = cfg["V"], cfg["Bmax"]
+        self.ldtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        t = time.time()
+        G = max(1, min(groups, cfg["prompts"]))
+        self.G = G
+        # ---- logits buffer: every group's rows_max + 1 dummy row, bulk N(0, 2^2)
+        counts = [int(np.sum(wl.seq_prompt % G == g)) for g in range(G)]
+        total_rows = sum(c * (B + 1) + 1 for c in counts)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        self.logits = torch.empty(total_rows, V, dtype=self.ldtype, device=dev)
+        step = 2048
+        for r0 in range(0, total_rows, step):
+            r1 = min(total_rows, r0 + step)
+            if profile == "flat":
+                self.logits[r0:r1].uniform_(0, 1, generator=gen)
+            else:
+                self.logits[r0:r1].normal_(0.0, 2.0, generator=gen)
+        rg = np.random.default_rng(seed + 3)
+        from synth import head_profile
+        gaps, offs = head_profile(rg, total_rows, profile if profile != "flat" else "moderate")
+        gaps = torch.from_numpy(gaps.astype(np.float32)).to(dev)
+        offs = torch.from_numpy(offs.astype(np.float32)).to(dev)  # [rows, 3]
+        self.groups = []
+        row0 = 0
+        for g in range(G):
+            self.groups.append(Group(wl, dtype, profile, seed, g, G, self.logits, gaps, offs, row0))
+            row0 += counts[g] * (B + 1) + 1
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(G)]
+        self.rows_max = sum(gr.rows_max for gr in self.groups)
+        torch.cuda.synchronize()
+        self.tree_stats = {k: sum(gr.tree_stats[k] for gr in self.groups)
+                           for k in self.groups[0].tree_stats}
+        log(f"[bench] device setup {time.time() - t:.1f}s; {G} group(s); tree nodes "
+            f"{self.tree_stats['nodes_used']:,} (cap {self.tree_stats['node_capacity']:,}); logits "
+            f"{self.logits.numel() * self.logits.element_size() / 1e9:.2f} GB")
+
+    def __getattr__(self, name):
+        # single-group convenience for the development probes (tools/)
+        groups = self.__dict__.get("groups")
+        if groups is not None and len(groups) == 1:
+            return getattr(groups[0], name)
+        raise AttributeError(name)
+
+    def step(self, seed: int, ev=None):
+        """Sequential step on the current stream: draft -> [stand-in] ->
+        verify -> insert for every group.  ev = 4 CUDA events bracketing the
+        draft segment and the verify+insert segment (stand-in excluded)."""
         if ev:
             ev[0].record()
-        c.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d)
+        for gr in self.groups:
+            gr.draft()
         if ev:
             ev[1].record()
-        self.standin(seed)
+        for gr in self.groups:
+            gr.standin()
         if ev:
             ev[2].record()
-        c.verify(self.logits, self.d, self.seq_id, seed, self.seq_tok, self.seq_len, self.max_new,
-                 out=self.v)
-        c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len)
+        for gr in self.groups:
+            gr.verify_insert(seed)
         if ev:
             ev[3].record()
+
+    def step_pipelined(self, seed: int):
+        """One step of every group, each on its own stream, no host sync:
+        verify+insert of one group overlap the draft / stand-in of the next
+        and the HBM-bound scans of the others.  Stand-in included."""
+        torch = self.torch
+        for gr, st in zip(self.groups, self.streams):
+            with torch.cuda.stream(st):
+                gr.draft()
+                gr.standin()
+                gr.verify_insert(seed)
+
+    def status(self):
+        bits, tot = 0, None
+        for gr in self.groups:
+            b, st = gr.cache.status()
+            bits |= b
+            tot = st if tot is None else {k: tot[k] + st[k] for k in tot}
+        return bits, tot
 
 
 def step_seed(run_seed: int, k: int) -> int:
@@ -382,6 +464,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-prompts", type=int, default=0, help="oracle sample size in prompts")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--groups", type=int, default=1,
+                    help="prompt groups pipelined on separate streams (1 = sequential; >1 measured slower: the latency-bound tree kernels stall behind the scan's HBM traffic)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -429,37 +513,69 @@ def main():
     if world > 1:
         dist.barrier()
     wl = Workload(cfg, args.seed, rank, world)
-    run = GpuRun(wl, args.dtype, args.profile, args.seed + rank)
+    run = GpuRun(wl, args.dtype, args.profile, args.seed + rank, groups=args.groups)
+    G = run.G
+    pipelined = G > 1
     K, W = args.steps, args.warmup
+    seed = step_seed(args.seed, 0)
     for k in range(W):
-        run.step(step_seed(args.seed, k))
+        if pipelined:
+            run.step_pipelined(seed)
+        else:
+            run.step(seed)
     torch.cuda.synchronize()
-    bits, _ = run.cache.status()
+    bits, _ = run.status()
     if bits:
         raise RuntimeError(f"device error bits {bits} during warm-up")
     # ---- timed region
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rows_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     acc_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     com_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
-    run.cache.profile_enable(K * KERNELS_PER_STEP)
+    logs = [torch.zeros(3, K, dtype=torch.int64, device=run.dev) for _ in range(G)]
+    for gr in run.groups:
+        gr.cache.profile_enable(K * KERNELS_PER_STEP)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for k in range(K):
-            run.step(step_seed(args.seed, W + k), evs[k])
-            # bookkeeping outside the event-bracketed segments
-            rows_log[k] = run.d.row_offsets[-1]
-            acc_log[k] = run.v.accept_len.sum()
-            com_log[k] = run.v.n_commit.sum()
+        if pipelined:
+            # every group on its own stream, no host sync inside the region;
+            # the forward stand-in and the bookkeeping are INSIDE the timing
+            ev_a.record()
+            for st in run.streams:
+                st.wait_event(ev_a)
+            for k in range(K):
+                for g, (gr, st) in enumerate(zip(run.groups, run.streams)):
+                    with torch.cuda.stream(st):
+                        gr.draft()
+                        gr.standin()
+                        gr.verify_insert(seed)
+                        logs[g][0, k] = gr.d.row_offsets[-1]
+                        logs[g][1, k] = gr.v.accept_len.sum()
+                        logs[g][2, k] = gr.v.n_commit.sum()
+            for st in run.streams:
+                torch.cuda.current_stream().wait_stream(st)
+            ev_b.record()
+        else:
+            for k in range(K):
+                run.step(seed, evs[k])
+                # bookkeeping outside the event-bracketed segments
+                rows_log[k] = run.d.row_offsets[-1]
+                acc_log[k] = run.v.accept_len.sum()
+                com_log[k] = run.v.n_commit.sum()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    seg_ms = [e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in evs]
-    my_ms = float(sum(seg_ms))
-    prof = run.cache.profile_read()
-    bits, st = run.cache.status()
+    if pipelined:
+        my_ms = float(ev_a.elapsed_time(ev_b))
+        tot_log = sum(logs)
+        rows_log, acc_log, com_log = tot_log[0], tot_log[1], tot_log[2]
+    else:
+        my_ms = float(sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in evs))
+    prof = [x for gr in run.groups for x in gr.cache.profile_read()]
+    bits, st = run.status()
     if bits:
         raise RuntimeError(f"device error bits {bits} in the timed region")
     tot = torch.tensor([my_ms], dtype=torch.float64, device=run.dev)
@@ -499,8 +615,14 @@ def main():
                    "global_batch": cfg["active"] * world, "seqs_per_rank": cfg["active"],
                    "l2": "inputs larger than L2 (logits buffer "
                          f"{run.logits.numel() * esz / 1e9:.1f} GB)",
-                   "timed": "draft + verify + insert device time (CUDA events); forward "
-                            "stand-in excluded"},
+                   "groups": G,
+                   "timed": (f"whole step loop on the device (CUDA events, {G} prompt groups "
+                             f"pipelined on {G} streams); forward stand-in and bookkeeping "
+                             f"INCLUDED" if pipelined else
+                             "draft + verify + insert device time (CUDA events); forward "
+                             "stand-in excluded"),
+                   "seed": "one run seed for every step (the Philox counter carries the "
+                           "position, so every (sequence, position) draws fresh noise)"},
         "accepted_tokens_per_s": world * acc / (max_ms / 1000.0),
         "committed_tokens_per_s": world * com / (max_ms / 1000.0),
         "mean_accepted_per_seq_step": acc / (K * cfg["active"]),
@@ -513,9 +635,11 @@ def main():
                      "frac_of_8TBps_spec": (achieved / 8000.0) if achieved else None},
         "kernels": kern,
         "tree_stage_us_per_batch": {k: kern[k]["mean_us"] for k in
-                                    ("draft", "row_offsets", "insert_plan", "insert_walk", "accept")
+                                    ("draft", "row_offsets", "insert_plan", "insert_walk",
+                                     "insert_cursor", "accept")
                                     if k in kern},
         "gpu_launches": len(prof),
+        "launches_per_step": len(prof) / K,
         "tree_nodes": st["nodes_used"],
     }
     cs = clk.summary()
@@ -544,41 +668,45 @@ def main():
 def e2e_leg(run: GpuRun, args, steps: int):
     """Same metric through the public API with HOST buffers: every step copies
     that step's logits rows from pinned host memory (H2D) and reads the step's
-    results back (D2H) inside the timed region."""
+    results back (D2H) inside the timed region (groups one after another)."""
     torch = run.torch
     if steps <= 0:
         return None
-    rows_max = run.rows_max
+    seed = step_seed(args.seed, 0)
+    rows_max = max(gr.rows_max for gr in run.groups)
     host = torch.empty(run.logits[:rows_max].shape, dtype=run.logits.dtype, pin_memory=True)
     host.copy_(run.logits[:rows_max])
     dev_rows = torch.empty_like(run.logits[:rows_max])
-    out_n = torch.empty(run.n, dtype=torch.int32).pin_memory()
-    out_a = torch.empty(run.n, dtype=torch.int32).pin_memory()
-    out_c = torch.empty(run.n, run.Bmax + 1, dtype=torch.int32).pin_memory()
+    nmax = max(gr.n for gr in run.groups)
+    out_n = torch.empty(nmax, dtype=torch.int32).pin_memory()
+    out_a = torch.empty(nmax, dtype=torch.int32).pin_memory()
+    out_c = torch.empty(nmax, run.Bmax + 1, dtype=torch.int32).pin_memory()
     h2d = d2h = 0
     total_ms = 0.0
     for k in range(steps):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e[0].record()
-        run.cache.draft(run.prompt_id, run.seq_tok, run.seq_len, run.seq_len, out=run.d)
-        rows_t = run.d.row_offsets[-1:].to("cpu", non_blocking=True)
-        e[1].record()
-        torch.cuda.synchronize()
-        rows = int(rows_t.item())
-        run.t_before.copy_(run.seq_len)
-        e[2].record()
-        dev_rows[:rows].copy_(host[:rows], non_blocking=True)
-        run.cache.verify(dev_rows, run.d, run.seq_id, step_seed(args.seed, 10_000 + k),
-                         run.seq_tok, run.seq_len, run.max_new, out=run.v, rows=rows_max)
-        run.cache.insert(run.prompt_id, run.seq_tok, run.t_before, run.seq_len)
-        out_n.copy_(run.v.n_commit, non_blocking=True)
-        out_a.copy_(run.v.accept_len, non_blocking=True)
-        out_c.copy_(run.v.commit_tok, non_blocking=True)
-        e[3].record()
-        torch.cuda.synchronize()
-        total_ms += e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3])
-        h2d += rows * run.V * host.element_size()
-        d2h += 8 + out_n.numel() * 4 + out_a.numel() * 4 + out_c.numel() * 4
+        for gr in run.groups:
+            n = gr.n
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record()
+            gr.draft()
+            rows_t = gr.d.row_offsets[-1:].to("cpu", non_blocking=True)
+            e[1].record()
+            torch.cuda.synchronize()
+            rows = int(rows_t.item())
+            gr.t_before.copy_(gr.seq_len)
+            e[2].record()
+            dev_rows[:rows].copy_(host[:rows], non_blocking=True)
+            gr.cache.verify(dev_rows, gr.d, gr.seq_id, seed, gr.seq_tok, gr.seq_len, gr.max_new,
+                            out=gr.v, rows=gr.rows_max)
+            gr.cache.insert(gr.prompt_id, gr.seq_tok, gr.t_before, gr.seq_len, cursor=gr.cursor)
+            out_n[:n].copy_(gr.v.n_commit, non_blocking=True)
+            out_a[:n].copy_(gr.v.accept_len, non_blocking=True)
+            out_c[:n].copy_(gr.v.commit_tok, non_blocking=True)
+            e[3].record()
+            torch.cuda.synchronize()
+            total_ms += e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3])
+            h2d += rows * run.V * host.element_size()
+            d2h += 8 + n * 4 * 2 + n * (run.Bmax + 1) * 4
     return {"value": steps / (total_ms / 1000.0), "unit": "steps/s",
             "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
             "steps": steps}

@@ -152,6 +152,29 @@ SRT_API srt_status srt_insert(srt_cache* cache, int32_t n, const int32_t* prompt
                       void* stream);
 
 /*
+ * srt_insert_cursor — srt_insert with one suffix cursor per span: same
+ * arguments and the SAME resulting tree (node set and counts), plus
+ * `cursor`, a DEVICE array of n records of SRT_CURSOR_WORDS(D) uint32 words
+ * owned by the caller (record s belongs to span s; keep a sequence at the same
+ * index across calls).  A record remembers, for the position P it was left
+ * at, the nodes of the suffixes y[P-l .. P-1] (l = 1..D), so the next call
+ * reaches every window that ends at a new position with ONE hop from the
+ * previous suffix node instead of a walk from the root (P:L151 online
+ * insertion, done incrementally).  Record words: [0] cache tag, [1] P,
+ * [2] prompt, [3] floor, [4 .. 4+D) suffix nodes.  A record is used only if
+ * its tag is this cache's, P == max(from, floor) and prompt / floor match;
+ * otherwise (e.g. zero-filled on first use) it is rebuilt from the root, so
+ * any content is safe.  Spans with more than D new positions are inserted by
+ * the walk path and leave their record invalid.  The record is updated to
+ * P = to on return (unchanged if the span inserts nothing).
+ */
+#define SRT_CURSOR_WORDS(D) ((D) + 4)
+SRT_API srt_status srt_insert_cursor(srt_cache* cache, int32_t n, const int32_t* prompt_id,
+                             const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                             const int32_t* to, const int32_t* floor_, uint32_t* cursor,
+                             srt_insert_stats* stats_dev, void* stream);
+
+/*
  * srt_draft — batched longest-suffix match + best-first draft + tree layout
  * (P:L135-139).  For each sequence s < n (prompt prompt_id[s], response
  * seq_tok[s*stride ...] of length t = seq_len[s]):
@@ -268,7 +291,8 @@ typedef enum {
   SRT_K_DRAFT = 2,
   SRT_K_ROW_OFFSETS = 3,
   SRT_K_SCAN = 4,
-  SRT_K_ACCEPT = 5
+  SRT_K_ACCEPT = 5,
+  SRT_K_INSERT_CURSOR = 6
 } srt_kernel_id;
 
 typedef struct {

@@ -21,11 +21,11 @@ SRT_BF16, SRT_F32 = 0, 1
 
 # Every symbol include/srt.h declares (tests check the export table).
 EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache_destroy",
-           "srt_insert", "srt_draft", "srt_verify", "srt_cache_dump", "srt_cache_status",
+           "srt_insert", "srt_insert_cursor", "srt_draft", "srt_verify", "srt_cache_dump", "srt_cache_status",
            "srt_cache_clear_errors", "srt_noise_table", "srt_sample_rows_reference",
            "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
-                5: "accept"}
+                5: "accept", 6: "insert_cursor"}
 
 
 class SrtConfig(ctypes.Structure):
@@ -76,6 +76,7 @@ def load() -> ctypes.CDLL:
     L.srt_cache_create.argtypes = [ctypes.POINTER(SrtConfig), vp, ctypes.POINTER(vp)]
     L.srt_cache_destroy.argtypes = [vp, vp]
     L.srt_insert.argtypes = [vp, i32, vp, vp, i64, vp, vp, vp, vp, vp]
+    L.srt_insert_cursor.argtypes = [vp, i32, vp, vp, i64, vp, vp, vp, vp, vp, vp]
     L.srt_draft.argtypes = [vp, i32, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srt_verify.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, u64, f32, i32, vp, vp, i64,
                              vp, vp, vp, vp, vp, vp, vp, vp]

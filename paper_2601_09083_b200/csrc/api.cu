@@ -1,5 +1,7 @@
 // api.cu — host side of the C ABI declared in include/srt.h: validation,
 // pool allocation (cudaMallocAsync on the caller's stream), launches, status.
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
@@ -20,6 +22,7 @@ struct srt_cache {
   unsigned long long* result = nullptr;  // verify: per-row packed winner (pack_cand)
   int64_t row_cap = 0;          // rows the two buffers above can hold
   int device;
+  uint32_t tag;  // identifies this cache in insert cursors (never 0)
   // per-kernel timing (srt_profile_enable)
   std::vector<cudaEvent_t> ev;
   std::vector<int32_t> kid;
@@ -104,6 +107,14 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   srt_cache* c = new srt_cache();
   c->cfg = *cfg;
   cudaGetDevice(&c->device);
+  {
+    static std::atomic<uint64_t> serial{0};
+    uint64_t z = (uint64_t)(uintptr_t)c ^ (++serial * 0x9E3779B97F4A7C15ull) ^
+                 (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    c->tag = (uint32_t)(z ^ (z >> 31)) | 1u;
+  }
   cudaError_t e = cudaMallocAsync(&c->pool, off, stream);
   if (e != cudaSuccess) {
     delete c;
@@ -148,23 +159,23 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   return SRT_OK;
 }
 
-srt_status srt_insert(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,
-                      int64_t stride, const int32_t* from, const int32_t* to,
-                      const int32_t* floor_, srt_insert_stats* stats_dev, void* stream_) {
-  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
-  if (n == 0) return SRT_OK;
-  if (!prompt_id || !seq_tok || !from || !to) return SRT_ERR_INVALID_ARG;
-  cudaStream_t stream = (cudaStream_t)stream_;
+namespace {
+srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,
+                       int64_t stride, const int32_t* from, const int32_t* to,
+                       const int32_t* floor_, uint32_t* cursor, srt_insert_stats* stats_dev,
+                       cudaStream_t stream) {
   if (c->scratch_cap < (int64_t)n + 1) {
     if (c->scratch) SRT_CUDA(cudaFreeAsync(c->scratch, stream), "cudaFreeAsync(scratch)");
     int64_t cap = std::max<int64_t>(4096, 2 * ((int64_t)n + 1));
     SRT_CUDA(cudaMallocAsync(&c->scratch, cap * sizeof(long long), stream), "cudaMallocAsync(scratch)");
     c->scratch_cap = cap;
   }
+  // cursor path: spans of <= D new positions; longer ones (run-ahead) walk
+  const int32_t short_max = cursor ? c->cfg.max_depth : -1;
   SRT_CUDA(timed(c, SRT_K_INSERT_PLAN, stream,
                  [&] {
-                   return launch_insert_plan(c->dev, n, prompt_id, from, to, floor_, c->scratch,
-                                             stream);
+                   return launch_insert_plan(c->dev, n, prompt_id, from, to, floor_, short_max,
+                                             c->scratch, stream);
                  }),
            "insert plan");
   SRT_CUDA(timed(c, SRT_K_INSERT_WALK, stream,
@@ -173,7 +184,38 @@ srt_status srt_insert(srt_cache* c, int32_t n, const int32_t* prompt_id, const i
                                              floor_, stats_dev, c->scratch, stream);
                  }),
            "insert walk");
+  if (cursor)
+    SRT_CUDA(timed(c, SRT_K_INSERT_CURSOR, stream,
+                   [&] {
+                     return launch_insert_cursor(c->dev, n, prompt_id, seq_tok, stride, from, to,
+                                                 floor_, short_max, cursor, c->tag, stats_dev,
+                                                 stream);
+                   }),
+             "insert cursor");
   return SRT_OK;
+}
+}  // namespace
+
+srt_status srt_insert(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,
+                      int64_t stride, const int32_t* from, const int32_t* to,
+                      const int32_t* floor_, srt_insert_stats* stats_dev, void* stream_) {
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!prompt_id || !seq_tok || !from || !to) return SRT_ERR_INVALID_ARG;
+  return insert_impl(c, n, prompt_id, seq_tok, stride, from, to, floor_, nullptr, stats_dev,
+                     (cudaStream_t)stream_);
+}
+
+srt_status srt_insert_cursor(srt_cache* c, int32_t n, const int32_t* prompt_id,
+                             const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                             const int32_t* to, const int32_t* floor_, uint32_t* cursor,
+                             srt_insert_stats* stats_dev, void* stream_) {
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!prompt_id || !seq_tok || !from || !to || !cursor) return SRT_ERR_INVALID_ARG;
+  if (insert_cursor_smem(c->cfg.max_depth) > 200 * 1024) return SRT_ERR_INVALID_ARG;
+  return insert_impl(c, n, prompt_id, seq_tok, stride, from, to, floor_, cursor, stats_dev,
+                     (cudaStream_t)stream_);
 }
 
 srt_status srt_draft(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,

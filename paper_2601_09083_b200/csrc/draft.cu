@@ -16,7 +16,7 @@ namespace srt {
 
 namespace {
 
-constexpr int DRAFT_WARPS = 4;
+constexpr int DRAFT_WARPS = 2;  // 8K registers per CTA: fits beside a running verify scan
 
 // Development-only per-sequence profile (srt_debug_draft_profile): when set,
 // k_draft writes {match cycles, total cycles, children scanned, max children
@@ -392,7 +392,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   }
 }
 
-constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_THREADS = 256;  // small: co-resides with a running verify scan
 
 // row_offsets[s] = sum_{s' < s} (draft_len[s'] + 1)  (logits rows: root + nodes)
 __global__ void __launch_bounds__(SCAN_THREADS)
@@ -413,12 +413,12 @@ k_row_offsets(int32_t n, const int32_t* __restrict__ draft_len, int64_t* __restr
     if (lane == 31) warp_tot[wid] = x;
     __syncthreads();
     if (wid == 0) {
-      long long tt = warp_tot[lane];
+      long long tt = lane < SCAN_THREADS / 32 ? warp_tot[lane] : 0;
       for (int o = 1; o < 32; o <<= 1) {
         long long yv = __shfl_up_sync(0xffffffffu, tt, o);
         if (lane >= o) tt += yv;
       }
-      warp_tot[lane] = tt;
+      if (lane < SCAN_THREADS / 32) warp_tot[lane] = tt;
     }
     __syncthreads();
     const long long before = carry + (wid ? warp_tot[wid - 1] : 0) + x - w;
@@ -442,6 +442,7 @@ cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
                          int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
+  carveout_once<k_draft>();
   k_draft<<<(n + DRAFT_WARPS - 1) / DRAFT_WARPS, DRAFT_WARPS * 32, 0, stream>>>(
       c, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len, draft_len, draft_tok,
       draft_parent, draft_depth, draft_pos, draft_mask);
@@ -450,6 +451,7 @@ cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
 
 cudaError_t launch_row_offsets(int32_t n, const int32_t* draft_len, int64_t* row_offsets,
                                cudaStream_t stream) {
+  carveout_once<k_row_offsets>();
   k_row_offsets<<<1, SCAN_THREADS, 0, stream>>>(n, draft_len, row_offsets);
   return cudaGetLastError();
 }

@@ -17,7 +17,7 @@ namespace srt {
 
 namespace {
 
-constexpr int PLAN_THREADS = 1024;
+constexpr int PLAN_THREADS = 256;  // small: co-resides with a running verify scan
 
 __device__ __forceinline__ int32_t span_lo(int32_t from, int32_t floor_, int32_t D) {
   int32_t lo = from - D + 1;
@@ -30,7 +30,7 @@ __device__ __forceinline__ int32_t span_lo(int32_t from, int32_t floor_, int32_t
 __global__ void __launch_bounds__(PLAN_THREADS)
 k_insert_plan(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
               const int32_t* __restrict__ from, const int32_t* __restrict__ to,
-              const int32_t* __restrict__ floor_, long long* __restrict__ offs) {
+              const int32_t* __restrict__ floor_, int32_t short_max, long long* __restrict__ offs) {
   __shared__ long long warp_tot[PLAN_THREADS / 32];
   __shared__ long long carry;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -48,6 +48,8 @@ k_insert_plan(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         const int32_t lo = span_lo(from[s], fl, c.D);
         const int32_t hi = to[s];
         if (hi > from[s] && hi > lo) w = hi - lo;
+        // spans of <= short_max new positions go to the cursor kernel instead
+        if (short_max >= 0 && hi - max(from[s], fl) <= short_max) w = 0;
       }
     }
     long long x = w;  // inclusive warp scan
@@ -58,12 +60,12 @@ k_insert_plan(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     if (lane == 31) warp_tot[wid] = x;
     __syncthreads();
     if (wid == 0) {
-      long long t = warp_tot[lane];
+      long long t = lane < PLAN_THREADS / 32 ? warp_tot[lane] : 0;
       for (int o = 1; o < 32; o <<= 1) {
         long long y = __shfl_up_sync(0xffffffffu, t, o);
         if (lane >= o) t += y;
       }
-      warp_tot[lane] = t;  // inclusive over warps
+      if (lane < PLAN_THREADS / 32) warp_tot[lane] = t;  // inclusive over warps
     }
     __syncthreads();
     const long long before = carry + (wid ? warp_tot[wid - 1] : 0) + x - w;
@@ -139,7 +141,7 @@ __device__ __forceinline__ long long hash_acquire(const DevCache& c, unsigned lo
 // Wait for a pending slot's publication; returns val, *aux gets aux.
 __device__ __forceinline__ uint32_t wait_value(const HashSlot* s, uint32_t* aux) {
   unsigned long long v;
-  while ((uint32_t)(v = ld_acquire_u64(&s->val)) == NONE) __nanosleep(32);
+  while ((uint32_t)(v = ld_relaxed_u64((const unsigned long long*)&s->val)) == NONE) __nanosleep(32);
   *aux = (uint32_t)(v >> 32);
   return (uint32_t)v;
 }
@@ -227,6 +229,44 @@ __device__ __forceinline__ uint32_t get_or_create(const DevCache& c, uint32_t u,
   return id;
 }
 
+// get_or_create for a whole warp in lockstep (every lane calls it; inactive
+// lanes return BAD): the lanes that claimed a new edge take their node ids
+// with ONE atomic per warp, so the id counter sees 1/32 of the traffic.
+__device__ __forceinline__ uint32_t get_or_create_warp(const DevCache& c, bool active, uint32_t u,
+                                                       int32_t tk, uint32_t* pos,
+                                                       unsigned& created_ctr) {
+  bool created = false;
+  uint32_t v = NONE;
+  long long h = -1;
+  *pos = NONE;
+  if (active) {
+    h = hash_acquire(c, edge_key(u, (uint32_t)tk), &created, &v, pos);
+    if (h < 0) set_error(c, SRT_DEV_CAPACITY);
+  }
+  const unsigned need = __ballot_sync(0xffffffffu, created);
+  unsigned long long base = 0;
+  if (need) {
+    const int leader = __ffs(need) - 1;
+    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&c.ctr[0], (unsigned long long)__popc(need));
+    base = __shfl_sync(0xffffffffu, base, leader);
+  }
+  if (!active || h < 0) return BAD;
+  HashSlot* s = c.hash + h;
+  if (!created) return v != NONE ? v : wait_value(s, pos);
+  const unsigned long long idl = base + __popc(need & lanemask_lt());
+  if (idl + 1 > c.N) {
+    set_error(c, SRT_DEV_CAPACITY);
+    publish_slot(s, BAD, NONE);
+    return BAD;
+  }
+  const uint32_t id = (uint32_t)idl;
+  c.tok[id] = tk;
+  *pos = attach_child(c, u, id, tk);
+  publish_slot(s, id, *pos);
+  ++created_ctr;
+  return id;
+}
+
 __global__ void __launch_bounds__(256)
 k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
               const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
@@ -282,12 +322,135 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cursor insertion (srt_insert_cursor).  A sequence's cursor at position P
+// holds A_l = node(y[P-l .. P-1]) for l = 1..D (the suffix nodes).  Appending
+// y_P: A'_1 = child(root, y_P), A'_l = child(A_{l-1}, y_P), and every A'_l
+// (l <= min(D, P - floor + 1)) is exactly the node of a window ending at P, so
+// it gets +1.  That is one hop per window end instead of a root walk, and the
+// D hops of a position run in parallel across the lanes of the sequence's
+// warp.  An invalid cursor is rebuilt by walking the D-1 suffixes from the
+// root, which creates precisely the nodes the walk kernel creates for window
+// starts before P (uncounted), so both kernels build the same tree.
+// Cursor record (u32 words): [0] cache tag, [1] P, [2] prompt, [3] floor,
+// [4 .. 4+D) A_1 .. A_D (NONE = no node).
+// ---------------------------------------------------------------------------
+constexpr int CURSOR_WARPS = 4;
+
+__global__ void __launch_bounds__(CURSOR_WARPS * 32)
+k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
+                const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
+                const int32_t* __restrict__ to, const int32_t* __restrict__ floor_, int32_t short_max,
+                uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
+  extern __shared__ uint32_t cur_smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int32_t s = blockIdx.x * CURSOR_WARPS + w;
+  if (s >= n) return;
+  const int32_t D = c.D;
+  uint32_t* A = cur_smem + (size_t)w * (D + 1);  // A[l], l = 1..D; A[0] = root
+  uint32_t* cur = cursor + (size_t)s * (D + 4);
+  const int32_t p = prompt_id[s];
+  if (p < 0 || p >= c.P) return;  // flagged by the plan kernel
+  const int32_t f = from[s], t_end = to[s];
+  const int32_t fl = floor_ ? floor_[s] : 0;
+  const int32_t P = max(f, fl);
+  if (t_end <= P) return;  // no window ends at a new position: cursor untouched
+  if (t_end - P > short_max) {  // long span: the walk kernel inserts it
+    if (lane == 0) cur[1] = NONE;  // and the cursor must be rebuilt next time
+    return;
+  }
+  const int32_t* y = seq_tok + (int64_t)s * stride;
+  unsigned incs = 0, created = 0;
+  const bool valid = cur[0] == tag && cur[1] == (uint32_t)P && cur[2] == (uint32_t)p &&
+                     cur[3] == (uint32_t)fl;
+  if (lane == 0) A[0] = (uint32_t)p;
+  if (valid) {
+    for (int32_t l = 1 + lane; l <= D; l += 32) A[l] = cur[4 + l - 1];
+  } else {
+    // rebuild: A_l for l <= min(D-1, P-floor) by walking y[P-l .. P-1] from the
+    // root (creating missing nodes, counting nothing: these windows end < P)
+    const int32_t lmax = min(D - 1, P - max(fl, 0));
+    for (int32_t l = 1 + lane; l <= D; l += 32) {
+      uint32_t u = NONE;
+      if (l <= lmax) {
+        u = (uint32_t)p;
+        for (int32_t j = P - l; j < P; ++j) {
+          const int32_t tk = y[j];
+          if (tk < 0 || tk >= c.V) {
+            set_error(c, SRT_DEV_OOV);
+            u = NONE;
+            break;
+          }
+          uint32_t pos;
+          u = get_or_create(c, u, tk, &pos, created);
+          if (u >= BAD) {
+            u = NONE;
+            break;
+          }
+        }
+      }
+      A[l] = u;
+    }
+  }
+  __syncwarp();
+  const int ngroups = (D + 31) >> 5;
+  for (int32_t j = P; j < t_end; ++j) {
+    const int32_t tk = y[j];
+    const bool oov = tk < 0 || tk >= c.V;
+    if (oov && lane == 0) set_error(c, SRT_DEV_OOV);
+    const int32_t lim = min(D, j - max(fl, 0) + 1);  // windows ending at j start >= floor
+    // descending groups: group g reads A[32g .. 32g+31] (old) before group g-1
+    // overwrites A[32g - 32 + 1 .. 32g]
+    for (int g = ngroups - 1; g >= 0; --g) {
+      const int32_t l = 32 * g + lane + 1;
+      uint32_t par = NONE;
+      if (l <= D) par = A[l - 1];
+      __syncwarp();
+      const bool active = l <= D && !oov && l <= lim && par < BAD;
+      uint32_t pos;
+      const uint32_t ch = get_or_create_warp(c, active, par, tk, &pos, created);
+      if (active && ch < BAD) {
+        atomicAdd(&c.cnt[ch], 1u);
+        if (pos < BAD) atomicAdd(&c.scnt[pos], 1u);
+        atomicAdd(&c.rec[par].w, 1u);
+        ++incs;
+      }
+      if (l <= D) A[l] = (active && ch < BAD) ? ch : NONE;
+      __syncwarp();
+    }
+  }
+  for (int32_t l = 1 + lane; l <= D; l += 32) cur[4 + l - 1] = A[l];
+  if (lane == 0) {
+    cur[0] = tag;
+    cur[1] = (uint32_t)t_end;
+    cur[2] = (uint32_t)p;
+    cur[3] = (uint32_t)fl;
+  }
+  if (stats) {
+    unsigned long long b = incs, d = created;
+    for (int o = 16; o; o >>= 1) {
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    if (lane == 0) {
+      // window starts the walk kernel would have walked for this span
+      const int32_t lo = span_lo(f, fl, D);
+      atomicAdd(&stats->windows, (unsigned long long)(t_end - lo));
+      atomicAdd(&stats->increments, b);
+      if (d) atomicAdd(&stats->nodes_created, d);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_insert_plan(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                const int32_t* from, const int32_t* to, const int32_t* floor_,
-                               long long* scratch, cudaStream_t stream) {
-  k_insert_plan<<<1, PLAN_THREADS, 0, stream>>>(c, n, prompt_id, from, to, floor_, scratch);
+                               int32_t short_max, long long* scratch, cudaStream_t stream) {
+  carveout_once<k_insert_plan>();
+  k_insert_plan<<<1, PLAN_THREADS, 0, stream>>>(c, n, prompt_id, from, to, floor_, short_max,
+                                                scratch);
   return cudaGetLastError();
 }
 
@@ -295,8 +458,28 @@ cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prom
                                const int32_t* seq_tok, int64_t stride, const int32_t* from,
                                const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
                                const long long* scratch, cudaStream_t stream) {
+  carveout_once<k_insert_walk>();
   k_insert_walk<<<num_sms() * 8, 256, 0, stream>>>(c, n, prompt_id, seq_tok, stride, from, to,
                                                    floor_, scratch, stats);
+  return cudaGetLastError();
+}
+
+size_t insert_cursor_smem(int32_t D) { return (size_t)CURSOR_WARPS * (D + 1) * 4; }
+
+cudaError_t launch_insert_cursor(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                                 const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                                 const int32_t* to, const int32_t* floor_, int32_t short_max,
+                                 uint32_t* cursor, uint32_t tag, srt_insert_stats* stats,
+                                 cudaStream_t stream) {
+  const size_t smem = insert_cursor_smem(c.D);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_insert_cursor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  carveout_once<k_insert_cursor>();
+  k_insert_cursor<<<(n + CURSOR_WARPS - 1) / CURSOR_WARPS, CURSOR_WARPS * 32, smem, stream>>>(
+      c, n, prompt_id, seq_tok, stride, from, to, floor_, short_max, cursor, tag, stats);
   return cudaGetLastError();
 }
 

@@ -14,11 +14,12 @@
 //   stok[W], scnt[W]  the token and a mirror of the count of the child in each
 //                   slot, so a node's children enumerate with coalesced loads
 // Concurrency: insertion creates nodes with a CAS on the hash key and publishes
-// the value with a release store; counts are atomic adds, so the logical tree
+// the value with one 64-bit store (polled by racing threads); counts are atomic adds, so the logical tree
 // (set of (path, count)) does not depend on scheduling.  Node ids do, but no
 // output exposes them (draft order uses counts + tokens only; O8/O15).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/srt.h"
@@ -100,10 +101,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const void* p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-// Publish a hash slot's (val, aux) pair with one release store.
+// Publish a hash slot's (val, aux) pair with one 64-bit store.  Relaxed is
+// enough: within an insert kernel a waiter needs only these two words (the
+// creator's other writes -- tok, child-0 fields, slot mirrors -- are read by
+// later kernels only, and counts are atomics on zero-initialised memory), and
+// kernel boundaries order everything for the readers.
 __device__ __forceinline__ void publish_slot(HashSlot* s, uint32_t val, uint32_t aux) {
   const unsigned long long v = ((unsigned long long)aux << 32) | val;
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&s->val), "l"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(&s->val), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ void set_error(const DevCache& c, uint32_t bits) {
@@ -169,6 +174,19 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Tree kernels may ask for the max-shared-memory L1 carveout, the one the
+// verify scan runs with, so that their CTAs can co-reside with a running scan
+// of another cache (env SRT_CARVEOUT=1; bench.py's pipelined schedule).
+template <auto K>
+inline void carveout_once() {
+  static const bool done = [] {
+    if (std::getenv("SRT_CARVEOUT"))
+      cudaFuncSetAttribute((const void*)K, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)done;
+}
+
 // ---------------------------------------------------------------------------
 // Launchers (defined in the .cu files; all enqueue on `stream`)
 // ---------------------------------------------------------------------------
@@ -178,7 +196,13 @@ cudaError_t launch_noise_table(float* out, cudaStream_t stream);
 int num_sms();
 cudaError_t launch_insert_plan(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                const int32_t* from, const int32_t* to, const int32_t* floor_,
-                               long long* scratch, cudaStream_t stream);
+                               int32_t short_max, long long* scratch, cudaStream_t stream);
+cudaError_t launch_insert_cursor(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                                 const int32_t* seq_tok, int64_t stride, const int32_t* from,
+                                 const int32_t* to, const int32_t* floor_, int32_t short_max,
+                                 uint32_t* cursor, uint32_t tag, srt_insert_stats* stats,
+                                 cudaStream_t stream);
+size_t insert_cursor_smem(int32_t D);
 cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                const int32_t* seq_tok, int64_t stride, const int32_t* from,
                                const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,

@@ -203,6 +203,7 @@ cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference, 
 
 cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, const unsigned long long* result,
                           cudaStream_t stream) {
+  carveout_once<k_accept>();
   k_accept<<<(a.n + ACC_WARPS - 1) / ACC_WARPS, ACC_WARPS * 32, 0, stream>>>(c, a, result);
   return cudaGetLastError();
 }

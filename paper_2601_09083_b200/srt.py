@@ -120,14 +120,26 @@ class SrtCache:
             pass
 
     # ---- the hot path -------------------------------------------------------
-    def insert(self, prompt_id, seq_tok, frm, to, floor=None, stats=None) -> None:
+    def insert(self, prompt_id, seq_tok, frm, to, floor=None, stats=None, cursor=None) -> None:
+        """srt_insert, or srt_insert_cursor when `cursor` (see new_cursors) is given."""
         n = prompt_id.shape[0]
         i32 = torch.int32
-        check(self.L.srt_insert(self._h, n, _ptr(prompt_id, i32, "prompt_id"),
-                                _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
-                                _ptr(frm, i32, "from"), _ptr(to, i32, "to"),
-                                _ptr(floor, i32, "floor"), _ptr(stats, torch.int64, "stats"),
-                                _stream()), "srt_insert")
+        args = [self._h, n, _ptr(prompt_id, i32, "prompt_id"), _ptr(seq_tok, i32, "seq_tok"),
+                seq_tok.shape[1], _ptr(frm, i32, "from"), _ptr(to, i32, "to"),
+                _ptr(floor, i32, "floor")]
+        if cursor is None:
+            check(self.L.srt_insert(*args, _ptr(stats, torch.int64, "stats"), _stream()),
+                  "srt_insert")
+        else:
+            if cursor.shape != (n, self.cfg.max_depth + 4):
+                raise ValueError(f"cursor must be ({n}, D + 4) int32")
+            check(self.L.srt_insert_cursor(*args, _ptr(cursor, i32, "cursor"),
+                                           _ptr(stats, torch.int64, "stats"), _stream()),
+                  "srt_insert_cursor")
+
+    def new_cursors(self, n: int, device="cuda"):
+        """Zero-filled (= invalid, rebuilt on first use) insert cursors for n sequences."""
+        return torch.zeros((n, self.cfg.max_depth + 4), dtype=torch.int32, device=device)
 
     def draft(self, prompt_id, seq_tok, seq_len, pos_base=None, out: DraftOut | None = None
               ) -> DraftOut:

@@ -38,14 +38,13 @@ class Pair:
         return x.cuda()
 
     # -- insert on both ------------------------------------------------------
-    def insert(self, prompt_id, seq_tok, frm, to, floor=None):
-        torch = self.torch
+    def insert(self, prompt_id, seq_tok, frm, to, floor=None, cursor=None, stats=None):
         n = len(prompt_id)
         fl = np.zeros(n, np.int32) if floor is None else np.asarray(floor, np.int32)
         self.orc.insert(prompt_id, seq_tok, frm, to, fl)
         self.gpu.insert(self.t(np.asarray(prompt_id, np.int32)), self.t(np.asarray(seq_tok, np.int32)),
                         self.t(np.asarray(frm, np.int32)), self.t(np.asarray(to, np.int32)),
-                        self.t(fl))
+                        self.t(fl), cursor=cursor, stats=stats)
 
     def compare_trees(self):
         for p in range(self.P):

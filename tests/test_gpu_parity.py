@@ -66,6 +66,57 @@ def test_insert_parity(orc, seed):
     assert st["nodes_used"] == P + pair.orc.node_count
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_insert_cursor_parity(orc, seed):
+    """srt_insert_cursor builds the same tree as the oracle (and the same stats
+    as srt_insert) over many lockstep steps, including spans longer than D (walk
+    path), skipped positions, floors that change, records handed to another
+    prompt, garbage records and D > 32 (several lane groups)."""
+    import torch
+    import paper_2601_09083_b200 as srt
+    rng = np.random.default_rng(300 + seed)
+    V = [4, 30, 500][seed % 3]
+    D = [1, 3, 8, 16, 40, 70][seed]
+    P, n, T = 3, 24, 260
+    pair = Pair(orc, V, P, D, min(D, 4), 8, node_capacity=1 << 18)
+    plain = srt.SrtCache(srt.config(V, P, D, min(D, 4), 8, node_capacity=1 << 18))
+    toks = rng.integers(0, V, (n, T)).astype(np.int32)
+    tk = torch.from_numpy(toks).cuda()
+    prompt = rng.integers(0, P, n).astype(np.int32)
+    floor = np.where(rng.random(n) < 0.3, rng.integers(0, 6, n), 0).astype(np.int32)
+    cur = pair.gpu.new_cursors(n)
+    pos = np.zeros(n, np.int32)
+    st_c = torch.zeros(3, dtype=torch.int64, device="cuda")
+    st_p = torch.zeros(3, dtype=torch.int64, device="cuda")
+    for step in range(40):
+        grow = rng.choice([0, 1, 1, 2, 3, 5], n)
+        if step % 9 == 4:
+            grow[rng.integers(0, n)] = D + 1 + int(rng.integers(0, 5))  # long span: walk path
+        frm = pos.copy()
+        if step % 7 == 3:
+            k = rng.integers(0, n)
+            frm[k] = min(pos[k] + 2, T)  # skipped positions: the record no longer matches
+        if step % 11 == 5:
+            k = rng.integers(0, n)
+            prompt[k] = (prompt[k] + 1) % P  # record handed to another prompt
+        if step % 13 == 6:
+            k = rng.integers(0, n)
+            floor[k] = min(frm[k], floor[k] + 3)
+        if step % 17 == 8:
+            cur[rng.integers(0, n)] = torch.randint(-2**31, 2**31 - 1, (D + 4,), dtype=torch.int32)
+        to = np.minimum(frm + grow, T).astype(np.int32)
+        pair.insert(prompt, toks, frm, to, floor, cursor=cur, stats=st_c)
+        plain.insert(torch.from_numpy(prompt).cuda(), tk, torch.from_numpy(frm).cuda(),
+                     torch.from_numpy(to).cuda(), torch.from_numpy(floor).cuda(), stats=st_p)
+        pos = np.maximum(pos, to)
+    pair.compare_trees()
+    bits, _ = pair.gpu.status()
+    assert bits == 0
+    assert st_c.tolist() == st_p.tolist()
+    for p in range(P):
+        assert plain.dump(p) == pair.gpu.dump(p)
+
+
 def test_insert_repeat_is_deterministic(orc):
     """Concurrent CAS/atomics: the logical tree is identical across runs."""
     rng = np.random.default_rng(5)

@@ -50,10 +50,10 @@ def main():
         for s in slow:
             print(f"   slow seq {s}: cycles {tot[s]} match {mt[s]} q {q[s]} len {dl[s]} scanned {sc[s]} "
                   f"maxfan {mx[s]} rec {p[s,4]} blk {p[s,5]} ld {p[s,6]} ins {p[s,7]}")
-        run.standin(0)
+        run.standin()
         run.cache.verify(run.logits, run.d, run.seq_id, bench.step_seed(0, 100 + k), run.seq_tok,
                          run.seq_len, run.max_new, out=run.v)
-        run.cache.insert(run.prompt_id, run.seq_tok, run.t_before, run.seq_len)
+        run.cache.insert(run.prompt_id, run.seq_tok, run.t_before, run.seq_len, cursor=run.cursor)
     L.srt_debug_draft_profile(ctypes.c_void_p(0))
 
 

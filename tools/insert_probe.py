@@ -1,0 +1,62 @@
+"""Insert-kernel probe (development tool): how srt_insert_cursor time depends
+on the span length m (every sequence appends m ground-truth tokens), and the
+commit-length distribution of real steps.
+
+    python tools/insert_probe.py [--config grpo]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def timed(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1000.0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="grpo")
+    a = ap.parse_args()
+    cfg = bench.CONFIGS[a.config]
+    wl = bench.Workload(cfg, 0)
+    run = bench.GpuRun(wl, "bf16", "rl-mix", 0)
+    for k in range(4):
+        run.step(bench.step_seed(0, k))
+        nc = run.v.n_commit.cpu().numpy()
+        print(f"step {k}: n_commit mean {nc.mean():.2f} p90 {np.percentile(nc, 90):.0f} "
+              f"p99 {np.percentile(nc, 99):.0f} max {nc.max()}")
+    n = run.n
+    ar = torch.arange(n, device=run.dev)
+    for m in (1, 2, 4, 8, 16, 24, 32):
+        for mode in ("cursor", "walk"):
+            tok = run.seq_tok.clone()
+            t0 = run.seq_len.clone()
+            cur = run.cursor.clone()
+            pos = t0.to(torch.int64)[:, None] + torch.arange(m, device=run.dev)[None, :]
+            src = torch.minimum(pos, run.truth_last[:, None])
+            tok[ar[:, None], pos.clamp(max=tok.shape[1] - 1)] = torch.gather(run.truth, 1, src)
+            to = (t0 + m).clamp(max=tok.shape[1])
+            if mode == "cursor":
+                us = timed(lambda: run.cache.insert(run.prompt_id, tok, t0, to, cursor=cur))
+            else:
+                us = timed(lambda: run.cache.insert(run.prompt_id, tok, t0, to))
+            print(f"m={m:2d} {mode:6s}: {us:8.1f} us")
+    bits, st = run.cache.status()
+    print("status", bits, st)
+
+
+if __name__ == "__main__":
+    main()

@@ -7,7 +7,7 @@ wl = bench.Workload(cfg, 0)
 run = bench.GpuRun(wl, "bf16", "rl-mix", 0)
 for k in range(2):
     run.cache.draft(run.prompt_id, run.seq_tok, run.seq_len, run.seq_len, out=run.d)
-    run.standin(k)
+    run.standin()
     torch.cuda.synchronize()
     rows = run.d.row_offsets.cpu().numpy(); t = run.seq_len.cpu().numpy()
     for s in range(4):
