@@ -136,17 +136,17 @@ def owned_prompts(rank: int, world: int, count: int):
 
 
 class Workload:
-    def __init__(self, cfg: dict, seed: int, rank: int = 0, world: int = 1):
+    def __init__(self, cfg: dict, seed: int, rank: int = 0, world: int = 1, prompt_ids=None):
         from synth import make_workload
         self.cfg = cfg
         t = time.time()
-        gp = owned_prompts(rank, world, cfg["prompts"])
+        gp = list(prompt_ids) if prompt_ids is not None else owned_prompts(rank, world, cfg["prompts"])
         self.global_prompts = gp
         w = make_workload(seed + 1000003 * gp[0], cfg["V"], cfg["prompts"], cfg["samples"],
                           cfg["median"], cfg["cap"], prior_epochs=cfg["prior_epochs"],
                           active=cfg["active"])
         self.w = w
-        rng = np.random.default_rng(seed + 7)
+        rng = np.random.default_rng(seed + 7 + gp[0])
         # every active sequence starts part-way into its rollout (steady state):
         # t0 ~ U[0, len/2], its prefix already committed and inserted online
         self.truth = w.truth
@@ -278,10 +278,10 @@ class Group:
     def draft(self):
         self.cache.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d)
 
-    def verify_insert(self, seed: int):
+    def verify_insert(self, seed: int, logits=None):
         c = self.cache
-        c.verify(self.logits, self.d, self.seq_id, seed, self.seq_tok, self.seq_len, self.max_new,
-                 out=self.v, rows=self.rows_max)
+        c.verify(self.logits if logits is None else logits, self.d, self.seq_id, seed, self.seq_tok,
+                 self.seq_len, self.max_new, out=self.v, rows=self.rows_max)
         c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len, cursor=self.cursor)
 
 
@@ -380,6 +380,163 @@ class GpuRun:
         return bits, tot
 
 
+class ShardedRun:
+    """One rank of the hash-sharded multi-GPU step (SURVEY
+    §8(e)): global prompt blocks of cfg["prompts"] prompts, block b decoded by
+    rank b (contiguous, prompt-major); prompt p's tree on owner(p) =
+    splitmix64(p) mod G with a mirror of its sequences; drafts returned and
+    committed spans sent to the owners by NCCL all-gathers every step."""
+
+    def __init__(self, cfg: dict, seed: int, rank: int, world: int, dtype: str, profile: str,
+                 gather=None):
+        import torch
+        import paper_2601_09083_b200 as srt
+        from paper_2601_09083_b200.dist import GpuOps, ShardPlan, ShardedStep, all_gather_rows
+        self.torch = torch
+        self.cfg = cfg
+        t = time.time()
+        npb = cfg["prompts"]
+        blocks = [Workload(cfg, seed, prompt_ids=range(b * npb, (b + 1) * npb)) for b in range(world)]
+        S_b = cfg["active"]
+        seq_prompt = np.concatenate([b.seq_prompt.astype(np.int64) + i * npb
+                                     for i, b in enumerate(blocks)])
+        plan = ShardPlan.build(seq_prompt, world)
+        self.plan = plan
+        assert all(len(plan.local[r]) == S_b for r in range(world))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        V, B = cfg["V"], cfg["Bmax"]
+        self.V, self.Bmax = V, B
+        self.ldtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        i32 = dict(dtype=torch.int32, device=dev)
+
+        def seq_data(g):  # global sequence g -> (block, index in block)
+            return blocks[g // S_b], g % S_b
+
+        # ---- owner side: trees of the owned prompts + mirror of their sequences
+        owned = plan.prompts[rank]
+        c = srt.config(V, max(1, len(owned)), cfg["D"], cfg["L"], B,
+                       node_capacity=cfg["node_capacity"], logits_dtype=self.ldtype)
+        self.cache = srt.SrtCache(c)
+        cap = cfg["cap"]
+        prior = [(int(np.searchsorted(owned, b * npb + p)), tk)
+                 for b, blk in enumerate(blocks) for p, tk in blk.w.prior
+                 if owner_of_global(b * npb + p, world) == rank]
+        for i0 in range(0, len(prior), 4096):
+            part = prior[i0:i0 + 4096]
+            tab = np.zeros((len(part), cap), np.int32)
+            for i, (_, tk) in enumerate(part):
+                tab[i, :len(tk)] = tk
+            self.cache.insert(torch.tensor([p for p, _ in part], **i32), torch.from_numpy(tab).to(dev),
+                              torch.zeros(len(part), **i32),
+                              torch.tensor([len(tk) for _, tk in part], **i32))
+        stride = cfg["act_cap"] + B + 2
+        mirror = plan.mirror[rank]
+        nm = len(mirror)
+        mtab = np.zeros((max(1, nm), stride), np.int32)
+        mlen = np.zeros(max(1, nm), np.int32)
+        for j, g in enumerate(mirror):
+            blk, i = seq_data(g)
+            mtab[j, :blk.t0[i]] = blk.truth[i][:blk.t0[i]]
+            mlen[j] = blk.t0[i]
+        self.m_tok = torch.from_numpy(mtab[:nm]).to(dev)
+        self.m_len = torch.from_numpy(mlen[:nm]).to(dev)
+        self.m_prompt = torch.from_numpy(plan.mirror_prompt[rank]).to(dev)
+        self.m_cursor = self.cache.new_cursors(nm, dev)
+        self.m_draft = srt.DraftOut.empty(nm, B, dev)
+        if nm:
+            self.cache.insert(self.m_prompt, self.m_tok, torch.zeros(nm, **i32), self.m_len,
+                              cursor=self.m_cursor)
+        # ---- decode side: the local block's sequences (same layout as Group)
+        blk = blocks[rank]
+        n = S_b
+        self.n = n
+        tab = np.zeros((n, stride), np.int32)
+        truth = np.zeros((n, cfg["act_cap"]), np.int32)
+        for j in range(n):
+            tr = blk.truth[j]
+            tab[j, :blk.t0[j]] = tr[:blk.t0[j]]
+            truth[j, :len(tr)] = tr
+            truth[j, len(tr):] = tr[-1]
+        self.seq_tok = torch.from_numpy(tab).to(dev)
+        self.seq_len = torch.from_numpy(blk.t0.copy()).to(dev)
+        self.t_before = self.seq_len.clone()
+        self.truth = torch.from_numpy(truth).to(dev)
+        self.truth_last = torch.from_numpy(np.maximum(blk.max_new - 1, 0)).to(dev).to(torch.int64)
+        self.max_new = torch.from_numpy(blk.max_new).to(dev)
+        self.seq_id = torch.from_numpy(blk.seq_id.view(np.int64)).to(dev)
+        self.rows_max = n * (B + 1)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed + rank)
+        self.logits = torch.empty(self.rows_max + 1, V, dtype=self.ldtype, device=dev)
+        for r0 in range(0, self.rows_max + 1, 2048):
+            r1 = min(self.rows_max + 1, r0 + 2048)
+            if profile == "flat":
+                self.logits[r0:r1].uniform_(0, 1, generator=gen)
+            else:
+                self.logits[r0:r1].normal_(0.0, 2.0, generator=gen)
+        from synth import head_profile
+        gaps, offs = head_profile(np.random.default_rng(seed + 3 + rank), self.rows_max + 1,
+                                  profile if profile != "flat" else "moderate")
+        self.gaps = torch.from_numpy(gaps.astype(np.float32)).to(dev)
+        self.offs = torch.from_numpy(offs.astype(np.float32)).to(dev)
+        self.profile = profile
+        self.flat_logits = self.logits.view(-1)
+        self.d = srt.DraftOut.empty(n, B, dev)
+        self.v = srt.VerifyOut.empty(n, self.rows_max, B, dev)
+        self.slot = torch.arange(B + 1, device=dev, dtype=torch.int64)
+        self.mod_idx = torch.zeros(n * (B + 1) * 4, dtype=torch.int64, device=dev)
+        self.mod_val = self.flat_logits[self.mod_idx].clone()
+        # ---- the exchange
+        ops = GpuOps(self.cache, B, self.m_prompt, self.m_tok, self.m_len, self.m_cursor,
+                     self.m_draft, self.d, self.seq_len, self.v)
+        self.ex = ShardedStep(plan, rank, ops, gather or all_gather_rows, B, device=dev)
+        bits, st = self.cache.status()
+        if bits:
+            raise RuntimeError(f"cache error bits {bits} after warm-up inserts ({st})")
+        self.tree_stats = st
+        torch.cuda.synchronize()
+        log(f"[bench] rank {rank}/{world}: {len(owned)} owned prompts, {nm} mirror / {n} local "
+            f"sequences, tree nodes {st['nodes_used']:,}; setup {time.time() - t:.1f}s")
+
+    standin = Group.standin
+
+    def draft(self):
+        self.ex.draft()
+
+    def verify_insert(self, seed: int, logits=None):
+        self.cache.verify(self.logits if logits is None else logits, self.d, self.seq_id, seed,
+                          self.seq_tok, self.seq_len, self.max_new, out=self.v, rows=self.rows_max)
+        self.ex.commit()
+
+    def step(self, seed: int, ev=None):
+        """draft (owner) -> draft return -> [stand-in] -> verify -> span
+        all-gather -> owner insert.  ev = 4 events (stand-in excluded)."""
+        if ev:
+            ev[0].record()
+        self.draft()
+        if ev:
+            ev[1].record()
+        self.standin()
+        if ev:
+            ev[2].record()
+        self.verify_insert(seed)
+        if ev:
+            ev[3].record()
+
+    @property
+    def groups(self):
+        return [self]
+
+    def status(self):
+        return self.cache.status()
+
+
+def owner_of_global(p: int, world: int) -> int:
+    from paper_2601_09083_b200.dist import owner_of
+    return owner_of(p, world)
+
+
 def step_seed(run_seed: int, k: int) -> int:
     from synth import splitmix64
     return splitmix64(run_seed ^ k)
@@ -437,7 +594,7 @@ def oracle_sample_steps(wl: Workload, dtype: str, steps: int, n_prompts_sample: 
         t_c = time.perf_counter()
         t0 = seq_len.copy()
         v = o.verify(host, d["row_offsets"], d["draft_len"], d["draft_tok"], d["draft_parent"],
-                     d["draft_depth"], wl.seq_id[seqs], step_seed(seed, k), seq_tok, seq_len,
+                     d["draft_depth"], wl.seq_id[seqs], step_seed(seed, 0), seq_tok, seq_len,
                      wl.max_new[seqs])
         o.insert(prompt, seq_tok, t0, seq_len)
         t_d = time.perf_counter()
@@ -464,6 +621,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-prompts", type=int, default=0, help="oracle sample size in prompts")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="N=1: run the multi-GPU exchange path (owner draft, draft return, span "
+                         "all-gather) on one rank")
     ap.add_argument("--groups", type=int, default=1,
                     help="prompt groups pipelined on separate streams (1 = sequential; >1 measured slower: the latency-bound tree kernels stall behind the scan's HBM traffic)")
     args = ap.parse_args()
@@ -512,9 +672,16 @@ def main():
         build.build()
     if world > 1:
         dist.barrier()
-    wl = Workload(cfg, args.seed, rank, world)
-    run = GpuRun(wl, args.dtype, args.profile, args.seed + rank, groups=args.groups)
-    G = run.G
+    if world > 1 or args.sharded:
+        # hash-sharded trees + draft return / span all-gather
+        run = ShardedRun(cfg, args.seed, rank, world, args.dtype, args.profile,
+                         gather=None if world > 1 else (lambda t: t))
+        wl = None
+        G = 1
+    else:
+        wl = Workload(cfg, args.seed, rank, world)
+        run = GpuRun(wl, args.dtype, args.profile, args.seed + rank, groups=args.groups)
+        G = run.G
     pipelined = G > 1
     K, W = args.steps, args.warmup
     seed = step_seed(args.seed, 0)
@@ -616,6 +783,10 @@ def main():
                    "l2": "inputs larger than L2 (logits buffer "
                          f"{run.logits.numel() * esz / 1e9:.1f} GB)",
                    "groups": G,
+                   "placement": ("hash-sharded trees (owner = splitmix64(p) mod N), sequences "
+                                 "decoded on a contiguous split; per step an all-gather of draft "
+                                 "records (draft return) and of span records (before insertion)"
+                                 if (world > 1 or args.sharded) else "single rank"),
                    "timed": (f"whole step loop on the device (CUDA events, {G} prompt groups "
                              f"pipelined on {G} streams); forward stand-in and bookkeeping "
                              f"INCLUDED" if pipelined else
@@ -647,7 +818,7 @@ def main():
         out["clocks"] = cs
     if e2e:
         out["e2e"] = e2e
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and wl is not None:
         try:
             npr = args.cpu_prompts or max(1, min(cfg["prompts"], 64 // cfg["samples"]))
             bulk = run.logits[:npr * cfg["samples"] * (cfg["Bmax"] + 1)].float().cpu().numpy()
@@ -696,9 +867,7 @@ def e2e_leg(run: GpuRun, args, steps: int):
             gr.t_before.copy_(gr.seq_len)
             e[2].record()
             dev_rows[:rows].copy_(host[:rows], non_blocking=True)
-            gr.cache.verify(dev_rows, gr.d, gr.seq_id, seed, gr.seq_tok, gr.seq_len, gr.max_new,
-                            out=gr.v, rows=gr.rows_max)
-            gr.cache.insert(gr.prompt_id, gr.seq_tok, gr.t_before, gr.seq_len, cursor=gr.cursor)
+            gr.verify_insert(seed, dev_rows)
             out_n[:n].copy_(gr.v.n_commit, non_blocking=True)
             out_a[:n].copy_(gr.v.accept_len, non_blocking=True)
             out_c[:n].copy_(gr.v.commit_tok, non_blocking=True)

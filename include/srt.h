@@ -238,6 +238,58 @@ SRT_API srt_status srt_verify(srt_cache* cache, int32_t n, const void* logits,
                       int32_t* accepted_nodes, uint8_t* finished, void* stream);
 
 /*
+ * ---- Multi-GPU exchange records (BJ:north_star "prompts shard by hash across
+ * the GPUs ... decoded spans are NCCL all-gathered over NVLink before
+ * insertion").  A prompt's tree lives on its owner rank, which
+ * keeps a mirror of its sequences' response tokens and drafts for them; the
+ * drafts return to the decoding ranks and the committed spans go back to the
+ * owners.  Records are fixed-size int32 rows so that one all-gather moves a
+ * whole batch; these calls only pack, route and unpack them (stateless, no
+ * cache needed).  All pointers are DEVICE pointers.
+ *
+ * Draft record (SRT_DRAFT_RECORD_WORDS(Bmax) words): [0] match_len, [1]
+ * draft_len, then Bmax each of draft_tok, draft_parent, draft_depth, and the
+ * low and high words of draft_mask.  (Positions are re-derived from the
+ * receiving rank's pos_base.)
+ * Span record (SRT_SPAN_RECORD_WORDS(Bmax) words): [0] n_commit, [1 ..]
+ * commit_tok (Bmax + 1 words).
+ */
+#define SRT_DRAFT_RECORD_WORDS(Bmax) (2 + 5 * (Bmax))
+#define SRT_SPAN_RECORD_WORDS(Bmax) ((Bmax) + 2)
+
+/* records[s] <- the draft of sequence s < n (srt_draft's outputs). */
+SRT_API srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
+                           const int32_t* draft_len, const int32_t* draft_tok,
+                           const int32_t* draft_parent, const int32_t* draft_depth,
+                           const uint64_t* draft_mask, int32_t* records, void* stream);
+
+/*
+ * For s < n: unpack records[src[s]] into sequence s's draft outputs, with
+ * draft_pos = pos_base[s] + depth (pos_base may be NULL = 0), padding as
+ * srt_draft, and row_offsets[n+1] = exclusive scan of (draft_len + 1) -- the
+ * same outputs srt_draft would have written for these sequences.
+ */
+SRT_API srt_status srt_unpack_drafts(int32_t n, int32_t Bmax, const int32_t* records,
+                             const int32_t* src, const int32_t* pos_base, int32_t* match_len,
+                             int32_t* draft_len, int32_t* draft_tok, int32_t* draft_parent,
+                             int32_t* draft_depth, int32_t* draft_pos, uint64_t* draft_mask,
+                             int64_t* row_offsets, void* stream);
+
+/* records[s] <- {n_commit[s], commit_tok[s][0 .. Bmax]} (srt_verify's outputs). */
+SRT_API srt_status srt_pack_spans(int32_t n, int32_t Bmax, const int32_t* n_commit,
+                          const int32_t* commit_tok, int32_t* records, void* stream);
+
+/*
+ * Owner side: for mirror sequence m < n, append the k = records[src[m]][0]
+ * committed tokens to its row of the mirror table (seq_tok[m*stride ...],
+ * seq_len[m] += k, never past stride) and write the insertion span
+ * from[m] = old length, to[m] = new length for srt_insert / srt_insert_cursor.
+ */
+SRT_API srt_status srt_apply_spans(int32_t n, int32_t Bmax, const int32_t* records,
+                           const int32_t* src, int32_t* seq_tok, int64_t stride,
+                           int32_t* seq_len, int32_t* from, int32_t* to, void* stream);
+
+/*
  * srt_cache_dump — canonical serialization of T_p (BLOCKING; test path).
  * Preorder records, children in ascending token order.
  * host_buf (HOST pointer, capacity cap records) may be NULL to query the size;

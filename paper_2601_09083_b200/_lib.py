@@ -23,7 +23,8 @@ SRT_BF16, SRT_F32 = 0, 1
 EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache_destroy",
            "srt_insert", "srt_insert_cursor", "srt_draft", "srt_verify", "srt_cache_dump", "srt_cache_status",
            "srt_cache_clear_errors", "srt_noise_table", "srt_sample_rows_reference",
-           "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile"]
+           "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile",
+           "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
                 5: "accept", 6: "insert_cursor"}
 
@@ -77,6 +78,10 @@ def load() -> ctypes.CDLL:
     L.srt_cache_destroy.argtypes = [vp, vp]
     L.srt_insert.argtypes = [vp, i32, vp, vp, i64, vp, vp, vp, vp, vp]
     L.srt_insert_cursor.argtypes = [vp, i32, vp, vp, i64, vp, vp, vp, vp, vp, vp]
+    L.srt_pack_drafts.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.srt_unpack_drafts.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.srt_pack_spans.argtypes = [i32, i32, vp, vp, vp, vp]
+    L.srt_apply_spans.argtypes = [i32, i32, vp, vp, vp, i64, vp, vp, vp, vp]
     L.srt_draft.argtypes = [vp, i32, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.srt_verify.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, u64, f32, i32, vp, vp, i64,
                              vp, vp, vp, vp, vp, vp, vp, vp]

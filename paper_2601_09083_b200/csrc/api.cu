@@ -365,6 +365,62 @@ srt_status srt_debug_draft_profile(int64_t* dev_buf) {
   return SRT_OK;
 }
 
+// ---- multi-GPU exchange records (exchange.cu)
+srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
+                           const int32_t* draft_len, const int32_t* draft_tok,
+                           const int32_t* draft_parent, const int32_t* draft_depth,
+                           const uint64_t* draft_mask, int32_t* records, void* stream) {
+  if (n < 0 || Bmax < 1 || Bmax > 64) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!match_len || !draft_len || !draft_tok || !draft_parent || !draft_depth || !draft_mask ||
+      !records)
+    return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(launch_pack_drafts(n, Bmax, match_len, draft_len, draft_tok, draft_parent, draft_depth,
+                              draft_mask, records, (cudaStream_t)stream),
+           "pack drafts");
+  return SRT_OK;
+}
+
+srt_status srt_unpack_drafts(int32_t n, int32_t Bmax, const int32_t* records, const int32_t* src,
+                             const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                             int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
+                             int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
+                             void* stream) {
+  if (n < 0 || Bmax < 1 || Bmax > 64 || !row_offsets) return SRT_ERR_INVALID_ARG;
+  if (n > 0 && (!records || !src || !match_len || !draft_len || !draft_tok || !draft_parent ||
+                !draft_depth || !draft_pos || !draft_mask))
+    return SRT_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n > 0)
+    SRT_CUDA(launch_unpack_drafts(n, Bmax, records, src, pos_base, match_len, draft_len, draft_tok,
+                                  draft_parent, draft_depth, draft_pos, draft_mask, st),
+             "unpack drafts");
+  SRT_CUDA(launch_row_offsets(n, draft_len, row_offsets, st), "row offsets");
+  return SRT_OK;
+}
+
+srt_status srt_pack_spans(int32_t n, int32_t Bmax, const int32_t* n_commit,
+                          const int32_t* commit_tok, int32_t* records, void* stream) {
+  if (n < 0 || Bmax < 1 || Bmax > 64) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!n_commit || !commit_tok || !records) return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(launch_pack_spans(n, Bmax, n_commit, commit_tok, records, (cudaStream_t)stream),
+           "pack spans");
+  return SRT_OK;
+}
+
+srt_status srt_apply_spans(int32_t n, int32_t Bmax, const int32_t* records, const int32_t* src,
+                           int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* from,
+                           int32_t* to, void* stream) {
+  if (n < 0 || Bmax < 1 || Bmax > 64 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!records || !src || !seq_tok || !seq_len || !from || !to) return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(launch_apply_spans(n, Bmax, records, src, seq_tok, stride, seq_len, from, to,
+                              (cudaStream_t)stream),
+           "apply spans");
+  return SRT_OK;
+}
+
 srt_status srt_noise_table(float* out, void* stream) {
   if (!out) return SRT_ERR_INVALID_ARG;
   SRT_CUDA(launch_noise_table(out, (cudaStream_t)stream), "noise table");

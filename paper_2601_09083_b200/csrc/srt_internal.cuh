@@ -248,6 +248,19 @@ cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference, 
                         unsigned long long* result, cudaStream_t stream);
 cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, const unsigned long long* result,
                           cudaStream_t stream);
+cudaError_t launch_pack_drafts(int32_t n, int32_t B, const int32_t* match_len,
+                               const int32_t* draft_len, const int32_t* draft_tok,
+                               const int32_t* draft_parent, const int32_t* draft_depth,
+                               const uint64_t* draft_mask, int32_t* rec, cudaStream_t stream);
+cudaError_t launch_unpack_drafts(int32_t n, int32_t B, const int32_t* rec, const int32_t* src,
+                                 const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                                 int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
+                                 int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream);
+cudaError_t launch_pack_spans(int32_t n, int32_t B, const int32_t* n_commit,
+                              const int32_t* commit_tok, int32_t* rec, cudaStream_t stream);
+cudaError_t launch_apply_spans(int32_t n, int32_t B, const int32_t* rec, const int32_t* src,
+                               int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* from,
+                               int32_t* to, cudaStream_t stream);
 cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
                               uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,
                               uint32_t* out_cnt, uint32_t* out_nchild, unsigned int* out_n,

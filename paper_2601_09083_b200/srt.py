@@ -15,7 +15,9 @@ import torch
 from . import _lib
 from ._lib import SrtCacheStats, SrtConfig, SrtDumpRecord, SrtError, check
 
-__all__ = ["SrtCache", "DraftOut", "VerifyOut", "config", "noise_table", "SrtError"]
+__all__ = ["SrtCache", "DraftOut", "VerifyOut", "config", "noise_table", "SrtError",
+           "pack_drafts", "unpack_drafts", "pack_spans", "apply_spans", "draft_record_words",
+           "span_record_words"]
 
 _DT = {torch.bfloat16: _lib.SRT_BF16, torch.float32: _lib.SRT_F32}
 
@@ -229,6 +231,58 @@ class SrtCache:
         check(self.L.srt_cache_dump(self._h, prompt_id, buf, n.value, ctypes.byref(n), _stream()),
               "srt_cache_dump")
         return [(buf[i].token, int(buf[i].count), buf[i].n_children) for i in range(n.value)]
+
+
+# ---- multi-GPU exchange records (include/srt.h) ----------------
+def draft_record_words(Bmax: int) -> int:
+    return 2 + 5 * Bmax
+
+
+def span_record_words(Bmax: int) -> int:
+    return Bmax + 2
+
+
+def pack_drafts(d: DraftOut, Bmax: int, out: torch.Tensor) -> torch.Tensor:
+    """out[s] <- draft record of sequence s (out: [>= n, draft_record_words] int32)."""
+    n = d.draft_len.shape[0]
+    i32 = torch.int32
+    check(_lib.load().srt_pack_drafts(n, Bmax, _ptr(d.match_len, i32), _ptr(d.draft_len, i32),
+                                      _ptr(d.draft_tok, i32), _ptr(d.draft_parent, i32),
+                                      _ptr(d.draft_depth, i32), _ptr(d.draft_mask, torch.int64),
+                                      _ptr(out, i32, "records"), _stream()), "srt_pack_drafts")
+    return out
+
+
+def unpack_drafts(records: torch.Tensor, src: torch.Tensor, Bmax: int, out: DraftOut,
+                  pos_base=None) -> DraftOut:
+    n = out.draft_len.shape[0]
+    i32 = torch.int32
+    check(_lib.load().srt_unpack_drafts(n, Bmax, _ptr(records, i32, "records"), _ptr(src, i32, "src"),
+                                        _ptr(pos_base, i32, "pos_base"), _ptr(out.match_len, i32),
+                                        _ptr(out.draft_len, i32), _ptr(out.draft_tok, i32),
+                                        _ptr(out.draft_parent, i32), _ptr(out.draft_depth, i32),
+                                        _ptr(out.draft_pos, i32), _ptr(out.draft_mask, torch.int64),
+                                        _ptr(out.row_offsets, torch.int64), _stream()),
+          "srt_unpack_drafts")
+    return out
+
+
+def pack_spans(v: VerifyOut, Bmax: int, out: torch.Tensor) -> torch.Tensor:
+    n = v.n_commit.shape[0]
+    i32 = torch.int32
+    check(_lib.load().srt_pack_spans(n, Bmax, _ptr(v.n_commit, i32), _ptr(v.commit_tok, i32),
+                                     _ptr(out, i32, "records"), _stream()), "srt_pack_spans")
+    return out
+
+
+def apply_spans(records: torch.Tensor, src: torch.Tensor, Bmax: int, seq_tok: torch.Tensor,
+                seq_len: torch.Tensor, frm: torch.Tensor, to: torch.Tensor) -> None:
+    n = seq_len.shape[0]
+    i32 = torch.int32
+    check(_lib.load().srt_apply_spans(n, Bmax, _ptr(records, i32, "records"), _ptr(src, i32, "src"),
+                                      _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+                                      _ptr(seq_len, i32, "seq_len"), _ptr(frm, i32, "from"),
+                                      _ptr(to, i32, "to"), _stream()), "srt_apply_spans")
 
 
 def noise_table(device=None) -> torch.Tensor:
