@@ -34,10 +34,11 @@
  *
  * Data layout in HBM (owned by the cache): a node pool shared by
  * all prompts (node id p is the root of prompt p's tree T_p) as
- * structure-of-arrays (token, count, child count, first child inline, first
- * child block), an open-addressing edge hash ((parent << 32) | token -> child
- * id), and a pool of child-id blocks (4, 4, 8, 16, 32, 32, ... slots) holding
- * children 1.. for coalesced enumeration.
+ * structure-of-arrays (token, count, and a 16-byte record {child count, first
+ * child, its token, sum of the children's counts}), an open-addressing edge
+ * hash ((parent << 32) | token -> child id and its slot), and a pool of child
+ * slots in geometric blocks (4, 4, 8, 16, 32, 64, ... slots) holding children
+ * 1.. with their tokens and count mirrors for coalesced enumeration.
  */
 #ifndef SRT_H_
 #define SRT_H_
