@@ -690,6 +690,9 @@ def main():
             run.step_pipelined(seed)
         else:
             run.step(seed)
+        if os.environ.get("BENCH_ROWS_LOG"):  # profiling support: rows of each warm-up scan
+            log(f"[bench] warm-up step {k}: rows "
+                f"{[int(gr.d.row_offsets[-1].item()) for gr in run.groups]}")
     torch.cuda.synchronize()
     bits, _ = run.status()
     if bits:
@@ -766,10 +769,13 @@ def main():
     scan_bytes = float(rows.sum()) * cfg["V"] * esz
     peak, peak_kind = load_peaks()
     achieved = scan_bytes / (sum(scan_ms) / 1000.0) / 1e9 if scan_ms else None
-    traffic = None
+    traffic = traffic_ratio = None
     tf = os.path.join(ROOT, "profiles", f"scan_traffic_{args.config}_{args.dtype}.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get("bytes_per_launch")
+        tj = json.load(open(tf))
+        traffic = tj.get("bytes_per_launch")
+        if tj.get("algorithmic_bytes_same_launch"):
+            traffic_ratio = traffic / tj["algorithmic_bytes_same_launch"]
     value = world * K / (max_ms / 1000.0)
     kern = {k: {"launches": len(v), "mean_us": 1000 * float(np.mean(v)),
                 "share": float(sum(v) / sum(sum(x) for x in per_kernel.values()))}
@@ -801,6 +807,10 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "scan (k_scan_rows + k_rowinfo)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_over_algorithmic": traffic_ratio,
+                     "traffic_source": "one ncu --set full capture of k_scan_rows "
+                                       "(profiles/scan_traffic_*.json; its launch's rows differ "
+                                       "from this run's mean)",
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": scan_bytes / max(1, len(scan_ms)),
                      "frac_of_8TBps_spec": (achieved / 8000.0) if achieved else None},
