@@ -63,12 +63,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// non-suspending variant: poll with test_wait (a try_wait may park the warp
+// for a scheduler time slice after the phase completes)
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SPIN_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SPIN_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// same, with an L2 cache-policy hint (evict_first: streamed logits should not
+// displace the trees' hash and records from L2)
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 
@@ -135,7 +158,6 @@ __device__ __forceinline__ float block_max_scalar(const unsigned char* blk, int 
   return m;
 }
 
-constexpr uint32_t CHUNK = 32768;  // TMA chunk (bytes); a multiple of a block pair
 
 struct ScanParams {
   const void* logits;
@@ -149,11 +171,19 @@ struct ScanParams {
   int32_t nblk;                // ceil(V / 64)
   uint32_t sum_bytes;          // row summary bytes (nblk floats, 128-aligned)
   uint32_t debug;              // development only (SRT_SCAN_DEBUG=8 prints the launch)
+  uint32_t l2_hint;            // 0 = default policy, 1 = evict_first on the streamed rows
+  uint32_t spin;               // 1 = stream warps poll the ring with test_wait
 };
 
-// Warp roles: warp 0 = producer, warps 1..NSW = stream, the rest = tail.
-template <int DT, int NSW, int NT, int NST, int NS>
+// Warp roles: warp 0 = producer, warps 1..NSW = stream (NG groups taking
+// alternate chunks, so NG chunks are summarised at once), the rest = tail.
+template <int DT, int NSW, int NT, int NST, int NS, uint32_t CHUNK, int NG>
 __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c, ScanParams a) {
+  constexpr int GW = NSW / NG;  // warps per stream group
+  static_assert(NSW % NG == 0, "stream groups must be equal");
+  // each ring stage must always be consumed by the same group, in order: a
+  // parity wait cannot tell use k from use k + 2
+  static_assert(NST % NG == 0, "ring stages must map to one stream group each");
   constexpr int ESZ = DT == SRT_BF16 ? 2 : 4;
   constexpr int BLKB = NOISE_BLK * ESZ;  // bytes per block
   constexpr int PAIRB = 2 * BLKB;
@@ -169,7 +199,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   unsigned long long* p1key = reinterpret_cast<unsigned long long*>(sum_free + NS);  // [NS]
   unsigned long long* rowhdr = p1key + NS;                               // [NS]
   uint32_t* p1cnt = reinterpret_cast<uint32_t*>(rowhdr + NS);            // [NS]
-  float* tab = reinterpret_cast<float*>(p1cnt + ((NS + 3) & ~3));        // [1024]
+  uint32_t* rowM = p1cnt + ((NS + 3) & ~3);                              // [NS] shared M keys
+  float* tab = reinterpret_cast<float*>(rowM + ((NS + 3) & ~3));         // [1024]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t total = *a.total;
@@ -183,13 +214,14 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&ring_full[s], 1);
-      mbar_init(&ring_empty[s], NSW);
+      mbar_init(&ring_empty[s], GW);
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sum_ready[s], 1);
       mbar_init(&sum_free[s], NT);
       p1key[s] = 0;
       p1cnt[s] = 0;
+      rowM[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -198,6 +230,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   if (wid == 0) {
     // ===================== producer: the rows' chunks into the ring ========
     if (lane == 0) {
+      uint64_t pol = 0;
+      if (a.l2_hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       uint64_t kc = 0;
       for (int64_t row = blockIdx.x; row < total; row += gridDim.x) {
         const char* base = (const char*)a.logits + row * row_bytes;
@@ -208,7 +242,10 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
           const int64_t left = row_bytes - (int64_t)ch * CHUNK;
           const uint32_t nb = (uint32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
           mbar_arrive_expect_tx(&ring_full[s], nb);
-          tma_load_1d(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s]);
+          if (a.l2_hint)
+            tma_load_1d_hint(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s], pol);
+          else
+            tma_load_1d(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s]);
         }
       }
     }
@@ -217,7 +254,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
 
   if (wid <= NSW) {
     // ===================== stream: block bounds U_b, the row's max logit ====
-    const int w = wid - 1;
+    const int grp = (wid - 1) / GW, w = (wid - 1) % GW;
     uint64_t kc = 0;
     int64_t u = 0;
     for (int64_t row = blockIdx.x; row < total; row += gridDim.x, ++u) {
@@ -232,13 +269,15 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
       uint32_t tblk = 0xFFFFFFFFu;
       bool nan = false;
       for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
+        if (NG > 1 && (int)(kc % NG) != grp) continue;  // the other group's chunk
         const int s = (int)(kc % NST);
-        mbar_wait(&ring_full[s], (uint32_t)((kc / NST) & 1));
+        if (a.spin) mbar_spin(&ring_full[s], (uint32_t)((kc / NST) & 1));
+        else mbar_wait(&ring_full[s], (uint32_t)((kc / NST) & 1));
         const int64_t left = row_bytes - (int64_t)ch * CHUNK;
         const int32_t nb = (int32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
         const int32_t npairs = (nb + PAIRB - 1) / PAIRB;
         const unsigned char* st = ring + s * CHUNK;
-        for (int32_t pi = w * 32 + lane; pi < npairs; pi += NSW * 32) {
+        for (int32_t pi = w * 32 + lane; pi < npairs; pi += GW * 32) {
           const uint32_t gp = ch * PAIRS_PER_CHUNK + (uint32_t)pi;  // pair index in the row
           const int64_t e0 = (int64_t)gp * 2 * NOISE_BLK;             // first element
           const int nA = block_len(a.V, 2 * (int64_t)gp);
@@ -290,6 +329,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         if (atomicAdd(&p1cnt[sb], 1u) == NSW - 1) {  // the last stream warp publishes
           rowhdr[sb] = atomicExch(&p1key[sb], 0ull);
           p1cnt[sb] = 0;
+          rowM[sb] = 0u;  // the tail's shared bound for this row starts empty
           mbar_arrive(&sum_ready[sb]);  // release: the summary is complete
         }
       }
@@ -335,14 +375,86 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         }
         M = perturbed(X, g, T, unit_t);
       }
-      // every block whose bound reaches M is evaluated exactly by the whole
-      // warp (lane = 2 consecutive tokens, coalesced), BATCH blocks at a time
-      // so their L2 loads overlap
-      constexpr int BATCH = 4;
+      // Exact evaluation of block b by the whole warp (lane = 2 consecutive
+      // tokens, coalesced); the best (z, v) and M are raised as it goes.
+      auto eval_block = [&](int32_t b, float2 xx) {
+        const int n = block_len(a.V, b);
+        uint32_t wa, wb;
+        block_words((uint32_t)b, pos, s_lo, s_hi, k0, k1, wa, wb);
+        const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+        const float xs0 = unit_t ? xx.x : __fdiv_rn(xx.x, T);
+        const float xs1 = unit_t ? xx.y : __fdiv_rn(xx.y, T);
+        // g_v <= G_b: skip a token if even the block maximum cannot reach M
+        const bool n0 = __fadd_rn(xs0, bn.G) >= M, n1 = __fadd_rn(xs1, bn.G) >= M;
+        if (!(n0 || n1)) return;  // (NaN fails both tests)
+        const int64_t v = (int64_t)b * NOISE_BLK + 2 * lane;
+        const Philox4 pw = philox4x32_10((uint32_t)(v >> 2), pos, s_lo, s_hi, k0, k1);
+        const bool hi = (lane & 1) != 0;  // tokens 2l, 2l+1 are words 0,1 or 2,3
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (!(k ? n1 : n0)) continue;
+          const uint32_t j = 2 * lane + k;
+          const uint32_t wd = hi ? (k ? pw.w : pw.z) : (k ? pw.y : pw.x);
+          const float g = j == bn.p ? bn.G : element_noise_from_word(wd, bn);
+          const float z = __fadd_rn(k ? xs1 : xs0, g);
+          if (cand_better(z, (int32_t)(v + k), bz, bv)) {
+            bz = z;
+            bv = (int32_t)(v + k);
+            M = fmaxf(M, z);
+          }
+        }
+      };
+      auto load_block = [&](int32_t b) {
+        const int n = block_len(a.V, b);
+        const int64_t v = (int64_t)b * NOISE_BLK + 2 * lane;
+        float2 xx;
+        xx.x = 2 * lane < n ? load_x<DT>(rowp, v) : NAN;
+        xx.y = 2 * lane + 1 < n ? load_x<DT>(rowp, v + 1) : NAN;
+        return xx;
+      };
+      // the warp's M joins the row's shared bound; the row's best M comes back
+      auto share_M = [&]() {
+        const uint32_t wk = __reduce_max_sync(0xffffffffu, fkey(M));  // M is never NaN
+        if (lane == 0) atomicMax(&rowM[sb], wk);
+        __syncwarp();
+        const uint32_t k = *(volatile uint32_t*)&rowM[sb];
+        M = fmaxf(M, key_value(k));
+      };
       const int32_t nchunk = (a.nblk + 31) / 32;
+      // Phase 1 (branch and bound): each tail warp first evaluates the block
+      // of its share with the largest bound U_b, which usually holds a z near
+      // the row's maximum; the tail warps pool their M before phase 2, so far
+      // fewer blocks pass U_b >= M than against z(i*) alone.
+      int32_t b1 = -1;
+      {
+        uint32_t bu = 0;
+        int32_t bi = INT_MAX;
+        for (int32_t cb = t; cb < nchunk; cb += NT) {
+          const int32_t b = cb * 32 + lane;
+          if (b < a.nblk) {
+            const float ub = U[b];
+            if (ub >= M) {
+              const uint32_t k = fkey(ub);
+              if (k > bu) { bu = k; bi = b; }
+            }
+          }
+        }
+        const uint32_t wbu = __reduce_max_sync(0xffffffffu, bu);
+        const int32_t wbi = __reduce_min_sync(0xffffffffu, (wbu && bu == wbu) ? bi : INT_MAX);
+        if (wbu) {
+          b1 = wbi;
+          eval_block(b1, load_block(b1));
+        }
+      }
+      share_M();
+      asm volatile("bar.sync 1, %0;" ::"r"(NT * 32) : "memory");
+      share_M();
+      // Phase 2: every other block whose bound reaches M, BATCH at a time so
+      // their L2 loads overlap; M is re-pooled after each batch.
+      constexpr int BATCH = 4;
       for (int32_t cb = t; cb < nchunk; cb += NT) {
         const int32_t b = cb * 32 + lane;
-        unsigned surv = __ballot_sync(0xffffffffu, b < a.nblk && U[b] >= M);
+        unsigned surv = __ballot_sync(0xffffffffu, b < a.nblk && b != b1 && U[b] >= M);
         while (surv) {
           int32_t bb[BATCH];
           float2 xx[BATCH];
@@ -352,42 +464,18 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
             if (surv) {
               bb[i] = cb * 32 + __ffs(surv) - 1;
               surv &= surv - 1;
-              const int n = block_len(a.V, bb[i]);
-              const int64_t v = (int64_t)bb[i] * NOISE_BLK + 2 * lane;
-              xx[i].x = 2 * lane < n ? load_x<DT>(rowp, v) : NAN;
-              xx[i].y = 2 * lane + 1 < n ? load_x<DT>(rowp, v + 1) : NAN;
+              xx[i] = load_block(bb[i]);
             }
           }
 #pragma unroll
-          for (int i = 0; i < BATCH; ++i) {
-            if (bb[i] < 0) continue;
-            const int n = block_len(a.V, bb[i]);
-            uint32_t wa, wb;
-            block_words((uint32_t)bb[i], pos, s_lo, s_hi, k0, k1, wa, wb);
-            const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
-            const float xs0 = unit_t ? xx[i].x : __fdiv_rn(xx[i].x, T);
-            const float xs1 = unit_t ? xx[i].y : __fdiv_rn(xx[i].y, T);
-            // g_v <= G_b: skip a token if even the block maximum cannot reach M
-            const bool n0 = __fadd_rn(xs0, bn.G) >= M, n1 = __fadd_rn(xs1, bn.G) >= M;
-            if (!(n0 || n1)) continue;  // (NaN fails both tests)
-            const int64_t v = (int64_t)bb[i] * NOISE_BLK + 2 * lane;
-            const Philox4 pw = philox4x32_10((uint32_t)(v >> 2), pos, s_lo, s_hi, k0, k1);
-            const bool hi = (lane & 1) != 0;  // tokens 2l, 2l+1 are words 0,1 or 2,3
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              if (!(k ? n1 : n0)) continue;
-              const uint32_t j = 2 * lane + k;
-              const uint32_t wd = hi ? (k ? pw.w : pw.z) : (k ? pw.y : pw.x);
-              const float g = j == bn.p ? bn.G : element_noise_from_word(wd, bn);
-              const float z = __fadd_rn(k ? xs1 : xs0, g);
-              if (cand_better(z, (int32_t)(v + k), bz, bv)) {
-                bz = z;
-                bv = (int32_t)(v + k);
-                M = fmaxf(M, z);
-              }
-            }
+          for (int i = 0; i < BATCH; ++i)
+            if (bb[i] >= 0 && U[bb[i]] >= M) eval_block(bb[i], xx[i]);
+          if (surv) {
+            share_M();
+            surv &= __ballot_sync(0xffffffffu, b < a.nblk && U[b] >= M);
           }
         }
+        share_M();
       }
     }
     const unsigned long long mine = bv == INT_MAX ? 0ull : pack_cand(bz, bv);
@@ -420,13 +508,13 @@ __global__ void k_rowinfo(VerifyArgs a, int32_t Bmax, int2* rowinfo,
   }
 }
 
-template <int DT, int NSW, int NT, int NST, int NS>
+template <int DT, int NSW, int NT, int NST, int NS, uint32_t CHUNK, int NG>
 cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
   constexpr int THREADS = (1 + NSW + NT) * 32;
   const size_t smem = (size_t)NST * CHUNK + (size_t)NS * p.sum_bytes +
-                      (2 * NST + 2 * NS) * 8 + 2 * NS * 8 + ((NS + 3) & ~3) * 4 +
+                      (2 * NST + 2 * NS) * 8 + 2 * NS * 8 + 2 * ((NS + 3) & ~3) * 4 +
                       NOISE_BUCKETS * 4;
-  auto kern = k_scan_rows<DT, NSW, NT, NST, NS>;
+  auto kern = k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   static int blocks = 0;
@@ -436,10 +524,10 @@ cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
     if (e != cudaSuccess || per_sm <= 0) per_sm = 1;
     blocks = per_sm * num_sms();
     if (p.debug & 8)
-      fprintf(stderr, "[srt scan] rows: NSW=%d NT=%d NST=%d NS=%d smem=%zu -> %d CTAs\n", NSW,
-              NT, NST, NS, smem, blocks);
+      fprintf(stderr, "[srt scan] rows: NSW=%d NT=%d NST=%d NS=%d CHUNK=%u NG=%d hint=%u spin=%u smem=%zu -> %d CTAs\n",
+              NSW, NT, NST, NS, CHUNK, NG, p.l2_hint, p.spin, smem, blocks);
   }
-  k_scan_rows<DT, NSW, NT, NST, NS><<<blocks, THREADS, smem, stream>>>(c, p);
+  k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG><<<blocks, THREADS, smem, stream>>>(c, p);
   return cudaGetLastError();
 }
 
@@ -476,26 +564,34 @@ cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* ro
     dbg = s ? atoi(s) : 0;
   }
   p.debug = (uint32_t)dbg;
-  static int nsw = -1, nt = -1;
-  if (nsw < 0) {  // SRT_SCAN_ROWS="NSW,NT" picks another instantiated split (dev knob)
-    nsw = 4;
-    nt = 12;
+  // SRT_SCAN_ROWS="NSW,NT,NST,NS,CHUNK_KB,HINT,NG,SPIN" picks another
+  // instantiated pipeline shape (development knob; tools/scan_sweep.sh)
+  static int cfg[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
+  if (cfg[0] < 0) {
+    int d[8] = {8, 10, 4, 4, 32, 1, 2, 0};
     if (const char* s = getenv("SRT_SCAN_ROWS")) {
-      int x = 0, y = 0;
-      if (sscanf(s, "%d,%d", &x, &y) == 2) { nsw = x; nt = y; }
+      int x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const int k = sscanf(s, "%d,%d,%d,%d,%d,%d,%d,%d", &x[0], &x[1], &x[2], &x[3], &x[4], &x[5],
+                           &x[6], &x[7]);
+      for (int i = 0; i < k; ++i) d[i] = x[i];
     }
+    for (int i = 0; i < 8; ++i) cfg[i] = d[i];
   }
-#define SRT_ROWS_CASE(A, B)                                                      \
-  if (nsw == A && nt == B)                                                       \
-    return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, A, B, 4, 4>(c, p, stream) \
-                               : launch_rows<SRT_F32, A, B, 4, 4>(c, p, stream);
-  SRT_ROWS_CASE(4, 8)
-  SRT_ROWS_CASE(6, 8)
-  SRT_ROWS_CASE(6, 10)
-  SRT_ROWS_CASE(8, 8)
+  p.l2_hint = (uint32_t)cfg[5];
+  p.spin = (uint32_t)cfg[7];
+#define SRT_ROWS_CASE(A, B, C, D, K, G)                                                            \
+  if (cfg[0] == A && cfg[1] == B && cfg[2] == C && cfg[3] == D && cfg[4] == K && cfg[6] == G)     \
+    return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, A, B, C, D, K * 1024u, G>(c, p, stream)    \
+                               : launch_rows<SRT_F32, A, B, C, D, K * 1024u, G>(c, p, stream);
+  SRT_ROWS_CASE(4, 12, 4, 4, 32, 1)
+  SRT_ROWS_CASE(8, 8, 4, 4, 32, 2)
+  SRT_ROWS_CASE(8, 12, 4, 4, 32, 2)
+  SRT_ROWS_CASE(8, 10, 6, 2, 32, 2)
+  SRT_ROWS_CASE(12, 8, 6, 2, 32, 3)
+  SRT_ROWS_CASE(12, 9, 6, 3, 32, 3)
 #undef SRT_ROWS_CASE
-  return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, 4, 12, 4, 4>(c, p, stream)
-                             : launch_rows<SRT_F32, 4, 12, 4, 4>(c, p, stream);
+  return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, 8, 10, 4, 4, 32768u, 2>(c, p, stream)
+                             : launch_rows<SRT_F32, 8, 10, 4, 4, 32768u, 2>(c, p, stream);
 }
 
 }  // namespace srt
