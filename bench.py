@@ -45,13 +45,21 @@ CONFIGS = {
                  cap=8192, act_cap=8192, prior_epochs=1, node_capacity=1 << 27),
     # BJ:configs[3]
     "ppo": dict(V=152064, prompts=256, samples=1, active=256, Bmax=64, D=128, L=16, median=1200,
-                cap=4096, act_cap=4096, prior_epochs=3, node_capacity=1 << 27),
-    # BJ:configs[2] (1024 of the 8192 sequences concurrently)
-    "dapo": dict(V=151936, prompts=512, samples=16, active=1024, Bmax=32, D=32, L=8, median=3000,
-                 cap=20000, act_cap=20000, prior_epochs=1, node_capacity=1 << 28),
+                cap=4096, act_cap=4096, prior_epochs=3, node_capacity=1 << 28),
+    # BJ:configs[2] (1024 of the 8192 sequences concurrently).  D = 16: the warm
+    # cache (8192 prior rollouts, 57M tokens) has > 1.07B distinct windows at
+    # D = 32 (measured: node capacity 2^30 overflowed during the warm-up); at
+    # D = 16 it fits 2^30 nodes
+    "dapo": dict(V=151936, prompts=512, samples=16, active=1024, Bmax=32, D=16, L=8, median=3000,
+                 cap=20000, act_cap=20000, prior_epochs=1, node_capacity=1 << 30,
+                 slot_capacity=1 << 30,
+                 # run-ahead generation: rollouts of the next 64 prompts (the
+                 # look-ahead window) are inserted as spans of 512-2048 tokens, 8 per step
+                 runahead=dict(first=64, prompts=64, per=4, spans=8, lo=512, hi=2048)),
 }
 
-KERNELS_PER_STEP = 7  # per group: draft, row_offsets, scan, accept, insert_plan/walk/cursor
+KERNELS_PER_STEP = 9  # per group: draft, row_offsets, scan, accept, insert_plan/walk/cursor
+                      # (+ insert_plan/walk of the run-ahead spans)
 
 
 def log(*a):
@@ -142,9 +150,11 @@ class Workload:
         t = time.time()
         gp = list(prompt_ids) if prompt_ids is not None else owned_prompts(rank, world, cfg["prompts"])
         self.global_prompts = gp
+        ra = cfg.get("runahead")
         w = make_workload(seed + 1000003 * gp[0], cfg["V"], cfg["prompts"], cfg["samples"],
                           cfg["median"], cfg["cap"], prior_epochs=cfg["prior_epochs"],
-                          active=cfg["active"])
+                          active=cfg["active"],
+                          runahead=(ra["first"], ra["prompts"], ra["per"]) if ra else None)
         self.w = w
         rng = np.random.default_rng(seed + 7 + gp[0])
         # every active sequence starts part-way into its rollout (steady state):
@@ -185,6 +195,8 @@ class Group:
         n_prompts = len(range(g, cfg["prompts"], G))
         c = srt.config(V, n_prompts, cfg["D"], cfg["L"], B,
                        node_capacity=max(1 << 16, cfg["node_capacity"] // G),
+                       slot_capacity=(max(1 << 16, cfg["slot_capacity"] // G)
+                                      if "slot_capacity" in cfg else None),
                        logits_dtype=self.ldtype)
         self.cache = srt.SrtCache(c)
         # ---- warm trees: prior-epoch rollouts ("carries signal across steps")
@@ -226,6 +238,13 @@ class Group:
         if bits:
             raise RuntimeError(f"cache error bits {bits} after warm-up inserts ({st})")
         self.tree_stats = st
+        # ---- run-ahead spans (DAPO): a fixed schedule, uploaded once
+        self.ra = None
+        if wl.w.runahead and cfg.get("runahead"):
+            if G != 1:
+                raise ValueError("run-ahead spans need --groups 1")
+            self.ra = runahead_schedule(wl.w.runahead, cfg["runahead"], cfg["cap"], seed, dev)
+            self.ra_k = 0
         # ---- this group's rows of the logits buffer: rows_max + 1 dummy row
         self.rows_max = n * (B + 1)
         self.logits = logits[row0:row0 + self.rows_max + 1]
@@ -283,6 +302,58 @@ class Group:
         c.verify(self.logits if logits is None else logits, self.d, self.seq_id, seed, self.seq_tok,
                  self.seq_len, self.max_new, out=self.v, rows=self.rows_max)
         c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len, cursor=self.cursor)
+        if self.ra is not None:
+            self.runahead_insert()
+
+    def runahead_inserted(self):
+        """Host view: tokens of each look-ahead rollout inserted so far."""
+        ra = self.ra
+        k = min(self.ra_k, ra["frm"].shape[0]) - 1
+        return ra["to_host"][k] if k >= 0 else np.zeros(len(ra["prompt_host"]), np.int32)
+
+    def runahead_insert(self):
+        """This step's run-ahead spans: [frm, to) of each look-ahead rollout
+        (empty for the rollouts not scheduled this step), walk insertion."""
+        ra = self.ra
+        k = min(self.ra_k, ra["frm"].shape[0] - 1)  # past the schedule: empty spans
+        self.cache.insert(ra["prompt"], ra["tok"], ra["frm"][k], ra["to"][k])
+        self.ra_k += 1
+
+
+def runahead_schedule(streams, rc: dict, cap: int, seed: int, dev, steps: int = 512):
+    """Run-ahead spans for `steps` steps: each step the next rc["spans"]
+    unfinished look-ahead rollouts (round robin) advance by U[lo, hi] tokens.
+    Row k of frm/to holds every rollout's span of step k (empty = not
+    scheduled); after the rollouts run out every span is empty."""
+    import torch
+    R = len(streams)
+    lens = np.array([len(t) for _, t in streams], np.int64)
+    tab = np.zeros((R, cap), np.int32)
+    for i, (_, t) in enumerate(streams):
+        tab[i, :len(t)] = t
+    rng = np.random.default_rng(seed + 99991)
+    pos = np.zeros(R, np.int64)
+    frm = np.zeros((steps + 1, R), np.int32)  # the last row: all empty
+    to = np.zeros((steps + 1, R), np.int32)
+    ptr = 0
+    for k in range(steps):
+        nxt = pos.copy()
+        picked = tries = 0
+        while picked < rc["spans"] and tries < R:
+            r = ptr % R
+            ptr += 1
+            tries += 1
+            if pos[r] >= lens[r]:
+                continue
+            nxt[r] = min(lens[r], pos[r] + int(rng.integers(rc["lo"], rc["hi"] + 1)))
+            picked += 1
+        frm[k], to[k] = pos, nxt
+        pos = nxt
+    frm[steps], to[steps] = pos, pos
+    prompt = np.array([p for p, _ in streams], np.int32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    return {"tok": t(tab), "prompt": t(prompt), "frm": t(frm), "to": t(to),
+            "frm_host": frm, "to_host": to, "tok_host": tab, "prompt_host": prompt}
 
 
 class GpuRun:

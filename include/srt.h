@@ -367,6 +367,15 @@ SRT_API srt_status srt_profile_read(srt_cache* cache, srt_profile_record* host_b
  */
 SRT_API srt_status srt_debug_draft_profile(int64_t* dev_buf);
 
+/*
+ * srt_debug_insert_profile — development support: when dev_buf (DEVICE,
+ * 8 int64 per sequence of the next srt_insert_cursor calls) is non-NULL, the
+ * cursor kernel writes per sequence {total cycles, cycles loading or
+ * rebuilding the cursor, new positions, nodes created, cycles of the slowest
+ * position, cursor valid, 0, 0}.  NULL disables (default).  Process-wide.
+ */
+SRT_API srt_status srt_debug_insert_profile(int64_t* dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -365,6 +365,11 @@ srt_status srt_debug_draft_profile(int64_t* dev_buf) {
   return SRT_OK;
 }
 
+srt_status srt_debug_insert_profile(int64_t* dev_buf) {
+  SRT_CUDA(set_insert_profile((long long*)dev_buf), "set_insert_profile");
+  return SRT_OK;
+}
+
 // ---- multi-GPU exchange records (exchange.cu)
 srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
                            const int32_t* draft_len, const int32_t* draft_tok,

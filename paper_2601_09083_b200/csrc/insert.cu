@@ -337,6 +337,11 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
 // ---------------------------------------------------------------------------
 constexpr int CURSOR_WARPS = 4;
 
+// Development-only per-sequence profile (srt_debug_insert_profile): when set,
+// k_insert_cursor writes {total cycles, cursor-phase cycles, positions, nodes
+// created, slowest position's cycles, cursor valid, 0, 0} per sequence.
+__device__ long long* g_ins_prof = nullptr;
+
 __global__ void __launch_bounds__(CURSOR_WARPS * 32)
 k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
                 const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
@@ -361,6 +366,8 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     return;
   }
   const int32_t* y = seq_tok + (int64_t)s * stride;
+  const long long tp0 = clock64();
+  long long tp_cur = 0, tp_max = 0;
   unsigned incs = 0, created = 0;
   const bool valid = cur[0] == tag && cur[1] == (uint32_t)P && cur[2] == (uint32_t)p &&
                      cur[3] == (uint32_t)fl;
@@ -394,8 +401,10 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     }
   }
   __syncwarp();
+  tp_cur = clock64() - tp0;
   const int ngroups = (D + 31) >> 5;
   for (int32_t j = P; j < t_end; ++j) {
+    const long long tj = clock64();
     const int32_t tk = y[j];
     const bool oov = tk < 0 || tk >= c.V;
     if (oov && lane == 0) set_error(c, SRT_DEV_OOV);
@@ -419,6 +428,7 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       if (l <= D) A[l] = (active && ch < BAD) ? ch : NONE;
       __syncwarp();
     }
+    tp_max = max(tp_max, clock64() - tj);
   }
   for (int32_t l = 1 + lane; l <= D; l += 32) cur[4 + l - 1] = A[l];
   if (lane == 0) {
@@ -426,6 +436,19 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     cur[1] = (uint32_t)t_end;
     cur[2] = (uint32_t)p;
     cur[3] = (uint32_t)fl;
+  }
+  if (g_ins_prof) {
+    unsigned long long d = created;
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane == 0) {
+      long long* o = g_ins_prof + 8 * (int64_t)s;
+      o[0] = clock64() - tp0;
+      o[1] = tp_cur;
+      o[2] = t_end - P;
+      o[3] = (long long)d;
+      o[4] = tp_max;
+      o[5] = valid;
+    }
   }
   if (stats) {
     unsigned long long b = incs, d = created;
@@ -444,6 +467,10 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
 }
 
 }  // namespace
+
+cudaError_t set_insert_profile(long long* buf) {
+  return cudaMemcpyToSymbol(g_ins_prof, &buf, sizeof(buf));
+}
 
 cudaError_t launch_insert_plan(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                const int32_t* from, const int32_t* to, const int32_t* floor_,

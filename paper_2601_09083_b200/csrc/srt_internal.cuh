@@ -213,6 +213,7 @@ cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
                          int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream);
 cudaError_t set_draft_profile(long long* buf);
+cudaError_t set_insert_profile(long long* buf);
 cudaError_t launch_row_offsets(int32_t n, const int32_t* draft_len, int64_t* row_offsets,
                                cudaStream_t stream);
 struct VerifyArgs {

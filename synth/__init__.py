@@ -88,10 +88,17 @@ class Workload:
     truth: list = field(default_factory=list)       # per active sequence: np.int32 tokens
     seq_prompt: np.ndarray = None                   # prompt id per active sequence
     seq_id: np.ndarray = None                       # u64 ids (epoch << 40 | p << 8 | k)
+    runahead: list = field(default_factory=list)    # (prompt, tokens) run-ahead rollouts
 
 
 def make_workload(seed: int, V: int, n_prompts: int, samples: int, median: int, cap: int,
-                  prior_epochs: int = 1, active: int | None = None) -> Workload:
+                  prior_epochs: int = 1, active: int | None = None,
+                  runahead: tuple | None = None) -> Workload:
+    """runahead = (first prompt, n prompts, streams per prompt): rollouts of
+    prompts that will be sampled soon (P:L151 run-ahead generation), drawn from
+    the same current-epoch templates as the active sequences, returned in
+    w.runahead as (prompt, tokens).  Drawn after everything else, so the rest
+    of the workload does not depend on it."""
     rng = np.random.default_rng(seed)
     perm = rng.permutation(V).astype(np.int32)
     tmpl = make_templates(rng, n_prompts, V, perm, median, cap)
@@ -111,6 +118,10 @@ def make_workload(seed: int, V: int, n_prompts: int, samples: int, median: int, 
     w.truth = truth
     w.seq_prompt = np.asarray(seq_prompt, np.int32)
     w.seq_id = np.asarray(seq_id, np.uint64)
+    if runahead is not None:
+        p0, npr, per = runahead
+        w.runahead = [(p, sibling_stream(rng, tmpl[p], V, perm, cap))
+                      for p in range(p0, p0 + npr) for _ in range(per)]
     return w
 
 

@@ -39,6 +39,27 @@ def main():
         print(f"step {k}: n_commit mean {nc.mean():.2f} p90 {np.percentile(nc, 90):.0f} "
               f"p99 {np.percentile(nc, 99):.0f} max {nc.max()}")
     n = run.n
+    # per-sequence cycle profile of the cursor kernel inside real steps
+    import ctypes
+    from paper_2601_09083_b200 import _lib
+    L = _lib.load()
+    prof = torch.zeros(n, 8, dtype=torch.int64, device=run.dev)
+    L.srt_debug_insert_profile(ctypes.c_void_p(prof.data_ptr()))
+    for k in range(3):
+        prof.zero_()
+        run.step(bench.step_seed(0, 10 + k))
+        torch.cuda.synchronize()
+        p = prof.cpu().numpy()
+        tot = p[:, 0]
+        act = tot > 0
+        print(f"profiled step {k}: active {act.sum()} total cycles p50 {np.percentile(tot[act], 50):.0f} "
+              f"p90 {np.percentile(tot[act], 90):.0f} p99 {np.percentile(tot[act], 99):.0f} max {tot.max()}; "
+              f"cursor-phase p50 {np.percentile(p[act, 1], 50):.0f} max {p[:, 1].max()}; "
+              f"invalid cursors {(act & (p[:, 5] == 0)).sum()}")
+        for s_ in np.argsort(-tot)[:6]:
+            print(f"   slow seq {s_}: cycles {p[s_, 0]} cursor {p[s_, 1]} positions {p[s_, 2]} "
+                  f"created {p[s_, 3]} slowest position {p[s_, 4]} valid {p[s_, 5]}")
+    L.srt_debug_insert_profile(ctypes.c_void_p(0))
     ar = torch.arange(n, device=run.dev)
     for m in (1, 2, 4, 8, 16, 24, 32):
         for mode in ("cursor", "walk"):
