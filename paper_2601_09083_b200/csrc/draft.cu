@@ -3,278 +3,249 @@
 //
 // One warp per sequence.  Match: lane q-1 walks the root along y[t-q .. t-1]
 // (q hash probes, all lanes in parallel) and a ballot keeps the largest q whose
-// node has a child.  Expansion: a frontier sorted under the total order O8 is
-// kept in shared memory (<= Bmax entries, truncated to B - popped, which is
-// exact because a child never outranks its parent); the children of each
-// popped node are enumerated 32 at a time from its child blocks (coalesced
-// reads of the child ids and their token / count mirrors) and inserted with
-// warp ballots.
-// Roofline: latency-bound (L + ~3 B dependent loads per warp); us per batch.
+// node has a child.  Expansion: the frontier lives in registers, sorted under
+// the total order O8 (lane i holds entries i and i + 32, so up to 64 entries),
+// truncated to B - popped (exact: a child never outranks its parent).  A pop is
+// a lane shift; a candidate enters with two ballots and a shift.  Children of
+// a multi-child node stream past 32 x UNR at a time (coalesced child ids,
+// tokens and count mirrors), the next round's loads in flight while this one
+// is ranked, and a count threshold (the largest count whose score is below the
+// frontier's last entry) rejects most of a hub's children with one integer
+// compare before any division.
+// Roofline: latency-bound (L probes + ~1 record load per pop + 1-2 round trips
+// per multi-child pop per warp); us per batch.
 #include "srt_internal.cuh"
 
 namespace srt {
 
 namespace {
 
-constexpr int DRAFT_WARPS = 2;  // 8K registers per CTA: fits beside a running verify scan
+constexpr int DRAFT_WARPS = 2;  // small CTAs: fit beside a running verify scan
 
 // Development-only per-sequence profile (srt_debug_draft_profile): when set,
 // k_draft writes {match cycles, total cycles, children scanned, max children
-// of one node, cycles in: record loads, block lookups, child loads,
-// frontier inserts} per sequence.
+// of one node, cycles waiting for records, cycles in block lookups, cycles in
+// child rounds, (multi-child pops << 20) | single-child pops} per sequence.
 __device__ long long* g_draft_prof = nullptr;
 struct ExpandProf {
-  long long rec = 0, blk = 0, ld = 0, ins = 0;
-};
-constexpr int FCAP = 64;
-
-struct FrontierSmem {
-  double score[FCAP];
-  int32_t depth[FCAP];
-  int32_t tok[FCAP];
-  int32_t parent[FCAP];
-  uint32_t node[FCAP];
-  unsigned long long mask[FCAP];  // ancestor-or-self masks of drafted nodes
+  long long rec = 0, blk = 0, ld = 0, pops = 0;
 };
 
-struct Cand {
+constexpr int32_t IMAX = 0x7FFFFFFF;
+constexpr unsigned long long META_NONE = ~0ull;
+
+// A frontier entry.  O8 orders entries by score desc, then depth asc, token
+// asc, parent draft index asc; the last three are packed into `meta` so that a
+// smaller meta is the better entry on equal scores:
+//   meta = depth << 38 | token << 7 | (parent + 1)   (depth <= 64, token < 2^31,
+//                                                     parent in [-1, 63])
+struct Ent {
   double score;
-  int32_t depth, tok, parent;
+  unsigned long long meta;
   uint32_t node;
 };
+__device__ __forceinline__ unsigned long long make_meta(int32_t depth, int32_t tok, int32_t parent) {
+  return ((unsigned long long)depth << 38) | ((unsigned long long)(uint32_t)tok << 7) |
+         (unsigned long long)(parent + 1);
+}
+__device__ __forceinline__ int32_t meta_depth(unsigned long long m) { return (int32_t)(m >> 38); }
+__device__ __forceinline__ int32_t meta_tok(unsigned long long m) {
+  return (int32_t)((m >> 7) & 0x7FFFFFFFull);
+}
+__device__ __forceinline__ int32_t meta_parent(unsigned long long m) { return (int32_t)(m & 0x7F) - 1; }
 
-// O8: score desc, depth asc, token asc, parent draft index asc.
-__device__ __forceinline__ bool better(double s1, int32_t d1, int32_t t1, int32_t p1, double s2,
-                                       int32_t d2, int32_t t2, int32_t p2) {
-  if (s1 != s2) return s1 > s2;
-  if (d1 != d2) return d1 < d2;
-  if (t1 != t2) return t1 < t2;
-  return p1 < p2;
+__device__ __forceinline__ bool better(const Ent& a, const Ent& b) {
+  return a.score > b.score || (a.score == b.score && a.meta < b.meta);
+}
+__device__ __forceinline__ Ent ent_shfl(const Ent& e, int src) {
+  return Ent{__shfl_sync(0xffffffffu, e.score, src), __shfl_sync(0xffffffffu, e.meta, src),
+             __shfl_sync(0xffffffffu, e.node, src)};
+}
+__device__ __forceinline__ Ent ent_up1(const Ent& e) {
+  return Ent{__shfl_up_sync(0xffffffffu, e.score, 1), __shfl_up_sync(0xffffffffu, e.meta, 1),
+             __shfl_up_sync(0xffffffffu, e.node, 1)};
+}
+__device__ __forceinline__ Ent ent_down1(const Ent& e) {
+  return Ent{__shfl_down_sync(0xffffffffu, e.score, 1), __shfl_down_sync(0xffffffffu, e.meta, 1),
+             __shfl_down_sync(0xffffffffu, e.node, 1)};
 }
 
-__device__ __forceinline__ bool entry_better(const FrontierSmem& F, int j, const Cand& c) {
-  return better(F.score[j], F.depth[j], F.tok[j], F.parent[j], c.score, c.depth, c.tok, c.parent);
+// Loads the compiler may not sink to their first use (software pipelining of
+// the child rounds) and fire-and-forget L1 prefetches.
+__device__ __forceinline__ uint32_t ldg_early(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
-// Insert c into the sorted frontier of current size `size`, keeping at most
-// `cap` entries.  Warp-collective; returns the new size.
-__device__ __forceinline__ int frontier_insert(FrontierSmem& F, int size, int cap, const Cand& c,
-                                               int lane) {
-  const bool b0 = lane < size && entry_better(F, lane, c);
-  const bool b1 = lane + 32 < size && entry_better(F, lane + 32, c);
-  const int pos = __popc(__ballot_sync(0xffffffffu, b0)) + __popc(__ballot_sync(0xffffffffu, b1));
-  if (pos >= cap) return size;
-  const int newsize = min(size + 1, cap);
-  Cand e0, e1;
-  const bool m0 = lane >= pos && lane < newsize - 1;
-  const bool m1 = lane + 32 >= pos && lane + 32 < newsize - 1;
-  if (m0) e0 = Cand{F.score[lane], F.depth[lane], F.tok[lane], F.parent[lane], F.node[lane]};
-  if (m1) e1 = Cand{F.score[lane + 32], F.depth[lane + 32], F.tok[lane + 32], F.parent[lane + 32],
-                    F.node[lane + 32]};
-  __syncwarp();
-  if (m0) {
-    F.score[lane + 1] = e0.score; F.depth[lane + 1] = e0.depth; F.tok[lane + 1] = e0.tok;
-    F.parent[lane + 1] = e0.parent; F.node[lane + 1] = e0.node;
+// The register frontier: entry j on lane j (e0) or lane j - 32 (e1); entries
+// [0, size) are valid and sorted, size <= cap <= 64.
+struct Frontier {
+  Ent e0, e1;
+  int size;
+
+  __device__ __forceinline__ Ent at(int j) const {
+    return j < 32 ? ent_shfl(e0, j) : ent_shfl(e1, j - 32);
   }
-  if (m1) {
-    F.score[lane + 33] = e1.score; F.depth[lane + 33] = e1.depth; F.tok[lane + 33] = e1.tok;
-    F.parent[lane + 33] = e1.parent; F.node[lane + 33] = e1.node;
+  // Insert candidate b (warp-uniform); entries past cap fall off.
+  __device__ __forceinline__ void insert(const Ent& b, int cap, int lane) {
+    int pos = __popc(__ballot_sync(0xffffffffu, lane < size && better(e0, b)));
+    if (size > 32) pos += __popc(__ballot_sync(0xffffffffu, lane + 32 < size && better(e1, b)));
+    if (pos >= cap) return;
+    const Ent u0 = ent_up1(e0);
+    if (cap > 32) {  // (warp-uniform) entries 32.. live in e1
+      const Ent u1 = ent_up1(e1);
+      const Ent last0 = ent_shfl(e0, 31);
+      if (lane + 32 >= pos) e1 = (lane + 32 == pos) ? b : (lane == 0 ? last0 : u1);
+    }
+    if (lane >= pos) e0 = (lane == pos) ? b : u0;
+    size = min(size + 1, cap);
   }
-  __syncwarp();
-  if (lane == 0) {
-    F.score[pos] = c.score; F.depth[pos] = c.depth; F.tok[pos] = c.tok;
-    F.parent[pos] = c.parent; F.node[pos] = c.node;
+  // Remove entry 0 (returned).
+  __device__ __forceinline__ Ent pop(int lane) {
+    const Ent top = ent_shfl(e0, 0);
+    const Ent d0 = ent_down1(e0);
+    if (size > 32) {  // (warp-uniform)
+      const Ent d1 = ent_down1(e1);
+      const Ent first1 = ent_shfl(e1, 0);
+      e0 = lane < 31 ? d0 : first1;
+      e1 = d1;
+    } else {
+      e0 = d0;
+    }
+    --size;
+    return top;
   }
-  __syncwarp();
-  return newsize;
+};
+
+// f(c) = score of a child with count c (O6): RN(score_u * RN(c / csum)).
+__device__ __forceinline__ double child_score(double score_u, double dsum, uint32_t c) {
+  return __dmul_rn(score_u, dsum > 0.0 ? __ddiv_rn((double)c, dsum) : 0.0);
 }
 
-__device__ __forceinline__ Cand frontier_pop(FrontierSmem& F, int size, int lane) {
-  const Cand top{F.score[0], F.depth[0], F.tok[0], F.parent[0], F.node[0]};
-  Cand e0, e1;
-  const bool m0 = lane >= 1 && lane < size;
-  const bool m1 = lane + 32 < size;
-  if (m0) e0 = Cand{F.score[lane], F.depth[lane], F.tok[lane], F.parent[lane], F.node[lane]};
-  if (m1) e1 = Cand{F.score[lane + 32], F.depth[lane + 32], F.tok[lane + 32], F.parent[lane + 32],
-                    F.node[lane + 32]};
-  __syncwarp();
-  if (m0) {
-    F.score[lane - 1] = e0.score; F.depth[lane - 1] = e0.depth; F.tok[lane - 1] = e0.tok;
-    F.parent[lane - 1] = e0.parent; F.node[lane - 1] = e0.node;
-  }
-  if (m1) {
-    F.score[lane + 31] = e1.score; F.depth[lane + 31] = e1.depth; F.tok[lane + 31] = e1.tok;
-    F.parent[lane + 31] = e1.parent; F.node[lane + 31] = e1.node;
-  }
-  __syncwarp();
-  return top;
-}
-
-
-// ---- register frontier (cap <= 32): lane i holds entry i while a node's
-// children stream past, so each candidate costs one compare against the
-// current bar (entry cap-1) and an entering one a ballot and a lane shift.
-constexpr int32_t IMAX = 0x7FFFFFFF;
-__device__ __forceinline__ Cand cand_shfl(const Cand& e, int src) {
-  return Cand{__shfl_sync(0xffffffffu, e.score, src), __shfl_sync(0xffffffffu, e.depth, src),
-              __shfl_sync(0xffffffffu, e.tok, src), __shfl_sync(0xffffffffu, e.parent, src),
-              __shfl_sync(0xffffffffu, e.node, src)};
-}
-__device__ __forceinline__ Cand cand_shfl_up1(const Cand& e) {
-  return Cand{__shfl_up_sync(0xffffffffu, e.score, 1), __shfl_up_sync(0xffffffffu, e.depth, 1),
-              __shfl_up_sync(0xffffffffu, e.tok, 1), __shfl_up_sync(0xffffffffu, e.parent, 1),
-              __shfl_up_sync(0xffffffffu, e.node, 1)};
-}
-__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
-  return better(a.score, a.depth, a.tok, a.parent, b.score, b.depth, b.tok, b.parent);
+// A count c_lo such that every child with count <= c_lo scores strictly
+// below w (so it cannot enter a full frontier whose last entry scores w), or
+// -1.  One rounded estimate x' of x = w * csum / score_u has relative error
+// below 2^-50, so floor(x') - 2 <= x - 1, and f(c) = RN(score_u * RN(c/csum))
+// <= score_u * (x - 1) / csum * (1 + 2^-51) < w for every c <= x - 1 as long
+// as x < 2^50 (counts < 2^32).  Exactness never depends on c_lo being tight.
+__device__ __forceinline__ long long count_floor(double w, double score_u, double dsum) {
+  if (!(w > 0.0) || score_u == 0.0) return -1;
+  const double x = __ddiv_rn(__dmul_rn(w, dsum), score_u);
+  if (!(x < 4294967296.0)) return (long long)dsum;  // every count scores below w
+  return (long long)floor(x) - 2;
 }
 
 // Push the children of u (C(v) = count(v) / csum(u), csum = the sum of the
 // counts of u's children; score = score_u * C) into the
 // frontier.  rec[u] is one 16-byte load; a single child needs nothing else
-// (its C is exactly 1); more children are enumerated 32 x UNR at a time with
-// every load of a round issued before any is used.
-__device__ int expand(const DevCache& c, FrontierSmem& F, int size, int cap, uint32_t u,
-                      double score_u, int32_t depth_u, int32_t parent_idx, int lane,
-                      ExpandProf& pf) {
-  if (cap <= 0) return size;
+// (its C is exactly 1).
+__device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, double score_u,
+                       int32_t depth_u, int32_t parent_idx, int lane, ExpandProf& pf) {
+  if (cap <= 0) return;
   long long t0 = clock64();
   const uint4 r = ld_rec(c, u);
-  const uint32_t nch = r.x;
+  uint32_t nch;
+  asm volatile("mov.b32 %0, %1;" : "=r"(nch) : "r"(r.x));  // (profile: time the wait)
   pf.rec += clock64() - t0;
-  if (nch == 0) return size;
+  if (nch == 0) return;
   if (nch == 1) {
     // C = cnt(child0) / csum(u) = 1 exactly when csum > 0 (0/0 -> 0, O6)
-    const Cand b{r.w ? __dmul_rn(score_u, 1.0) : 0.0, depth_u + 1, (int32_t)r.z, parent_idx, r.y};
-    if (size == cap && !better(b.score, b.depth, b.tok, b.parent, F.score[cap - 1],
-                               F.depth[cap - 1], F.tok[cap - 1], F.parent[cap - 1]))
-      return size;
-    return frontier_insert(F, size, cap, b, lane);
+    ++pf.pops;
+    F.insert(Ent{r.w ? score_u : 0.0, make_meta(depth_u + 1, (int32_t)r.z, parent_idx), r.y}, cap,
+             lane);
+    return;
   }
+  pf.pops += 1ll << 20;
   const double dsum = (double)r.w;  // exact (< 2^32)
+  const unsigned long long meta0 = make_meta(depth_u + 1, 0, parent_idx);
   // block bases of blocks 0..nb-1 (children 1..nch-1), one lane each
   const uint32_t nb = blk_index(nch - 2) + 1;
   t0 = clock64();
   const uint32_t mybase = lane < (int)nb ? hash_find(c, block_key(u, lane)) : 0u;
   __syncwarp();
   pf.blk += clock64() - t0;
+  t0 = clock64();
+  // the entry a candidate must beat, and the count at or below which none can
+  Ent bar = F.size == cap ? F.at(cap - 1) : Ent{-1.0, META_NONE, NONE};
+  long long c_lo = count_floor(bar.score, score_u, dsum);
   constexpr int UNR = 8;
-  if (cap <= 32) {
-    const Cand SENT{-1.0, IMAX, IMAX, IMAX, NONE};  // worse than every real entry (scores >= 0)
-    Cand fr = SENT;
-    if (lane < size) fr = Cand{F.score[lane], F.depth[lane], F.tok[lane], F.parent[lane], F.node[lane]};
-    Cand worst = cand_shfl(fr, cap - 1);  // the bar to enter
-    for (uint32_t kr = 0; kr < nch; kr += 32 * UNR) {
-      Cand cd[UNR];
-      uint32_t cc[UNR];
-      t0 = clock64();
-#pragma unroll
-      for (int m = 0; m < UNR; ++m) {  // child id, token and count mirror: coalesced
-        const uint32_t k = kr + m * 32 + lane;
-        const uint32_t jj = k >= 1 ? k - 1 : 0;
-        const uint32_t bi = blk_index(jj);
-        const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
-        const uint32_t pos = base + (jj - blk_start(bi));
-        cd[m] = Cand{-1.0, depth_u + 1, IMAX, parent_idx, NONE};
-        cc[m] = 0;
-        if (k == 0) {
-          cd[m].node = r.y;
-          cd[m].tok = (int32_t)r.z;
-          cc[m] = __ldg(&c.cnt[r.y]);
-        } else if (k < nch) {
-          cd[m].node = __ldg(&c.slots[pos]);
-          cd[m].tok = __ldg(&c.stok[pos]);
-          cc[m] = __ldg(&c.scnt[pos]);
-        }
-      }
-      __syncwarp();
-      pf.ld += clock64() - t0;
-      t0 = clock64();
-#pragma unroll
-      for (int m = 0; m < UNR; ++m)  // independent: the divisions pipeline
-        if (cd[m].node != NONE)
-          cd[m].score = __dmul_rn(score_u, r.w ? __ddiv_rn((double)cc[m], dsum) : 0.0);
-#pragma unroll
-      for (int m = 0; m < UNR; ++m) {
-        if (kr + m * 32 >= nch) break;
-        unsigned pending = __ballot_sync(0xffffffffu, cand_better(cd[m], worst));
-        while (pending) {
-          const int src = __ffs(pending) - 1;
-          pending &= pending - 1;
-          const Cand b = cand_shfl(cd[m], src);
-          if (!cand_better(b, worst)) continue;  // an earlier insertion raised the bar
-          const int at = __popc(__ballot_sync(0xffffffffu, cand_better(fr, b)));
-          const Cand prev = cand_shfl_up1(fr);
-          if (lane > at) fr = prev;
-          if (lane == at) fr = b;
-          worst = cand_shfl(fr, cap - 1);
-        }
-      }
-      pf.ins += clock64() - t0;
-    }
-    const int nsize = __popc(__ballot_sync(0xffffffffu, lane < cap && fr.score >= 0.0));
-    __syncwarp();
-    if (lane < nsize) {
-      F.score[lane] = fr.score; F.depth[lane] = fr.depth; F.tok[lane] = fr.tok;
-      F.parent[lane] = fr.parent; F.node[lane] = fr.node;
-    }
-    __syncwarp();
-    return nsize;
-  }
-  for (uint32_t kr = 0; kr < nch; kr += 32 * UNR) {
-    uint32_t ch[UNR], cc[UNR];
-    int32_t tk[UNR];
-    t0 = clock64();
+  uint32_t chA[UNR], ccA[UNR], chB[UNR], ccB[UNR];
+  int32_t tkA[UNR], tkB[UNR];
+  auto load_round = [&](uint32_t kr, uint32_t (&ch)[UNR], int32_t (&tk)[UNR],
+                        uint32_t (&cc)[UNR]) {
 #pragma unroll
     for (int m = 0; m < UNR; ++m) {  // child id, token and count mirror: coalesced
       const uint32_t k = kr + m * 32 + lane;
+      ch[m] = NONE;
+      cc[m] = 0;
+      tk[m] = IMAX;
+      if (kr + m * 32 >= nch) continue;  // (warp-uniform)
       const uint32_t jj = k >= 1 ? k - 1 : 0;
       const uint32_t bi = blk_index(jj);
       const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
       const uint32_t pos = base + (jj - blk_start(bi));
-      ch[m] = NONE;
-      cc[m] = 0;
-      tk[m] = 0;
       if (k == 0) {
         ch[m] = r.y;
         tk[m] = (int32_t)r.z;
-        cc[m] = __ldg(&c.cnt[r.y]);
+        cc[m] = ldg_early(&c.cnt[r.y]);
       } else if (k < nch) {
-        ch[m] = __ldg(&c.slots[pos]);
-        tk[m] = __ldg(&c.stok[pos]);
-        cc[m] = __ldg(&c.scnt[pos]);
+        ch[m] = ldg_early(&c.slots[pos]);
+        tk[m] = (int32_t)ldg_early((const uint32_t*)&c.stok[pos]);
+        cc[m] = ldg_early(&c.scnt[pos]);
       }
     }
-    __syncwarp();
-    pf.ld += clock64() - t0;
-    t0 = clock64();
+  };
+  auto rank_round = [&](uint32_t kr, const uint32_t (&ch)[UNR], const int32_t (&tk)[UNR],
+                        const uint32_t (&cc)[UNR]) {
+    bool entered = false;
 #pragma unroll
     for (int m = 0; m < UNR; ++m) {
       if (kr + m * 32 >= nch) break;
-      const bool valid = ch[m] != NONE;
-      Cand cd{0.0, depth_u + 1, tk[m], parent_idx, ch[m]};
-      if (valid) cd.score = __dmul_rn(score_u, r.w ? __ddiv_rn((double)cc[m], dsum) : 0.0);
-      // cheap prefilter against the current worst entry when full
-      bool want = valid;
-      if (want && size == cap) want = !entry_better(F, cap - 1, cd);
+      // count prefilter, then the exact comparison against the bar
+      Ent cd{-1.0, META_NONE, ch[m]};
+      bool want = ch[m] != NONE && (long long)cc[m] > c_lo;
+      if (want) {
+        cd.score = child_score(score_u, dsum, cc[m]);
+        cd.meta = meta0 | ((unsigned long long)(uint32_t)tk[m] << 7);
+        want = better(cd, bar);
+      }
       unsigned pending = __ballot_sync(0xffffffffu, want);
       while (pending) {
         const int src = __ffs(pending) - 1;
         pending &= pending - 1;
-        Cand b;
-        b.score = __shfl_sync(0xffffffffu, cd.score, src);
-        b.depth = cd.depth;
-        b.tok = __shfl_sync(0xffffffffu, cd.tok, src);
-        b.parent = parent_idx;
-        b.node = __shfl_sync(0xffffffffu, cd.node, src);
-        // re-check: earlier insertions of this round may have raised the worst entry
-        if (size == cap && entry_better(F, cap - 1, b)) continue;
-        size = frontier_insert(F, size, cap, b, lane);
+        const Ent b = ent_shfl(cd, src);
+        if (!better(b, bar)) continue;  // an earlier insertion raised the bar
+        F.insert(b, cap, lane);
+        entered = true;
+        if (F.size == cap) bar = F.at(cap - 1);
       }
     }
-    pf.ins += clock64() - t0;
+    if (entered && F.size == cap) c_lo = count_floor(bar.score, score_u, dsum);
+  };
+  load_round(0, chA, tkA, ccA);
+  for (uint32_t kr = 0; kr < nch; kr += 64 * UNR) {
+    const uint32_t k1 = kr + 32 * UNR;
+    if (k1 < nch) load_round(k1, chB, tkB, ccB);
+    rank_round(kr, chA, tkA, ccA);
+    if (k1 >= nch) break;
+    if (k1 + 32 * UNR < nch) load_round(k1 + 32 * UNR, chA, tkA, ccA);
+    rank_round(k1, chB, tkB, ccB);
   }
-  return size;
+  pf.ld += clock64() - t0;
+}
+
+// Warm L1 with what popping the next frontier entries reads first: their
+// records and the home slot of their first child block's hash key.
+__device__ __forceinline__ void prefetch_frontier(const DevCache& c, const Frontier& F, int lane) {
+  if (lane < 4 && lane < F.size) {
+    const uint32_t u = F.e0.node;
+    prefetch_l1(&c.rec[u]);
+    prefetch_l1(&c.hash[mix64(block_key(u, 0)) & (c.H - 1)]);
+  }
 }
 
 __global__ void __launch_bounds__(DRAFT_WARPS * 32)
@@ -284,12 +255,13 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         int32_t* __restrict__ draft_len, int32_t* __restrict__ draft_tok,
         int32_t* __restrict__ draft_parent, int32_t* __restrict__ draft_depth,
         int32_t* __restrict__ draft_pos, uint64_t* __restrict__ draft_mask) {
-  __shared__ FrontierSmem smem[DRAFT_WARPS];
+  __shared__ unsigned long long masks[DRAFT_WARPS][64];  // ancestor-or-self masks (O9)
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int32_t s = blockIdx.x * DRAFT_WARPS + w;
   if (s >= n) return;
-  FrontierSmem& F = smem[w];
+  unsigned long long* M = masks[w];
+  long long* const prof = g_draft_prof;  // (development profile; one load)
   const long long t_start = clock64();
   long long t_match = 0, scanned = 0, maxch = 0;
   ExpandProf pf;
@@ -333,38 +305,38 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   if (q > 0) {
     const long long bq = (long long)c.b0 + ((long long)q * c.snum) / c.sden;
     const int32_t B = (int32_t)min((long long)Bmax, bq);
-    if (g_draft_prof) {
+    if (prof) {
       const long long nc = ld_rec(c, uq).x;
       scanned += nc;
       maxch = max(maxch, nc);
     }
-    int size = expand(c, F, 0, B, uq, 1.0, 0, -1, lane, pf);
-    while (popped < B && size > 0) {
-      __syncwarp();
-      if (F.score[0] < c.min_score) break;
-      const Cand top = frontier_pop(F, size, lane);
-      --size;
+    Frontier F{Ent{-1.0, META_NONE, NONE}, Ent{-1.0, META_NONE, NONE}, 0};
+    expand(c, F, B, uq, 1.0, 0, -1, lane, pf);
+    prefetch_frontier(c, F, lane);
+    while (popped < B && F.size > 0) {
+      if (__shfl_sync(0xffffffffu, F.e0.score, 0) < c.min_score) break;
+      const Ent top = F.pop(lane);
       const int32_t i = popped++;
+      const int32_t par = meta_parent(top.meta), dep = meta_depth(top.meta);
       if (lane == 0) {
-        const unsigned long long m =
-            (top.parent >= 0 ? F.mask[top.parent] : 0ull) | (1ull << i);
-        F.mask[i] = m;
+        const unsigned long long m = (par >= 0 ? M[par] : 0ull) | (1ull << i);
+        M[i] = m;
         const int64_t o = (int64_t)s * Bmax + i;
-        draft_tok[o] = top.tok;
-        draft_parent[o] = top.parent;
-        draft_depth[o] = top.depth;
-        draft_pos[o] = pb + top.depth;
+        draft_tok[o] = meta_tok(top.meta);
+        draft_parent[o] = par;
+        draft_depth[o] = dep;
+        draft_pos[o] = pb + dep;
         draft_mask[o] = m;
       }
-      __syncwarp();
       const int cap = B - popped;
-      if (size > cap) size = cap;
-      if (g_draft_prof) {
+      if (F.size > cap) F.size = cap;
+      if (prof) {
         const long long nc = ld_rec(c, top.node).x;
         scanned += nc;
         maxch = max(maxch, nc);
       }
-      size = expand(c, F, size, cap, top.node, top.score, top.depth, i, lane, pf);
+      expand(c, F, cap, top.node, top.score, dep, i, lane, pf);
+      prefetch_frontier(c, F, lane);
     }
   }
   for (int32_t i = popped + lane; i < Bmax; i += 32) {
@@ -378,8 +350,8 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   if (lane == 0) {
     match_len[s] = q;
     draft_len[s] = popped;
-    if (g_draft_prof) {
-      long long* o = g_draft_prof + 8 * (int64_t)s;
+    if (prof) {
+      long long* o = prof + 8 * (int64_t)s;
       o[0] = t_match;
       o[1] = clock64() - t_start;
       o[2] = scanned;
@@ -387,7 +359,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       o[4] = pf.rec;
       o[5] = pf.blk;
       o[6] = pf.ld;
-      o[7] = pf.ins;
+      o[7] = pf.pops;
     }
   }
 }

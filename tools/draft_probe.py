@@ -46,10 +46,27 @@ def main():
         print(f"   q hist {np.bincount(q, minlength=9).tolist()}  draft_len mean {dl.mean():.1f}")
         print(f"   children scanned p50 {np.percentile(sc, 50):.0f} p99 {np.percentile(sc, 99):.0f} "
               f"max {sc.max()}; max fan-out p50 {np.percentile(mx, 50):.0f} p99 {np.percentile(mx, 99):.0f} max {mx.max()}")
+        nsing = p[:, 7] & ((1 << 20) - 1)
+        nmul = p[:, 7] >> 20
+        full = dl == cfg["Bmax"]
+        if full.any():
+            f = full
+            print(f"   full drafts: {f.sum()} seqs; per seq mean: single pops {nsing[f].mean():.1f}, "
+                  f"multi pops {nmul[f].mean():.1f}; cycles: total {tot[f].mean():.0f}, match "
+                  f"{mt[f].mean():.0f}, rec waits {p[f, 4].mean():.0f} "
+                  f"({p[f, 4].sum() / max(1, (nsing[f] + nmul[f]).sum()):.0f}/pop), block lookups "
+                  f"{p[f, 5].mean():.0f} ({p[f, 5].sum() / max(1, nmul[f].sum()):.0f}/multi), "
+                  f"child rounds {p[f, 6].mean():.0f} ({p[f, 6].sum() / max(1, nmul[f].sum()):.0f}/multi)")
+        for lo, hi in ((0, 64), (64, 256), (256, 1024), (1024, 1 << 30)):
+            sel = (sc >= lo) & (sc < hi)
+            if sel.any():
+                print(f"   scanned in [{lo},{hi}): {sel.sum()} seqs, cycles p50 "
+                      f"{np.percentile(tot[sel], 50):.0f} p90 {np.percentile(tot[sel], 90):.0f} "
+                      f"max {tot[sel].max()}; draft_len mean {dl[sel].mean():.1f}")
         slow = np.argsort(-tot)[:8]
         for s in slow:
             print(f"   slow seq {s}: cycles {tot[s]} match {mt[s]} q {q[s]} len {dl[s]} scanned {sc[s]} "
-                  f"maxfan {mx[s]} rec {p[s,4]} blk {p[s,5]} ld {p[s,6]} ins {p[s,7]}")
+                  f"maxfan {mx[s]} rec {p[s,4]} blk {p[s,5]} rounds {p[s,6]} single/multi {nsing[s]}/{nmul[s]}")
         run.standin()
         run.cache.verify(run.logits, run.d, run.seq_id, bench.step_seed(0, 100 + k), run.seq_tok,
                          run.seq_len, run.max_new, out=run.v)
