@@ -49,10 +49,10 @@ CONFIGS = {
     # BJ:configs[2] (1024 of the 8192 sequences concurrently).  D = 16: the warm
     # cache (8192 prior rollouts, 57M tokens) has > 1.07B distinct windows at
     # D = 32 (measured: node capacity 2^30 overflowed during the warm-up); at
-    # D = 16 it fits 2^30 nodes
+    # D = 16 it has 483M nodes, within 2^29
     "dapo": dict(V=151936, prompts=512, samples=16, active=1024, Bmax=32, D=16, L=8, median=3000,
-                 cap=20000, act_cap=20000, prior_epochs=1, node_capacity=1 << 30,
-                 slot_capacity=1 << 30,
+                 cap=20000, act_cap=20000, prior_epochs=1, node_capacity=1 << 29,
+                 slot_capacity=1 << 29,
                  # run-ahead generation: rollouts of the next 64 prompts (the
                  # look-ahead window) are inserted as spans of 512-2048 tokens, 8 per step
                  runahead=dict(first=64, prompts=64, per=4, spans=8, lo=512, hi=2048)),

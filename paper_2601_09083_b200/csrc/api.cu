@@ -59,6 +59,8 @@ srt_status validate(const srt_config* c) {
     return SRT_ERR_INVALID_CONFIG;
   if (!is_pow2(c->hash_capacity) || c->hash_capacity < 2 * c->node_capacity)
     return SRT_ERR_INVALID_CONFIG;
+  // node ids are hash slots and then the P roots: all must stay below BAD
+  if (c->hash_capacity + (int64_t)c->max_prompts >= (int64_t)AUX_CHILD0) return SRT_ERR_INVALID_CONFIG;
   if (c->slot_capacity < c->node_capacity || c->slot_capacity >= (int64_t)BAD)
     return SRT_ERR_INVALID_CONFIG;
   if (c->logits_dtype != SRT_BF16 && c->logits_dtype != SRT_F32) return SRT_ERR_INVALID_CONFIG;
@@ -93,10 +95,11 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   if (st != SRT_OK) return st;
   cudaStream_t stream = (cudaStream_t)stream_;
   const size_t N = cfg->node_capacity, H = cfg->hash_capacity, W = cfg->slot_capacity;
+  const size_t NN = H + (size_t)cfg->max_prompts;  // node ids = hash slots, then roots
   size_t off = 0;
-  const size_t o_tok = off;     off = align_up(off + N * 4);
-  const size_t o_cnt = off;     off = align_up(off + N * 4);
-  const size_t o_rec = off;     off = align_up(off + N * 16);
+  const size_t o_tok = off;     off = align_up(off + NN * 4);
+  const size_t o_cnt = off;     off = align_up(off + NN * 4);
+  const size_t o_rec = off;     off = align_up(off + NN * 32);
   const size_t o_hash = off;    off = align_up(off + H * sizeof(HashSlot));
   const size_t o_slots = off;   off = align_up(off + W * 4);
   const size_t o_stok = off;    off = align_up(off + W * 4);
@@ -445,10 +448,12 @@ srt_status srt_cache_dump(srt_cache* c, int32_t p, srt_dump_record* host_buf, in
   struct HNode { int32_t tok; uint32_t cnt; std::vector<int64_t> kids; };
   std::vector<HNode> nodes;
   uint32_t root_nchild = 0;
-  SRT_CUDA(cudaMemcpyAsync(&root_nchild, &c->dev.rec[p].x, 4, cudaMemcpyDeviceToHost, stream), "dump");
+  const uint32_t root = (uint32_t)(c->dev.H + (uint64_t)p);
+  SRT_CUDA(cudaMemcpyAsync(&root_nchild, &c->dev.rec[2 * (size_t)root].x, 4, cudaMemcpyDeviceToHost,
+                           stream), "dump");
   SRT_CUDA(cudaStreamSynchronize(stream), "dump");
   nodes.push_back(HNode{-1, 0, {}});
-  std::vector<uint32_t> frontier = {(uint32_t)p};
+  std::vector<uint32_t> frontier = {root};
   std::vector<int64_t> frontier_idx = {0};
   std::vector<uint32_t> frontier_nch = {root_nchild};
   while (!frontier.empty()) {

@@ -17,17 +17,19 @@ int num_sms() {
 }
 
 __global__ void k_init_counters(DevCache c) {
-  c.ctr[0] = (unsigned long long)c.P;  // node ids 0..P-1 are the roots
+  c.ctr[0] = (unsigned long long)c.P;  // the roots (node ids H .. H+P-1)
   c.ctr[1] = 0;
   *c.status = 0;
 }
 
 cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
   cudaError_t e;
-  if ((e = cudaMemsetAsync(c.tok, 0xFF, c.N * 4, stream)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(c.cnt, 0, c.N * 4, stream)) != cudaSuccess) return e;
-  // rec = {nchild 0, child0 -, token -, csum 0}: child0 is read only if nchild >= 1
-  if ((e = cudaMemsetAsync(c.rec, 0, c.N * 16, stream)) != cudaSuccess) return e;
+  const size_t NN = c.H + (size_t)c.P;  // node ids: hash slots, then the roots
+  if ((e = cudaMemsetAsync(c.tok, 0xFF, NN * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.cnt, 0, NN * 4, stream)) != cudaSuccess) return e;
+  // rec = {nchild 0, child0 -, token -, csum 0 | no blocks}: child0 is read only
+  // if nchild >= 1
+  if ((e = cudaMemsetAsync(c.rec, 0, NN * 32, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.hash, 0xFF, c.H * sizeof(HashSlot), stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.slots, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.stok, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
@@ -104,7 +106,7 @@ __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, u
   const int32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const uint32_t u = frontier[f];
-  const uint4 r = c.rec[u];
+  const uint4 r = *rec_of(c, u);
   const uint32_t F = r.x;
   for (uint32_t k = 0; k < F; ++k) {
     uint32_t ch;
@@ -116,7 +118,7 @@ __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, u
       n = c.cnt[ch];
     } else {
       const uint32_t j = k - 1, i = blk_index(j);
-      const uint32_t pos = hash_find(c, block_key(u, i)) + (j - blk_start(i));
+      const uint32_t pos = block_base(c, u, i) + (j - blk_start(i));
       ch = c.slots[pos];
       tk = c.stok[pos];
       n = c.scnt[pos];
@@ -127,7 +129,7 @@ __global__ void k_dump_level(DevCache c, const uint32_t* frontier, int32_t nf, u
     out_parent[o] = f;
     out_tok[o] = tk;
     out_cnt[o] = n;
-    out_nchild[o] = c.rec[ch].x;
+    out_nchild[o] = rec_of(c, ch)->x;
   }
 }
 

@@ -165,7 +165,7 @@ __device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, doub
   // block bases of blocks 0..nb-1 (children 1..nch-1), one lane each
   const uint32_t nb = blk_index(nch - 2) + 1;
   t0 = clock64();
-  const uint32_t mybase = lane < (int)nb ? hash_find(c, block_key(u, lane)) : 0u;
+  const uint32_t mybase = lane < (int)nb ? block_base(c, u, lane) : 0u;
   __syncwarp();
   pf.blk += clock64() - t0;
   t0 = clock64();
@@ -239,13 +239,9 @@ __device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, doub
 }
 
 // Warm L1 with what popping the next frontier entries reads first: their
-// records and the home slot of their first child block's hash key.
+// 32-byte records (child count, first child, csum and the first child blocks).
 __device__ __forceinline__ void prefetch_frontier(const DevCache& c, const Frontier& F, int lane) {
-  if (lane < 4 && lane < F.size) {
-    const uint32_t u = F.e0.node;
-    prefetch_l1(&c.rec[u]);
-    prefetch_l1(&c.hash[mix64(block_key(u, 0)) & (c.H - 1)]);
-  }
+  if (lane < 4 && lane < F.size) prefetch_l1(rec_of(c, F.e0.node));
 }
 
 __global__ void __launch_bounds__(DRAFT_WARPS * 32)
@@ -279,7 +275,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     const int32_t qmax = min(c.L, t);
     const int32_t myq = lane + 1;
     bool ok = myq <= qmax;
-    uint32_t node = (uint32_t)p;
+    uint32_t node = root_id(c, p);
     if (ok) {
       for (int32_t j = t - myq; j < t; ++j) {
         const int32_t tk = y[j];

@@ -1,20 +1,27 @@
 // srt_internal.cuh — device-side data structures and primitives of libsrt.
 //
-// Layout of one cache in HBM.  All prompts share one node pool;
-// node id p (0 <= p < P) is the root of prompt p's tree T_p.
-//   tok[N]     i32  token labelling the edge into the node
-//   cnt[N]     u32  count(u) ("frequency statistics"; reading O1)
-//   rec[N]     16 B {nchild, child0, token of child0, csum}: one load per pop;
+// Layout of one cache in HBM.  All prompts share one node pool.
+// A node's id IS the index of its edge's slot in the hash (so a lookup or a
+// CAS that claims a new edge yields the child's id with no allocation step);
+// the root of prompt p's tree T_p is node H + p.  Node arrays are
+// sized H + P:
+//   tok[]      i32  token labelling the edge into the node
+//   cnt[]      u32  count(u) ("frequency statistics"; reading O1)
+//   rec[]      32 B {nchild, child0, token of child0, csum, base of child
+//                   blocks 0..3 (+1; 0 = not yet created)}: one load per pop;
 //                   csum = sum of the children's counts (the denominator of
 //                   C(v)), maintained by insert alongside cnt
-//   hash[H]    16 B open-addressing edge hash: key (parent << 32) | token -> child id;
-//                   keys (node << 32) | 0x80000000 | i -> word offset of child block i
+//   hash[H]    16 B open-addressing edge hash: key (parent << 32) | token, the
+//                   child's slot word in aux (the child's id = the slot index);
+//                   keys (node << 32) | 0x80000000 | i -> word offset of child
+//                   block i >= 4 in val (blocks 0..3 are in the record)
 //   slots[W]   u32  child-id blocks for children 1.. : 4, 4, 8, 16, 32, 64, ...
 //                   (geometric, so a hub node with F children has O(log F) blocks)
 //   stok[W], scnt[W]  the token and a mirror of the count of the child in each
 //                   slot, so a node's children enumerate with coalesced loads
 // Concurrency: insertion creates nodes with a CAS on the hash key and publishes
-// the value with one 64-bit store (polled by racing threads); counts are atomic adds, so the logical tree
+// the child's slot word afterwards (polled by racing threads that need it);
+// counts are atomic adds, so the logical tree
 // (set of (path, count)) does not depend on scheduling.  Node ids do, but no
 // output exposes them (draft order uses counts + tokens only; O8/O15).
 #pragma once
@@ -28,13 +35,14 @@ namespace srt {
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;  // "no block" / "value pending"
 constexpr uint32_t BAD = 0xFFFFFFFEu;   // creation failed (capacity): walk stops
+constexpr uint32_t AUX_CHILD0 = 0xFFFFFFFDu;  // edge aux: the child is its parent's inline child 0
 constexpr unsigned long long EMPTY_KEY = ~0ull;
 constexpr uint32_t BLOCK_TAG = 0x80000000u;  // tokens are < 2^31
 
-// val and aux are published together by one 64-bit release store (pending =
-// both NONE).  Edge entries: val = child id, aux = the child's slot word in its
-// parent's child blocks (NONE for the inline child 0).  Block entries: val =
-// the block's first slot word.
+// Edge entries: aux = the child's slot word in its parent's child blocks
+// (AUX_CHILD0 for the inline child 0; NONE until published), val unused.
+// Block entries (blocks >= 4): val = the block's first slot word (NONE until
+// published).
 struct alignas(16) HashSlot {
   unsigned long long key;
   uint32_t val;
@@ -52,12 +60,13 @@ struct DevCache {
   unsigned long long N, H, W;
   int32_t* tok;
   uint32_t* cnt;
-  uint4* rec;  // .x nchild, .y child0, .z token of child0, .w csum
+  uint4* rec;  // 2 per node: [2u] = {nchild, child0, token of child0, csum},
+               //             [2u+1] = child block bases 0..3, each + 1 (0 = none yet)
   HashSlot* hash;
   uint32_t* slots;  // child ids (children 1.. of a node, in its blocks)
   int32_t* stok;    // their tokens (immutable)
   uint32_t* scnt;   // mirrors of their counts, contiguous for enumeration
-  unsigned long long* ctr;  // [0] next node id, [1] next slot word
+  unsigned long long* ctr;  // [0] nodes created (+ P roots), [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
   float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima
 };
@@ -122,6 +131,12 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   return z ^ (z >> 31);
 }
 
+// Home slot of a key: linear probing from an EVEN slot, so the first two
+// probes are one aligned 32-byte load (insert reads slot pairs).
+__device__ __forceinline__ unsigned long long home_slot(const DevCache& c, unsigned long long key) {
+  return mix64(key) & (c.H - 1) & ~1ull;
+}
+
 __device__ __forceinline__ unsigned long long edge_key(uint32_t parent, uint32_t tok) {
   return ((unsigned long long)parent << 32) | tok;
 }
@@ -141,7 +156,7 @@ __device__ __forceinline__ uint32_t blk_size(uint32_t i) { return i < 2 ? 4u : (
 // Returns NONE if the key is absent.
 __device__ __forceinline__ uint32_t hash_find(const DevCache& c, unsigned long long key) {
   unsigned long long mask = c.H - 1;
-  unsigned long long h = mix64(key) & mask;
+  unsigned long long h = home_slot(c, key);
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
     const HashSlot* s = c.hash + h;
     const unsigned long long k = __ldg(&s->key);
@@ -152,11 +167,42 @@ __device__ __forceinline__ uint32_t hash_find(const DevCache& c, unsigned long l
   return NONE;
 }
 
-__device__ __forceinline__ uint32_t child_of(const DevCache& c, uint32_t u, int32_t tok) {
-  return hash_find(c, edge_key(u, (uint32_t)tok));
+// Slot index of `key` (= the child's node id for an edge key), NONE if absent.
+__device__ __forceinline__ uint32_t hash_slot(const DevCache& c, unsigned long long key) {
+  unsigned long long mask = c.H - 1;
+  unsigned long long h = home_slot(c, key);
+  for (unsigned long long probe = 0; probe <= mask; ++probe) {
+    const unsigned long long k = __ldg(&c.hash[h].key);
+    if (k == key) return (uint32_t)h;
+    if (k == EMPTY_KEY) return NONE;
+    h = (h + 1) & mask;
+  }
+  return NONE;
 }
 
-__device__ __forceinline__ uint4 ld_rec(const DevCache& c, uint32_t u) { return __ldg(&c.rec[u]); }
+__device__ __forceinline__ uint32_t child_of(const DevCache& c, uint32_t u, int32_t tok) {
+  return hash_slot(c, edge_key(u, (uint32_t)tok));
+}
+
+__device__ __forceinline__ uint32_t root_id(const DevCache& c, int32_t p) {
+  return (uint32_t)(c.H + (unsigned long long)p);
+}
+
+// record of node u: {nchild, child0, token of child0, csum}
+__device__ __forceinline__ uint4 ld_rec(const DevCache& c, uint32_t u) { return __ldg(&c.rec[2 * (size_t)u]); }
+__device__ __forceinline__ uint4* rec_of(const DevCache& c, uint32_t u) { return &c.rec[2 * (size_t)u]; }
+// the record's block words (base of child block i < 4, + 1; 0 = not created)
+__device__ __forceinline__ uint32_t* rec_bases(const DevCache& c, uint32_t u) {
+  return reinterpret_cast<uint32_t*>(&c.rec[2 * (size_t)u + 1]);
+}
+// First slot word of child block i of node u (read-only kernels).
+__device__ __forceinline__ uint32_t block_base(const DevCache& c, uint32_t u, uint32_t i) {
+  if (i < 4) {
+    const uint32_t b = __ldg(rec_bases(c, u) + i);
+    return b ? b - 1 : NONE;
+  }
+  return hash_find(c, block_key(u, i));
+}
 
 // Child k of node u (read-only kernels; slow path — enumeration loops look the
 // block bases up once).  Child 0 is inline in rec; child k >= 1 is slot k-1.
@@ -165,7 +211,7 @@ __device__ __forceinline__ uint32_t child_at(const DevCache& c, uint32_t u, uint
   if (k == 0) return child0;
   const uint32_t j = k - 1;
   const uint32_t i = blk_index(j);
-  return c.slots[hash_find(c, block_key(u, i)) + (j - blk_start(i))];
+  return c.slots[block_base(c, u, i) + (j - blk_start(i))];
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

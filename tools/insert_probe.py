@@ -58,7 +58,30 @@ def main():
               f"invalid cursors {(act & (p[:, 5] == 0)).sum()}")
         for s_ in np.argsort(-tot)[:6]:
             print(f"   slow seq {s_}: cycles {p[s_, 0]} cursor {p[s_, 1]} positions {p[s_, 2]} "
-                  f"created {p[s_, 3]} slowest position {p[s_, 4]} valid {p[s_, 5]}")
+                  f"created {p[s_, 3]} slowest position {p[s_, 4]} valid {p[s_, 5]} batch {p[s_, 6]} "
+                  f"resolve {p[s_, 7] >> 32} counts {p[s_, 7] & 0xFFFFFFFF}")
+    # the longest span alone (every other sequence's span empty), then the rest
+    for k in range(2):
+        run.draft()
+        run.standin()
+        run.cache.verify(run.logits, run.d, run.seq_id, bench.step_seed(0, 20 + k), run.seq_tok,
+                         run.seq_len, run.max_new, out=run.v, rows=run.rows_max)
+        torch.cuda.synchronize()
+        nc = run.v.n_commit
+        big = int(torch.argmax(nc).item())
+        to1 = run.t_before.clone()
+        to1[big] = run.seq_len[big]
+        prof.zero_()
+        us1 = timed(lambda: run.cache.insert(run.prompt_id, run.seq_tok, run.t_before, to1,
+                                             cursor=run.cursor))
+        p1 = prof[big].cpu().numpy()
+        fr2 = run.t_before.clone()
+        fr2[big] = run.seq_len[big]
+        us2 = timed(lambda: run.cache.insert(run.prompt_id, run.seq_tok, fr2, run.seq_len,
+                                             cursor=run.cursor))
+        print(f"alone: seq {big} span {int(nc[big])}: insert {us1:.1f} us, cycles {p1[0]} "
+              f"slowest position {p1[4]} created {p1[3]} batch {p1[6] >> 20} rounds {p1[6] & 0xFFFFF} resolve {p1[7] >> 32} "
+              f"counts {p1[7] & 0xFFFFFFFF}; the other 1023 spans: {us2:.1f} us")
     L.srt_debug_insert_profile(ctypes.c_void_p(0))
     ar = torch.arange(n, device=run.dev)
     for m in (1, 2, 4, 8, 16, 24, 32):
