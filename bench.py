@@ -295,7 +295,8 @@ class Group:
         self.t_before.copy_(self.seq_len)
 
     def draft(self):
-        self.cache.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d)
+        self.cache.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d,
+                         cursor=self.cursor)
 
     def verify_insert(self, seed: int, logits=None):
         c = self.cache

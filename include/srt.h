@@ -205,6 +205,23 @@ SRT_API srt_status srt_draft(srt_cache* cache, int32_t n, const int32_t* prompt_
                      void* stream);
 
 /*
+ * srt_draft_cursor — srt_draft with the suffix cursors srt_insert_cursor
+ * keeps (cursor[s*(D+4) ...], caller-owned DEVICE memory, read only).  Same
+ * outputs as srt_draft.  When sequence s's cursor is valid for this cache and
+ * sits at t = seq_len[s] with floor 0, its suffix nodes A_q are exactly the
+ * nodes of y[t-q .. t-1], so the match (O3) reads the L candidates' records in
+ * one round trip instead of walking q hops from the root; otherwise the
+ * sequence walks as in srt_draft.
+ */
+SRT_API srt_status srt_draft_cursor(srt_cache* cache, int32_t n, const int32_t* prompt_id,
+                                    const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
+                                    const int32_t* pos_base, const uint32_t* cursor,
+                                    int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
+                                    int32_t* draft_parent, int32_t* draft_depth,
+                                    int32_t* draft_pos, uint64_t* draft_mask,
+                                    int64_t* row_offsets, void* stream);
+
+/*
  * srt_verify — lossless verification ("verifies and accepts drafted
  * tokens up to the first mismatch"; "one decode pass ... verify
  * multiple drafted tokens in parallel"; readings O10, O11, O13).

@@ -226,6 +226,17 @@ srt_status srt_draft(srt_cache* c, int32_t n, const int32_t* prompt_id, const in
                      int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
                      int32_t* draft_parent, int32_t* draft_depth, int32_t* draft_pos,
                      uint64_t* draft_mask, int64_t* row_offsets, void* stream) {
+  return srt_draft_cursor(c, n, prompt_id, seq_tok, stride, seq_len, pos_base, nullptr, match_len,
+                          draft_len, draft_tok, draft_parent, draft_depth, draft_pos, draft_mask,
+                          row_offsets, stream);
+}
+
+srt_status srt_draft_cursor(srt_cache* c, int32_t n, const int32_t* prompt_id,
+                            const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
+                            const int32_t* pos_base, const uint32_t* cursor, int32_t* match_len,
+                            int32_t* draft_len, int32_t* draft_tok, int32_t* draft_parent,
+                            int32_t* draft_depth, int32_t* draft_pos, uint64_t* draft_mask,
+                            int64_t* row_offsets, void* stream) {
   if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (!row_offsets) return SRT_ERR_INVALID_ARG;
   if (n > 0 && (!prompt_id || !seq_tok || !seq_len || !match_len || !draft_len || !draft_tok ||
@@ -236,8 +247,8 @@ srt_status srt_draft(srt_cache* c, int32_t n, const int32_t* prompt_id, const in
     SRT_CUDA(timed(c, SRT_K_DRAFT, st,
                    [&] {
                      return launch_draft(c->dev, n, prompt_id, seq_tok, stride, seq_len, pos_base,
-                                         match_len, draft_len, draft_tok, draft_parent,
-                                         draft_depth, draft_pos, draft_mask, st);
+                                         cursor, c->tag, match_len, draft_len, draft_tok,
+                                         draft_parent, draft_depth, draft_pos, draft_mask, st);
                    }),
              "draft");
   SRT_CUDA(timed(c, SRT_K_ROW_OFFSETS, st,

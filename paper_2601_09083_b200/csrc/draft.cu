@@ -247,8 +247,9 @@ __device__ __forceinline__ void prefetch_frontier(const DevCache& c, const Front
 __global__ void __launch_bounds__(DRAFT_WARPS * 32)
 k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ seq_len,
-        const int32_t* __restrict__ pos_base, int32_t* __restrict__ match_len,
-        int32_t* __restrict__ draft_len, int32_t* __restrict__ draft_tok,
+        const int32_t* __restrict__ pos_base, const uint32_t* __restrict__ cursor, uint32_t tag,
+        int32_t* __restrict__ match_len, int32_t* __restrict__ draft_len,
+        int32_t* __restrict__ draft_tok,
         int32_t* __restrict__ draft_parent, int32_t* __restrict__ draft_depth,
         int32_t* __restrict__ draft_pos, uint64_t* __restrict__ draft_mask) {
   __shared__ unsigned long long masks[DRAFT_WARPS][64];  // ancestor-or-self masks (O9)
@@ -276,7 +277,20 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     const int32_t myq = lane + 1;
     bool ok = myq <= qmax;
     uint32_t node = root_id(c, p);
-    if (ok) {
+    // a valid cursor at t with floor 0 holds node(y[t-q .. t-1]) for every
+    // q <= min(D, t) (L <= D): no walk
+    bool walk = true;
+    if (cursor) {
+      const uint32_t* cur = cursor + (size_t)s * (c.D + 4);
+      if (cur[0] == tag && cur[1] == (uint32_t)t && cur[2] == (uint32_t)p && cur[3] == 0u) {
+        walk = false;
+        if (ok) {
+          node = cur[4 + myq - 1];
+          ok = node < BAD;
+        }
+      }
+    }
+    if (ok && walk) {
       for (int32_t j = t - myq; j < t; ++j) {
         const int32_t tk = y[j];
         if (tk < 0 || tk >= c.V) {
@@ -406,14 +420,15 @@ cudaError_t set_draft_profile(long long* buf) {
 
 cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
-                         const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                         const int32_t* pos_base, const uint32_t* cursor, uint32_t tag,
+                         int32_t* match_len, int32_t* draft_len,
                          int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
                          int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   carveout_once<k_draft>();
   k_draft<<<(n + DRAFT_WARPS - 1) / DRAFT_WARPS, DRAFT_WARPS * 32, 0, stream>>>(
-      c, n, prompt_id, seq_tok, stride, seq_len, pos_base, match_len, draft_len, draft_tok,
-      draft_parent, draft_depth, draft_pos, draft_mask);
+      c, n, prompt_id, seq_tok, stride, seq_len, pos_base, cursor, tag, match_len, draft_len,
+      draft_tok, draft_parent, draft_depth, draft_pos, draft_mask);
   return cudaGetLastError();
 }
 

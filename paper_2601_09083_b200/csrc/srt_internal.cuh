@@ -255,7 +255,8 @@ cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prom
                                const long long* scratch, cudaStream_t stream);
 cudaError_t launch_draft(const DevCache& c, int32_t n, const int32_t* prompt_id,
                          const int32_t* seq_tok, int64_t stride, const int32_t* seq_len,
-                         const int32_t* pos_base, int32_t* match_len, int32_t* draft_len,
+                         const int32_t* pos_base, const uint32_t* cursor, uint32_t tag,
+                         int32_t* match_len, int32_t* draft_len,
                          int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
                          int32_t* draft_pos, uint64_t* draft_mask, cudaStream_t stream);
 cudaError_t set_draft_profile(long long* buf);

@@ -143,20 +143,23 @@ class SrtCache:
         """Zero-filled (= invalid, rebuilt on first use) insert cursors for n sequences."""
         return torch.zeros((n, self.cfg.max_depth + 4), dtype=torch.int32, device=device)
 
-    def draft(self, prompt_id, seq_tok, seq_len, pos_base=None, out: DraftOut | None = None
-              ) -> DraftOut:
+    def draft(self, prompt_id, seq_tok, seq_len, pos_base=None, out: DraftOut | None = None,
+              cursor=None) -> DraftOut:
+        """srt_draft, or srt_draft_cursor when the insert cursors are given."""
         n = prompt_id.shape[0]
         if out is None:
             out = DraftOut.empty(n, self.Bmax, seq_tok.device)
         i32 = torch.int32
-        check(self.L.srt_draft(self._h, n, _ptr(prompt_id, i32, "prompt_id"),
-                               _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
-                               _ptr(seq_len, i32, "seq_len"), _ptr(pos_base, i32, "pos_base"),
-                               _ptr(out.match_len, i32), _ptr(out.draft_len, i32),
-                               _ptr(out.draft_tok, i32), _ptr(out.draft_parent, i32),
-                               _ptr(out.draft_depth, i32), _ptr(out.draft_pos, i32),
-                               _ptr(out.draft_mask, torch.int64), _ptr(out.row_offsets, torch.int64),
-                               _stream()), "srt_draft")
+        head = (self._h, n, _ptr(prompt_id, i32, "prompt_id"), _ptr(seq_tok, i32, "seq_tok"),
+                seq_tok.shape[1], _ptr(seq_len, i32, "seq_len"), _ptr(pos_base, i32, "pos_base"))
+        tail = (_ptr(out.match_len, i32), _ptr(out.draft_len, i32), _ptr(out.draft_tok, i32),
+                _ptr(out.draft_parent, i32), _ptr(out.draft_depth, i32), _ptr(out.draft_pos, i32),
+                _ptr(out.draft_mask, torch.int64), _ptr(out.row_offsets, torch.int64), _stream())
+        if cursor is None:
+            check(self.L.srt_draft(*head, *tail), "srt_draft")
+        else:
+            check(self.L.srt_draft_cursor(*head, _ptr(cursor, torch.int32, "cursor"), *tail),
+                  "srt_draft_cursor")
         return out
 
     def verify(self, logits, d: DraftOut, seq_id, seed: int, seq_tok, seq_len, max_new,

@@ -34,7 +34,8 @@ def main():
     L.srt_debug_draft_profile(ctypes.c_void_p(prof.data_ptr()))
     for k in range(a.steps):
         torch.cuda.synchronize()
-        run.cache.draft(run.prompt_id, run.seq_tok, run.seq_len, run.seq_len, out=run.d)
+        run.cache.draft(run.prompt_id, run.seq_tok, run.seq_len, run.seq_len, out=run.d,
+                        cursor=run.cursor)
         torch.cuda.synchronize()
         p = prof.cpu().numpy()
         q = run.d.match_len.cpu().numpy()
