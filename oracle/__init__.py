@@ -87,6 +87,10 @@ def lib():
         L.orc_verify.restype = ctypes.c_int
         L.orc_dump.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i32p, _u64p, _i32p, ctypes.c_int64]
         L.orc_dump.restype = ctypes.c_int64
+        L.orc_prune.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64]
+        L.orc_prune.restype = ctypes.c_int64
+        L.orc_load.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i32p, _u64p, _i32p, ctypes.c_int64]
+        L.orc_load.restype = ctypes.c_int32
         L.orc_count_of.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i32p, ctypes.c_int32]
         L.orc_count_of.restype = ctypes.c_uint64
         _lib = L
@@ -241,6 +245,22 @@ class Oracle:
                 return np.stack([tok[:k].astype(np.int64), cnt[:k].astype(np.int64),
                                  nch[:k].astype(np.int64)], axis=1)
             cap = int(k)
+
+    def prune(self, p, theta) -> int:
+        """Remove every non-root node of T_p (all prompts if p < 0) with count < theta."""
+        r = lib().orc_prune(self.h, int(p), int(theta))
+        if r < 0:
+            raise ValueError("bad prompt id")
+        return int(r)
+
+    def load(self, p, records):
+        """Merge dump records [(token, count, n_children), ...] (preorder) into T_p."""
+        r = np.asarray(records, np.int64).reshape(-1, 3)
+        tok = np.ascontiguousarray(r[:, 0], np.int32)
+        cnt = np.ascontiguousarray(r[:, 1], np.uint64)
+        nch = np.ascontiguousarray(r[:, 2], np.int32)
+        if lib().orc_load(self.h, int(p), tok, cnt, nch, r.shape[0]) != 0:
+            raise ValueError("malformed dump records")
 
     def count_of(self, p, tokens) -> int:
         t = np.ascontiguousarray(tokens, np.int32)

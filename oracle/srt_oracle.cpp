@@ -569,6 +569,67 @@ int64_t orc_dump(void* h, int32_t p, int32_t* tok, uint64_t* count, int32_t* nch
   return k;
 }
 
+// ---------------------------------------------------------------------------
+// Capacity management (reading O17 in DESIGN.md).  The paper
+// bounds nothing ("can be stored in CPU memory"); SPEC's evict
+// removes whole subtrees in ascending count order.  Reading:
+// prune(p, theta) removes every non-root node whose count is below theta.
+// Because count(u) >= the count of each child (O1), that set is closed under
+// descendants, so exactly whole subtrees go, lowest counts first.
+// ---------------------------------------------------------------------------
+static uint64_t prune_node(Node* u, uint64_t theta) {
+  uint64_t removed = 0;
+  for (auto it = u->kids.begin(); it != u->kids.end();) {
+    if (it->second->count < theta) {
+      std::vector<Node*> stack = {it->second.get()};  // count the subtree
+      while (!stack.empty()) {
+        Node* v = stack.back();
+        stack.pop_back();
+        ++removed;
+        for (auto& kv : v->kids) stack.push_back(kv.second.get());
+      }
+      it = u->kids.erase(it);
+    } else {
+      removed += prune_node(it->second.get(), theta);
+      ++it;
+    }
+  }
+  return removed;
+}
+
+// Remove every non-root node of T_p (every p if p < 0) with count < theta.
+// Returns the number of nodes removed.
+int64_t orc_prune(void* h, int32_t p, uint64_t theta) {
+  Cache* c = (Cache*)h;
+  if (p >= c->cfg.max_prompts) return -1;
+  uint64_t removed = 0;
+  for (int32_t q = 0; q < c->cfg.max_prompts; ++q)
+    if (p < 0 || q == p) removed += prune_node(c->roots[q].get(), theta);
+  c->nodes -= removed;
+  return (int64_t)removed;
+}
+
+// Merge a canonical dump (orc_dump's records, preorder) into T_p: every
+// record's path is created if missing and its count added.  Loading a dump
+// into an empty tree reproduces it exactly (persistence across training
+// steps).  Returns 0, or -1 for a malformed record list.
+int32_t orc_load(void* h, int32_t p, const int32_t* tok, const uint64_t* count,
+                 const int32_t* nchild, int64_t n) {
+  Cache* c = (Cache*)h;
+  if (p < 0 || p >= c->cfg.max_prompts || n < 1 || tok[0] != -1) return -1;
+  // (node, children still to read) along the current preorder path
+  std::vector<std::pair<Node*, int32_t>> path = {{c->roots[p].get(), nchild[0]}};
+  for (int64_t k = 1; k < n; ++k) {
+    while (!path.empty() && path.back().second == 0) path.pop_back();
+    if (path.empty()) return -1;
+    path.back().second -= 1;
+    Node* v = child_or_create(c, path.back().first, tok[k]);
+    v->count += count[k];
+    path.push_back({v, nchild[k]});
+  }
+  return 0;
+}
+
 // Count of a string (root walk), 0 if absent.  Test helper.
 uint64_t orc_count_of(void* h, int32_t p, const int32_t* toks, int32_t len) {
   Cache* c = (Cache*)h;
