@@ -325,6 +325,34 @@ SRT_API srt_status srt_cache_dump(srt_cache* cache, int32_t prompt_id, srt_dump_
 SRT_API srt_status srt_cache_status(srt_cache* cache, uint32_t* dev_error_bits, srt_cache_stats* stats,
                             void* stream);
 
+/*
+ * Capacity management and persistence (O17).  The
+ * paper bounds nothing; these are maintenance calls between steps,
+ * all BLOCKING (they synchronise `stream`), none on the per-step path.
+ *
+ * srt_cache_prune — remove every non-root node of T_p (every prompt if
+ *   prompt_id = -1) whose count is below theta, i.e. the lowest-count whole
+ *   subtrees (count(u) >= the count of each child, O1).  theta = UINT32_MAX
+ *   resets T_p.  Kept children are compacted in their parents' child lists;
+ *   removed edges become hash tombstones (their slots are not reused until the
+ *   cache is rebuilt, e.g. by dump + load into a new cache).  Every insert
+ *   cursor of this cache becomes invalid (rebuilt on its next use).
+ *   *removed (HOST, nullable) = nodes removed.
+ * srt_cache_evict — if more than max_nodes nodes are live, prune every tree
+ *   with the smallest theta that leaves at most 0.9 * max_nodes (hysteresis,
+ *   S:L121); *theta_out (HOST, nullable) = the theta used (0 = nothing done).
+ * srt_cache_load — merge a canonical dump of T_p (srt_cache_dump's records,
+ *   HOST memory) into T_p: paths are created as needed and counts added, so a
+ *   dump loaded into an empty tree (a new cache, or after a reset) restores
+ *   it exactly.  SRT_ERR_INVALID_ARG for a malformed list.
+ */
+SRT_API srt_status srt_cache_prune(srt_cache* cache, int32_t prompt_id, uint32_t theta,
+                                   int64_t* removed, void* stream);
+SRT_API srt_status srt_cache_evict(srt_cache* cache, int64_t max_nodes, int64_t* removed,
+                                   uint32_t* theta_out, void* stream);
+SRT_API srt_status srt_cache_load(srt_cache* cache, int32_t prompt_id,
+                                  const srt_dump_record* host_buf, int64_t n_records, void* stream);
+
 /* Clear the sticky error bits (not SRT_DEV_CAPACITY, which poisons). */
 SRT_API srt_status srt_cache_clear_errors(srt_cache* cache, void* stream);
 

@@ -336,6 +336,153 @@ srt_status srt_cache_status(srt_cache* c, uint32_t* bits, srt_cache_stats* stats
   return h_status ? SRT_ERR_DEVICE : SRT_OK;
 }
 
+namespace {
+// device scratch for the maintenance calls (freed at the end of each call)
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st;
+  explicit DevBuf(cudaStream_t s) : st(s) {}
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, st); }
+};
+
+uint32_t next_tag(uint32_t tag) {
+  uint64_t z = (uint64_t)tag * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  return (uint32_t)(z ^ (z >> 31)) | 1u;
+}
+}  // namespace
+
+srt_status srt_cache_prune(srt_cache* c, int32_t p, uint32_t theta, int64_t* removed_out,
+                           void* stream_) {
+  if (!c || p < -1 || p >= c->cfg.max_prompts) return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint32_t bits = 0;
+  srt_cache_stats st{};
+  srt_status s0 = srt_cache_status(c, &bits, &st, stream);
+  if (s0 == SRT_ERR_CUDA) return s0;
+  if (bits & SRT_DEV_CAPACITY) return SRT_ERR_DEVICE;
+  // frontiers hold at most every live node; [4] counters
+  const size_t cap = st.nodes_used + 64;
+  DevBuf buf(stream);
+  SRT_CUDA(buf.alloc(4 * cap * 4 + 64), "cudaMallocAsync(prune)");
+  uint32_t* fk[2] = {(uint32_t*)buf.p, (uint32_t*)buf.p + cap};
+  uint32_t* fd[2] = {(uint32_t*)buf.p + 2 * cap, (uint32_t*)buf.p + 3 * cap};
+  unsigned* cnt = (unsigned*)((uint32_t*)buf.p + 4 * cap);           // [0] keep, [1] dead
+  unsigned long long* removed = (unsigned long long*)(cnt + 4);     // 8-byte aligned
+  std::vector<uint32_t> roots;
+  for (int32_t q = 0; q < c->cfg.max_prompts; ++q)
+    if (p < 0 || q == p) roots.push_back((uint32_t)(c->dev.H + (uint64_t)q));
+  SRT_CUDA(cudaMemcpyAsync(fk[0], roots.data(), roots.size() * 4, cudaMemcpyHostToDevice, stream),
+           "prune");
+  SRT_CUDA(cudaMemsetAsync(removed, 0, 8, stream), "prune");
+  int64_t nk = (int64_t)roots.size(), nd = 0;
+  int cur = 0;
+  while (nk > 0 || nd > 0) {
+    SRT_CUDA(cudaMemsetAsync(cnt, 0, 8, stream), "prune");
+    SRT_CUDA(launch_prune_level(c->dev, fk[cur], (int32_t)nk, theta, fk[cur ^ 1], cnt,
+                                fd[cur ^ 1], cnt + 1, stream), "prune level");
+    SRT_CUDA(launch_kill_level(c->dev, fd[cur], (int32_t)nd, fd[cur ^ 1], cnt + 1, removed, stream),
+             "kill level");
+    unsigned h[2];
+    SRT_CUDA(cudaMemcpyAsync(h, cnt, 8, cudaMemcpyDeviceToHost, stream), "prune");
+    SRT_CUDA(cudaStreamSynchronize(stream), "prune");
+    nk = h[0];
+    nd = h[1];
+    cur ^= 1;
+  }
+  unsigned long long h_removed = 0, h_ctr = 0;
+  SRT_CUDA(cudaMemcpyAsync(&h_removed, removed, 8, cudaMemcpyDeviceToHost, stream), "prune");
+  SRT_CUDA(cudaMemcpyAsync(&h_ctr, c->dev.ctr, 8, cudaMemcpyDeviceToHost, stream), "prune");
+  SRT_CUDA(cudaStreamSynchronize(stream), "prune");
+  h_ctr -= h_removed;
+  SRT_CUDA(cudaMemcpyAsync(c->dev.ctr, &h_ctr, 8, cudaMemcpyHostToDevice, stream), "prune");
+  SRT_CUDA(cudaStreamSynchronize(stream), "prune");
+  c->tag = next_tag(c->tag);  // cursors may name removed nodes: invalidate all
+  if (removed_out) *removed_out = (int64_t)h_removed;
+  return SRT_OK;
+}
+
+srt_status srt_cache_evict(srt_cache* c, int64_t max_nodes, int64_t* removed_out,
+                           uint32_t* theta_out, void* stream_) {
+  if (!c || max_nodes < 0) return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  constexpr int NB = 1 << 16;  // exact counts below 65535, one bin above
+  DevBuf buf(stream);
+  SRT_CUDA(buf.alloc(NB * 8), "cudaMallocAsync(evict)");
+  SRT_CUDA(cudaMemsetAsync(buf.p, 0, NB * 8, stream), "evict");
+  SRT_CUDA(launch_count_hist(c->dev, (unsigned long long*)buf.p, NB, stream), "count hist");
+  std::vector<unsigned long long> hist(NB);
+  SRT_CUDA(cudaMemcpyAsync(hist.data(), buf.p, NB * 8, cudaMemcpyDeviceToHost, stream), "evict");
+  SRT_CUDA(cudaStreamSynchronize(stream), "evict");
+  unsigned long long live = 0;
+  for (auto x : hist) live += x;
+  if (removed_out) *removed_out = 0;
+  if (theta_out) *theta_out = 0;
+  if (live <= (unsigned long long)max_nodes) return SRT_OK;
+  // smallest theta leaving at most 0.9 * max_nodes nodes (count >= theta)
+  const unsigned long long target = (unsigned long long)(0.9 * (double)max_nodes);
+  unsigned long long above = 0;
+  uint32_t theta = NB - 1;
+  for (int b = NB - 1; b >= 1; --b) {
+    if (above + hist[b] > target) {
+      theta = (uint32_t)b + 1;
+      break;
+    }
+    above += hist[b];
+    theta = (uint32_t)b;
+  }
+  if (theta_out) *theta_out = theta;
+  return srt_cache_prune(c, -1, theta, removed_out, stream);
+}
+
+srt_status srt_cache_load(srt_cache* c, int32_t p, const srt_dump_record* recs, int64_t n,
+                          void* stream_) {
+  if (!c || p < 0 || p >= c->cfg.max_prompts || n < 1 || !recs || recs[0].token != -1)
+    return SRT_ERR_INVALID_ARG;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  // preorder -> levels: (index of the parent in the previous level, token, count)
+  struct Lvl { std::vector<int32_t> par, tok; std::vector<unsigned long long> cnt; };
+  std::vector<Lvl> lv(1);
+  std::vector<std::pair<int32_t, int32_t>> path = {{0, recs[0].n_children}};  // (idx, left)
+  for (int64_t k = 1; k < n; ++k) {
+    while (!path.empty() && path.back().second == 0) path.pop_back();
+    if (path.empty() || recs[k].token < 0 || recs[k].n_children < 0) return SRT_ERR_INVALID_ARG;
+    path.back().second -= 1;
+    const size_t d = path.size();
+    if (lv.size() <= d) lv.resize(d + 1);
+    lv[d].par.push_back(path.back().first);
+    lv[d].tok.push_back(recs[k].token);
+    lv[d].cnt.push_back(recs[k].count);
+    path.push_back({(int32_t)lv[d].tok.size() - 1, recs[k].n_children});
+  }
+  size_t maxn = 1;
+  for (auto& l : lv) maxn = std::max(maxn, l.tok.size());
+  DevBuf buf(stream);
+  SRT_CUDA(buf.alloc(maxn * (4 + 4 + 4 + 8 + 4) + 64), "cudaMallocAsync(load)");
+  uint32_t* ids[2] = {(uint32_t*)buf.p, (uint32_t*)buf.p + maxn};
+  int32_t* d_par = (int32_t*)((uint32_t*)buf.p + 2 * maxn);
+  int32_t* d_tok = d_par + maxn;
+  unsigned long long* d_cnt = (unsigned long long*)(((uintptr_t)(d_tok + maxn) + 7) & ~uintptr_t(7));
+  const uint32_t root = (uint32_t)(c->dev.H + (uint64_t)p);
+  SRT_CUDA(cudaMemcpyAsync(ids[0], &root, 4, cudaMemcpyHostToDevice, stream), "load");
+  int cur = 0;
+  for (size_t d = 1; d < lv.size(); ++d) {
+    const int32_t m = (int32_t)lv[d].tok.size();
+    SRT_CUDA(cudaMemcpyAsync(d_par, lv[d].par.data(), m * 4, cudaMemcpyHostToDevice, stream), "load");
+    SRT_CUDA(cudaMemcpyAsync(d_tok, lv[d].tok.data(), m * 4, cudaMemcpyHostToDevice, stream), "load");
+    SRT_CUDA(cudaMemcpyAsync(d_cnt, lv[d].cnt.data(), m * 8, cudaMemcpyHostToDevice, stream), "load");
+    SRT_CUDA(launch_load_level(c->dev, ids[cur], d_par, d_tok, d_cnt, m, ids[cur ^ 1], stream),
+             "load level");
+    SRT_CUDA(cudaStreamSynchronize(stream), "load");  // the host arrays are reused
+    cur ^= 1;
+  }
+  SRT_CUDA(cudaStreamSynchronize(stream), "load");
+  return SRT_OK;
+}
+
 srt_status srt_cache_clear_errors(srt_cache* c, void* stream_) {
   if (!c) return SRT_ERR_INVALID_ARG;
   cudaStream_t stream = (cudaStream_t)stream_;

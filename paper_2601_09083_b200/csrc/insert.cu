@@ -243,6 +243,26 @@ __device__ uint32_t place_child(const DevCache& c, uint32_t u, uint32_t k, uint3
   const uint32_t i = blk_index(k);
   const uint32_t off = k - blk_start(i);
   uint32_t base;
+  if (off == 0 && i < 4) {  // (a block pruning left behind is reused)
+    const uint32_t old = ld_relaxed_u32(rec_bases(c, u) + i);
+    if (old != 0) {
+      if (old - 1 >= BAD) return BAD;
+      c.slots[old - 1] = ch;
+      c.stok[old - 1] = tk;
+      return old - 1;
+    }
+  }
+  if (off == 0 && i >= 4) {
+    const uint32_t hb = hash_slot(c, block_key(u, i));
+    if (hb != NONE) {  // left behind by pruning: reuse
+      uint32_t v;
+      while ((v = ld_relaxed_u32(&c.hash[hb].val)) == NONE) __nanosleep(32);
+      if (v >= BAD) return BAD;
+      c.slots[v] = ch;
+      c.stok[v] = tk;
+      return v;
+    }
+  }
   if (off == 0) {  // this thread creates block i
     const uint32_t sz = blk_size(i);
     const unsigned long long b = atomicAdd(&c.ctr[1], (unsigned long long)sz);
@@ -257,6 +277,15 @@ __device__ uint32_t place_child(const DevCache& c, uint32_t u, uint32_t k, uint3
       if (h < 0) {
         set_error(c, SRT_DEV_CAPACITY);
         return BAD;  // waiters poll the status word
+      }
+      if (!created) {  // a block pruning left behind: reuse it (this block is not needed)
+        uint32_t v;
+        while ((v = ld_relaxed_u32(&c.hash[h].val)) == NONE) __nanosleep(32);
+        base = v;
+        if (base >= BAD) return BAD;
+        c.slots[base] = ch;
+        c.stok[base] = tk;
+        return base;
       }
       publish_slot(c.hash + h, base, NONE);
     }
@@ -749,7 +778,45 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   }
 }
 
+// One dump record per thread (srt_cache_load): the child of its parent (the
+// previous level's node par_idx) labelled tok is created if missing and its
+// count, mirror count and the parent's csum grow by the record's count.
+__global__ void __launch_bounds__(256)
+k_load_level(DevCache c, const uint32_t* __restrict__ parent_ids, const int32_t* __restrict__ par_idx,
+             const int32_t* __restrict__ tok, const unsigned long long* __restrict__ cnt, int32_t n,
+             uint32_t* __restrict__ out_ids) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned created = 0;
+  if (i < n) {
+    const uint32_t u = parent_ids[par_idx[i]];
+    const int32_t tk = tok[i];
+    uint32_t id = BAD;
+    if (tk < 0 || tk >= c.V) {
+      set_error(c, SRT_DEV_OOV);
+    } else if (u < BAD) {
+      uint32_t pos;
+      id = get_or_create(c, u, tk, &pos, created);
+      if (id < BAD) {
+        const uint32_t k = (uint32_t)cnt[i];
+        atomicAdd(&c.cnt[id], k);
+        if (is_slot_word(pos)) atomicAdd(&c.scnt[pos], k);
+        atomicAdd(&rec_of(c, u)->w, k);
+      }
+    }
+    out_ids[i] = id;
+  }
+  count_created(c, created);
+}
+
 }  // namespace
+
+cudaError_t launch_load_level(const DevCache& c, const uint32_t* parent_ids, const int32_t* par_idx,
+                              const int32_t* tok, const unsigned long long* cnt, int32_t n,
+                              uint32_t* out_ids, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  k_load_level<<<(n + 255) / 256, 256, 0, stream>>>(c, parent_ids, par_idx, tok, cnt, n, out_ids);
+  return cudaGetLastError();
+}
 
 cudaError_t set_insert_profile(long long* buf) {
   return cudaMemcpyToSymbol(g_ins_prof, &buf, sizeof(buf));

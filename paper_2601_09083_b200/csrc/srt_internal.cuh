@@ -37,6 +37,9 @@ constexpr uint32_t NONE = 0xFFFFFFFFu;  // "no block" / "value pending"
 constexpr uint32_t BAD = 0xFFFFFFFEu;   // creation failed (capacity): walk stops
 constexpr uint32_t AUX_CHILD0 = 0xFFFFFFFDu;  // edge aux: the child is its parent's inline child 0
 constexpr unsigned long long EMPTY_KEY = ~0ull;
+// a removed edge or block key (srt_cache_prune): matches no key and is not
+// EMPTY, so probe sequences through it stay intact; its slot is not reused
+constexpr unsigned long long TOMB_KEY = ~0ull - 1;
 constexpr uint32_t BLOCK_TAG = 0x80000000u;  // tokens are < 2^31
 
 // Edge entries: aux = the child's slot word in its parent's child blocks
@@ -309,6 +312,17 @@ cudaError_t launch_pack_spans(int32_t n, int32_t B, const int32_t* n_commit,
 cudaError_t launch_apply_spans(int32_t n, int32_t B, const int32_t* rec, const int32_t* src,
                                int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* from,
                                int32_t* to, cudaStream_t stream);
+cudaError_t launch_prune_level(const DevCache& c, const uint32_t* front, int32_t nf, uint32_t theta,
+                               uint32_t* next_keep, unsigned* n_keep, uint32_t* next_dead,
+                               unsigned* n_dead, cudaStream_t stream);
+cudaError_t launch_kill_level(const DevCache& c, const uint32_t* dead, int32_t nd,
+                              uint32_t* next_dead, unsigned* n_dead, unsigned long long* removed,
+                              cudaStream_t stream);
+cudaError_t launch_count_hist(const DevCache& c, unsigned long long* hist, int32_t nb,
+                              cudaStream_t stream);
+cudaError_t launch_load_level(const DevCache& c, const uint32_t* parent_ids, const int32_t* par_idx,
+                              const int32_t* tok, const unsigned long long* cnt, int32_t n,
+                              uint32_t* out_ids, cudaStream_t stream);
 cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
                               uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,
                               uint32_t* out_cnt, uint32_t* out_nchild, unsigned int* out_n,

@@ -236,6 +236,36 @@ class SrtCache:
         return [(buf[i].token, int(buf[i].count), buf[i].n_children) for i in range(n.value)]
 
 
+    # ---- capacity management and persistence (include/srt.h; O17) --
+    def prune(self, prompt_id: int, theta: int) -> int:
+        """Remove every non-root node of T_p (all prompts if -1) with count < theta
+        (blocking); returns the number removed.  Invalidates the insert cursors."""
+        r = ctypes.c_int64(0)
+        check(self.L.srt_cache_prune(self._h, prompt_id, theta, ctypes.byref(r), _stream()),
+              "srt_cache_prune")
+        return r.value
+
+    def reset(self, prompt_id: int) -> int:
+        """Empty T_p (blocking)."""
+        return self.prune(prompt_id, 0xFFFFFFFF)
+
+    def evict(self, max_nodes: int):
+        """Prune every tree to <= 0.9 * max_nodes nodes if more than max_nodes are
+        live (blocking); returns (removed, theta)."""
+        r, th = ctypes.c_int64(0), ctypes.c_uint32(0)
+        check(self.L.srt_cache_evict(self._h, max_nodes, ctypes.byref(r), ctypes.byref(th),
+                                     _stream()), "srt_cache_evict")
+        return r.value, th.value
+
+    def load(self, prompt_id: int, records) -> None:
+        """Merge canonical dump records [(token, count, n_children), ...] into T_p."""
+        n = len(records)
+        buf = (SrtDumpRecord * max(1, n))()
+        for i, (t, cnt, nch) in enumerate(records):
+            buf[i].token, buf[i].count, buf[i].n_children = int(t), int(cnt), int(nch)
+        check(self.L.srt_cache_load(self._h, prompt_id, buf, n, _stream()), "srt_cache_load")
+
+
 # ---- multi-GPU exchange records (include/srt.h; DESIGN.md §8) ----------------
 def draft_record_words(Bmax: int) -> int:
     return 2 + 5 * Bmax
