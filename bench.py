@@ -238,6 +238,7 @@ class Group:
         if bits:
             raise RuntimeError(f"cache error bits {bits} after warm-up inserts ({st})")
         self.tree_stats = st
+        self.path_rounds = None  # srt_verify_path rounds (bench --verify path)
         # ---- run-ahead spans (DAPO): a fixed schedule, uploaded once
         self.ra = None
         if wl.w.runahead and cfg.get("runahead"):
@@ -301,7 +302,8 @@ class Group:
     def verify_insert(self, seed: int, logits=None):
         c = self.cache
         c.verify(self.logits if logits is None else logits, self.d, self.seq_id, seed, self.seq_tok,
-                 self.seq_len, self.max_new, out=self.v, rows=self.rows_max)
+                 self.seq_len, self.max_new, out=self.v, rows=self.rows_max,
+                 path_rounds=self.path_rounds)
         c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len, cursor=self.cursor)
         if self.ra is not None:
             self.runahead_insert()
@@ -696,6 +698,10 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="N=1: run the multi-GPU exchange path (owner draft, draft return, span "
                          "all-gather) on one rank")
+    ap.add_argument("--verify", default="full", choices=["full", "path"],
+                    help="full = srt_verify (every draft row sampled, the headline); path = "
+                         "srt_verify_path (only the accepted path's rows, SURVEY f3b)")
+    ap.add_argument("--path-rounds", type=int, default=3)
     ap.add_argument("--groups", type=int, default=1,
                     help="prompt groups pipelined on separate streams (1 = sequential; >1 measured slower: the latency-bound tree kernels stall behind the scan's HBM traffic)")
     args = ap.parse_args()
@@ -753,6 +759,9 @@ def main():
     else:
         wl = Workload(cfg, args.seed, rank, world)
         run = GpuRun(wl, args.dtype, args.profile, args.seed + rank, groups=args.groups)
+        if args.verify == "path":
+            for gr in run.groups:
+                gr.path_rounds = args.path_rounds
         G = run.G
     pipelined = G > 1
     K, W = args.steps, args.warmup
@@ -773,6 +782,7 @@ def main():
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rows_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
+    smp_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     acc_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     com_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     logs = [torch.zeros(3, K, dtype=torch.int64, device=run.dev) for _ in range(G)]
@@ -805,6 +815,10 @@ def main():
                 run.step(seed, evs[k])
                 # bookkeeping outside the event-bracketed segments
                 rows_log[k] = run.d.row_offsets[-1]
+                if args.verify == "path":  # rows srt_verify_path actually sampled
+                    nr = run.d.row_offsets[-1]
+                    smp_log[k] = ((run.v.sampled[:run.rows_max] >= 0)
+                                  & (torch.arange(run.rows_max, device=run.dev) < nr)).sum()
                 acc_log[k] = run.v.accept_len.sum()
                 com_log[k] = run.v.n_commit.sum()
         torch.cuda.synchronize()
@@ -838,7 +852,10 @@ def main():
         return
     esz = 2 if args.dtype == "bf16" else 4
     scan_ms = per_kernel.get("scan", [])
-    scan_bytes = float(rows.sum()) * cfg["V"] * esz
+    path_mode = args.verify == "path" and wl is not None
+    smp = smp_log.cpu().numpy() if path_mode else None
+    # bytes the scan reads: every drafted row (srt_verify) or the sampled ones (srt_verify_path)
+    scan_bytes = float((smp if path_mode else rows).sum()) * cfg["V"] * esz
     peak, peak_kind = load_peaks()
     achieved = scan_bytes / (sum(scan_ms) / 1000.0) / 1e9 if scan_ms else None
     traffic = traffic_ratio = None
@@ -876,7 +893,11 @@ def main():
         "committed_tokens_per_s": world * com / (max_ms / 1000.0),
         "mean_accepted_per_seq_step": acc / (K * cfg["active"]),
         "mean_rows_per_step": float(rows.mean()),
-        "roofline": {"bound": "hbm", "kernel": "scan (k_scan_rows + k_rowinfo)",
+        **({"verify": f"path-only (srt_verify_path, {args.path_rounds} rounds + subtree tail)",
+            "mean_rows_sampled_per_step": float(smp.mean())} if path_mode else {}),
+        "roofline": {"bound": "hbm", "kernel": ("path verify (all rounds of k_scan_rows + "
+                                                "k_path_*)" if path_mode else
+                                                "scan (k_scan_rows + k_rowinfo)"),
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_over_algorithmic": traffic_ratio,

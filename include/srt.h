@@ -275,6 +275,29 @@ SRT_API srt_status srt_verify(srt_cache* cache, int32_t n, const void* logits,
 #define SRT_DRAFT_RECORD_WORDS(Bmax) (2 + 5 * (Bmax))
 #define SRT_SPAN_RECORD_WORDS(Bmax) ((Bmax) + 2)
 
+/*
+ * srt_verify_path — srt_verify that samples only the rows the commit needs
+ * (SURVEY §8(f3b)).  The walk goes level by level: path_rounds rounds each
+ * scan one row per sequence still accepting (its current node: the root,
+ * then each accepted node), then every sequence still accepting has its
+ * current node's whole draft subtree scanned at once and the walk finishes.
+ * Same arguments and the same outputs as srt_verify -- commits, accept_len,
+ * n_commit, commit_tok, accepted_nodes, finished, the sequence table, and
+ * sampled[] for every row on the accepted path and the stopping row (the
+ * same Gumbel-max draws, O11) -- except sampled[r] = -1 for rows not
+ * sampled.  path_rounds = 0 samples every row (= srt_verify).  Requires
+ * 16-byte-aligned rows (SRT_ERR_INVALID_ARG otherwise).  No host sync.
+ */
+SRT_API srt_status srt_verify_path(srt_cache* cache, int32_t n, int32_t path_rounds,
+                                   const void* logits, const int64_t* row_offsets,
+                                   const int32_t* draft_len, const int32_t* draft_tok,
+                                   const int32_t* draft_parent, const int32_t* draft_depth,
+                                   const uint64_t* seq_id, uint64_t seed, float temperature,
+                                   int32_t eos_id, const int32_t* max_new, int32_t* seq_tok,
+                                   int64_t stride, int32_t* seq_len, int32_t* sampled,
+                                   int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+                                   int32_t* accepted_nodes, uint8_t* finished, void* stream);
+
 /* records[s] <- the draft of sequence s < n (srt_draft's outputs). */
 SRT_API srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
                            const int32_t* draft_len, const int32_t* draft_tok,

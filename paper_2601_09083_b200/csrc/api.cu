@@ -21,6 +21,8 @@ struct srt_cache {
   int2* rowinfo = nullptr;      // verify: per-row (sequence, position)
   unsigned long long* result = nullptr;  // verify: per-row packed winner (pack_cand)
   int64_t row_cap = 0;          // rows the two buffers above can hold
+  void* path = nullptr;         // srt_verify_path: row lists and walk state
+  size_t path_cap = 0;
   int device;
   uint32_t tag;  // identifies this cache in insert cursors (never 0)
   // per-kernel timing (srt_profile_enable)
@@ -158,6 +160,7 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   if (c->scratch) cudaFreeAsync(c->scratch, (cudaStream_t)stream);
   if (c->rowinfo) cudaFreeAsync(c->rowinfo, (cudaStream_t)stream);
   if (c->result) cudaFreeAsync(c->result, (cudaStream_t)stream);
+  if (c->path) cudaFreeAsync(c->path, (cudaStream_t)stream);
   delete c;
   return SRT_OK;
 }
@@ -291,6 +294,57 @@ srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t
   SRT_CUDA(timed(c, SRT_K_SCAN, stream,
                  [&] { return launch_scan(c->dev, a, false, c->rowinfo, c->result, stream); }),
            "verify scan");
+  SRT_CUDA(timed(c, SRT_K_ACCEPT, stream,
+                 [&] { return launch_accept(c->dev, a, c->result, stream); }),
+           "verify accept");
+  return SRT_OK;
+}
+
+srt_status srt_verify_path(srt_cache* c, int32_t n, int32_t path_rounds, const void* logits,
+                           const int64_t* row_offsets, const int32_t* draft_len,
+                           const int32_t* draft_tok, const int32_t* draft_parent,
+                           const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed,
+                           float temperature, int32_t eos_id, const int32_t* max_new,
+                           int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* sampled,
+                           int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+                           int32_t* accepted_nodes, uint8_t* finished, void* stream_) {
+  if (!c || n < 0 || stride < 0 || path_rounds < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!logits || !row_offsets || !draft_len || !draft_tok || !draft_parent || !draft_depth ||
+      !seq_id || !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit ||
+      !commit_tok || !accepted_nodes || !finished)
+    return SRT_ERR_INVALID_ARG;
+  if (!scan_cluster_size(c->cfg.vocab_size, (int)c->cfg.logits_dtype) ||
+      ((uintptr_t)logits % 16) != 0)
+    return SRT_ERR_INVALID_ARG;  // (the rows kernel's TMA needs 16-byte rows)
+  VerifyArgs a{n,       logits,     (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
+               draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
+               seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
+               accepted_nodes, finished};
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t rows_max = (int64_t)n * (c->cfg.budget_max + 1);
+  if (c->row_cap < rows_max) {
+    if (c->rowinfo) SRT_CUDA(cudaFreeAsync(c->rowinfo, stream), "cudaFreeAsync(rowinfo)");
+    if (c->result) SRT_CUDA(cudaFreeAsync(c->result, stream), "cudaFreeAsync(result)");
+    const int64_t cap = std::max<int64_t>(rows_max, 4096);
+    SRT_CUDA(cudaMallocAsync(&c->rowinfo, cap * sizeof(int2), stream), "cudaMallocAsync(rowinfo)");
+    SRT_CUDA(cudaMallocAsync(&c->result, cap * sizeof(unsigned long long), stream),
+             "cudaMallocAsync(result)");
+    c->row_cap = cap;
+  }
+  const size_t need = path_scratch_bytes(n, c->cfg.budget_max);
+  if (c->path_cap < need) {
+    if (c->path) SRT_CUDA(cudaFreeAsync(c->path, stream), "cudaFreeAsync(path)");
+    SRT_CUDA(cudaMallocAsync(&c->path, need, stream), "cudaMallocAsync(path)");
+    c->path_cap = need;
+  }
+  SRT_CUDA(timed(c, SRT_K_SCAN, stream,
+                 [&] {
+                   return launch_path_verify(c->dev, a, c->rowinfo, c->result, c->path,
+                                             path_rounds, stream);
+                 }),
+           "verify path");
   SRT_CUDA(timed(c, SRT_K_ACCEPT, stream,
                  [&] { return launch_accept(c->dev, a, c->result, stream); }),
            "verify accept");

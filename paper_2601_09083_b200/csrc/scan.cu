@@ -162,6 +162,7 @@ __device__ __forceinline__ float block_max_scalar(const unsigned char* blk, int 
 struct ScanParams {
   const void* logits;
   const int2* rowinfo;         // per row: (seq, pos)
+  const int32_t* row_list;     // nullable: scan rows row_list[0 .. total) instead of [0, total)
   const int64_t* total;        // -> row_offsets[n]
   const uint64_t* seq_id;
   uint64_t seed;
@@ -233,7 +234,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
       uint64_t pol = 0;
       if (a.l2_hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       uint64_t kc = 0;
-      for (int64_t row = blockIdx.x; row < total; row += gridDim.x) {
+      for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+        const int64_t row = a.row_list ? a.row_list[i] : i;
         const char* base = (const char*)a.logits + row * row_bytes;
         for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
           const int s = (int)(kc % NST);
@@ -257,7 +259,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     const int grp = (wid - 1) / GW, w = (wid - 1) % GW;
     uint64_t kc = 0;
     int64_t u = 0;
-    for (int64_t row = blockIdx.x; row < total; row += gridDim.x, ++u) {
+    for (int64_t i = blockIdx.x; i < total; i += gridDim.x, ++u) {
+      const int64_t row = a.row_list ? a.row_list[i] : i;
       const int sb = (int)(u % NS);
       const uint32_t suse = (uint32_t)(u / NS);
       if (suse > 0) mbar_wait(&sum_free[sb], (suse - 1) & 1);
@@ -340,7 +343,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   // ======================= tail: M, then the surviving blocks ==============
   const int t = wid - 1 - NSW;
   int64_t u = 0;
-  for (int64_t row = blockIdx.x; row < total; row += gridDim.x, ++u) {
+  for (int64_t i = blockIdx.x; i < total; i += gridDim.x, ++u) {
+    const int64_t row = a.row_list ? a.row_list[i] : i;
     const int sb = (int)(u % NS);
     mbar_wait(&sum_ready[sb], (uint32_t)((u / NS) & 1));
     const unsigned long long hdr = rowhdr[sb];
@@ -547,10 +551,21 @@ cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* ro
   k_rowinfo<<<(a.n + 127) / 128, 128, 0, stream>>>(a, c.Bmax, rowinfo, result);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  return launch_scan_list(c, a, rowinfo, nullptr, a.row_offsets + a.n, result, stream);
+}
+
+// The rows kernel over rows row_list[0 .. *count) (or [0, *count) when
+// row_list is null), rowinfo and result indexed by row id; result[row] must
+// be 0 for every listed row.
+cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2* rowinfo,
+                             const int32_t* row_list, const int64_t* count,
+                             unsigned long long* result, cudaStream_t stream) {
+  if (!scan_cluster_size(c.V, a.dtype)) return cudaErrorInvalidValue;
   ScanParams p;
   p.logits = a.logits;
   p.rowinfo = rowinfo;
-  p.total = a.row_offsets + a.n;
+  p.row_list = row_list;
+  p.total = count;
   p.seq_id = a.seq_id;
   p.seed = a.seed;
   p.temperature = a.temperature;

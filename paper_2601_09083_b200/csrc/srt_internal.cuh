@@ -299,6 +299,14 @@ cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference, 
                         unsigned long long* result, cudaStream_t stream);
 cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, const unsigned long long* result,
                           cudaStream_t stream);
+cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2* rowinfo,
+                             const int32_t* row_list, const int64_t* count,
+                             unsigned long long* result, cudaStream_t stream);
+// path-only verification (srt_verify_path): scratch = 2 row lists + per-seq state
+cudaError_t launch_path_verify(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
+                               unsigned long long* result, void* scratch, int rounds,
+                               cudaStream_t stream);
+size_t path_scratch_bytes(int32_t n, int32_t Bmax);
 cudaError_t launch_pack_drafts(int32_t n, int32_t B, const int32_t* match_len,
                                const int32_t* draft_len, const int32_t* draft_tok,
                                const int32_t* draft_parent, const int32_t* draft_depth,

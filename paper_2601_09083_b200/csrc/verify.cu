@@ -136,7 +136,10 @@ k_accept(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result
   const int32_t B = c.Bmax;
   const int32_t ns = a.draft_len[s];
   const int64_t r0 = a.row_offsets[s];
-  for (int32_t i = lane; i <= ns; i += 32) a.sampled[r0 + i] = unpack_index(result[r0 + i]);
+  for (int32_t i = lane; i <= ns; i += 32) {  // (~0: a row srt_verify_path did not sample)
+    const unsigned long long rr = result[r0 + i];
+    a.sampled[r0 + i] = rr == ~0ull ? -1 : unpack_index(rr);
+  }
   __syncwarp();
   const int32_t t = a.seq_len[s];
   const int64_t db = (int64_t)s * B;

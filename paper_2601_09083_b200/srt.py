@@ -164,8 +164,9 @@ class SrtCache:
 
     def verify(self, logits, d: DraftOut, seq_id, seed: int, seq_tok, seq_len, max_new,
                temperature: float = 1.0, eos_id: int = -1, out: VerifyOut | None = None,
-               rows: int | None = None) -> VerifyOut:
-        """Mutates seq_tok / seq_len (appends the committed tokens)."""
+               rows: int | None = None, path_rounds: int | None = None) -> VerifyOut:
+        """Mutates seq_tok / seq_len (appends the committed tokens).  path_rounds
+        = R selects srt_verify_path (only the accepted path's rows sampled)."""
         n = seq_len.shape[0]
         if logits.dtype != self.logits_dtype:
             raise SrtError(f"logits dtype {logits.dtype} != cache's {self.logits_dtype}")
@@ -175,7 +176,10 @@ class SrtCache:
             out = VerifyOut.empty(n, logits.shape[0] if rows is None else rows, self.Bmax,
                                   seq_tok.device)
         i32 = torch.int32
-        check(self.L.srt_verify(self._h, n, _ptr(logits, None, "logits"),
+        fn, head = self.L.srt_verify, (self._h, n)
+        if path_rounds is not None:
+            fn, head = self.L.srt_verify_path, (self._h, n, int(path_rounds))
+        check(fn(*head, _ptr(logits, None, "logits"),
                                 _ptr(d.row_offsets, torch.int64), _ptr(d.draft_len, i32),
                                 _ptr(d.draft_tok, i32), _ptr(d.draft_parent, i32),
                                 _ptr(d.draft_depth, i32), _ptr(seq_id, torch.int64, "seq_id"),
