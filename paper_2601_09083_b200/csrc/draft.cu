@@ -374,7 +374,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   }
 }
 
-constexpr int SCAN_THREADS = 256;  // small: co-resides with a running verify scan
+constexpr int SCAN_THREADS = 1024;  // one pass for the usual n <= 1024
 
 // row_offsets[s] = sum_{s' < s} (draft_len[s'] + 1)  (logits rows: root + nodes)
 __global__ void __launch_bounds__(SCAN_THREADS)

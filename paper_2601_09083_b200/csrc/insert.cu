@@ -19,7 +19,7 @@ namespace srt {
 
 namespace {
 
-constexpr int PLAN_THREADS = 256;  // small: co-resides with a running verify scan
+constexpr int PLAN_THREADS = 1024;  // one pass for the usual n <= 1024
 
 __device__ __forceinline__ int32_t span_lo(int32_t from, int32_t floor_, int32_t D) {
   int32_t lo = from - D + 1;

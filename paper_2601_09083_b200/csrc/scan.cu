@@ -496,18 +496,18 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
 }
 
 // per row: (sequence, position) — rows of sequence s are [row_offsets[s],
-// row_offsets[s+1]); also clears the row's packed result.
+// row_offsets[s+1]); also clears the row's packed result.  One warp per
+// sequence, a lane per row.
 __global__ void k_rowinfo(VerifyArgs a, int32_t Bmax, int2* rowinfo,
                           unsigned long long* result) {
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (s >= a.n) return;
   const int64_t r0 = a.row_offsets[s];
   const int32_t t = a.seq_len[s];
   const int32_t nd = (int32_t)(a.row_offsets[s + 1] - r0 - 1);
-  rowinfo[r0] = make_int2(s, t);
-  result[r0] = 0;
-  for (int32_t i = 0; i < nd; ++i) {
-    rowinfo[r0 + 1 + i] = make_int2(s, t + a.draft_depth[(int64_t)s * Bmax + i]);
+  for (int32_t i = lane - 1; i < nd; i += 32) {
+    rowinfo[r0 + 1 + i] = make_int2(s, i < 0 ? t : t + a.draft_depth[(int64_t)s * Bmax + i]);
     result[r0 + 1 + i] = 0;
   }
 }
@@ -548,7 +548,7 @@ int scan_cluster_size(int32_t V, int dtype) {
 cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
                                 unsigned long long* result, cudaStream_t stream) {
   if (!scan_cluster_size(c.V, a.dtype)) return cudaErrorInvalidValue;
-  k_rowinfo<<<(a.n + 127) / 128, 128, 0, stream>>>(a, c.Bmax, rowinfo, result);
+  k_rowinfo<<<(a.n * 32 + 255) / 256, 256, 0, stream>>>(a, c.Bmax, rowinfo, result);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_scan_list(c, a, rowinfo, nullptr, a.row_offsets + a.n, result, stream);
