@@ -702,6 +702,10 @@ def main():
                     help="full = srt_verify (every draft row sampled, the headline); path = "
                          "srt_verify_path (only the accepted path's rows, SURVEY f3b)")
     ap.add_argument("--path-rounds", type=int, default=3)
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: each step's draft segment and verify+insert segment replay as CUDA "
+                         "graphs (no launch gaps); the per-kernel breakdown then comes from a "
+                         "separate profiled eager pass")
     ap.add_argument("--groups", type=int, default=1,
                     help="prompt groups pipelined on separate streams (1 = sequential; >1 measured slower: the latency-bound tree kernels stall behind the scan's HBM traffic)")
     args = ap.parse_args()
@@ -786,8 +790,24 @@ def main():
     acc_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     com_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     logs = [torch.zeros(3, K, dtype=torch.int64, device=run.dev) for _ in range(G)]
-    for gr in run.groups:
-        gr.cache.profile_enable(K * KERNELS_PER_STEP)
+    use_graph = (args.graph and not pipelined and wl is not None and G == 1
+                 and run.groups[0].ra is None)
+    if use_graph:
+        # capture one step's two segments (the stand-in stays eager between them)
+        gr0 = run.groups[0]
+        g_draft, g_vi = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_draft):
+            gr0.draft()
+        with torch.cuda.graph(g_vi):
+            gr0.verify_insert(seed)
+        for _ in range(2):  # graph warm-up steps
+            g_draft.replay()
+            gr0.standin()
+            g_vi.replay()
+        torch.cuda.synchronize()
+    else:
+        for gr in run.groups:
+            gr.cache.profile_enable(K * KERNELS_PER_STEP)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -812,7 +832,17 @@ def main():
             ev_b.record()
         else:
             for k in range(K):
-                run.step(seed, evs[k])
+                if use_graph:
+                    e = evs[k]
+                    e[0].record()
+                    g_draft.replay()
+                    e[1].record()
+                    gr0.standin()
+                    e[2].record()
+                    g_vi.replay()
+                    e[3].record()
+                else:
+                    run.step(seed, evs[k])
                 # bookkeeping outside the event-bracketed segments
                 rows_log[k] = run.d.row_offsets[-1]
                 if args.verify == "path":  # rows srt_verify_path actually sampled
@@ -830,6 +860,14 @@ def main():
         rows_log, acc_log, com_log = tot_log[0], tot_log[1], tot_log[2]
     else:
         my_ms = float(sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in evs))
+    KP = K
+    if use_graph:  # per-kernel breakdown: a profiled eager pass after the timed region
+        KP = min(K, 20)
+        for gr in run.groups:
+            gr.cache.profile_enable(KP * KERNELS_PER_STEP)
+        for _ in range(KP):
+            run.step(seed)
+        torch.cuda.synchronize()
     prof = [x for gr in run.groups for x in gr.cache.profile_read()]
     bits, st = run.status()
     if bits:
@@ -857,7 +895,8 @@ def main():
     # bytes the scan reads: every drafted row (srt_verify) or the sampled ones (srt_verify_path)
     scan_bytes = float((smp if path_mode else rows).sum()) * cfg["V"] * esz
     peak, peak_kind = load_peaks()
-    achieved = scan_bytes / (sum(scan_ms) / 1000.0) / 1e9 if scan_ms else None
+    # per launch: the timed steps' mean bytes over the profiled launches' mean time
+    achieved = (scan_bytes / K) / (float(np.mean(scan_ms)) / 1000.0) / 1e9 if scan_ms else None
     traffic = traffic_ratio = None
     tf = os.path.join(ROOT, "profiles", f"scan_traffic_{args.config}_{args.dtype}.json")
     if os.path.exists(tf):
@@ -885,8 +924,12 @@ def main():
                    "timed": (f"whole step loop on the device (CUDA events, {G} prompt groups "
                              f"pipelined on {G} streams); forward stand-in and bookkeeping "
                              f"INCLUDED" if pipelined else
-                             "draft + verify + insert device time (CUDA events); forward "
-                             "stand-in excluded"),
+                             ("draft + verify + insert device time (CUDA events around the two "
+                              "CUDA-graph replays per step; per-kernel breakdown from a profiled "
+                              "eager pass of the same steps); forward stand-in excluded"
+                              if use_graph else
+                              "draft + verify + insert device time (CUDA events); forward "
+                              "stand-in excluded")),
                    "seed": "one run seed for every step (the Philox counter carries the "
                            "position, so every (sequence, position) draws fresh noise)"},
         "accepted_tokens_per_s": world * acc / (max_ms / 1000.0),
@@ -905,15 +948,15 @@ def main():
                                        "(profiles/scan_traffic_*.json; its launch's rows differ "
                                        "from this run's mean)",
                      "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": scan_bytes / max(1, len(scan_ms)),
+                     "algorithmic_bytes_per_launch": scan_bytes / K,
                      "frac_of_8TBps_spec": (achieved / 8000.0) if achieved else None},
         "kernels": kern,
         "tree_stage_us_per_batch": {k: kern[k]["mean_us"] for k in
                                     ("draft", "row_offsets", "insert_plan", "insert_walk",
                                      "insert_cursor", "accept")
                                     if k in kern},
-        "gpu_launches": len(prof),
-        "launches_per_step": len(prof) / K,
+        "gpu_launches": int(round(len(prof) / KP * K)),
+        "launches_per_step": len(prof) / KP,
         "tree_nodes": st["nodes_used"],
     }
     cs = clk.summary()
