@@ -42,3 +42,39 @@ def test_pipelined_groups_match_sequential():
     assert np.array_equal(l1, l3)
     assert np.array_equal(t1, t3)
     assert (l1 > wl.t0).all()  # every sequence advanced
+
+
+def test_graph_replay_matches_eager():
+    """bench.py's CUDA-graph step (draft segment + verify/insert segment
+    captured once, replayed) commits exactly what the eager step commits."""
+    import torch
+    import bench
+    cfg = dict(bench.CONFIGS["grpo"])
+    cfg.update(prompts=6, active=48, V=5000, cap=1024, act_cap=1024, median=300,
+               node_capacity=1 << 20)
+    seed = bench.step_seed(1, 0)
+    out = []
+    for graph in (False, True):
+        wl = bench.Workload(cfg, 1)
+        run = bench.GpuRun(wl, "bf16", "rl-mix", 1)
+        gr = run.groups[0]
+        run.step(seed)  # warm (allocations happen outside any capture)
+        if graph:
+            g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1):
+                gr.draft()
+            with torch.cuda.graph(g2):
+                gr.verify_insert(seed)
+            for _ in range(6):
+                g1.replay()
+                gr.standin()
+                g2.replay()
+        else:
+            for _ in range(6):
+                run.step(seed)
+        torch.cuda.synchronize()
+        assert run.status()[0] == 0
+        out.append((gr.seq_tok.cpu().numpy(), gr.seq_len.cpu().numpy(), gr.cache.dump(0)))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
