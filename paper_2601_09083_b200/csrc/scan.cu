@@ -359,13 +359,15 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
       const float X = key_value((uint32_t)(hdr >> 32));
       const uint32_t bX = 0xFFFFFFFFu - (uint32_t)hdr;
       // i* = the first element of block bX equal to X; M = z(i*), exactly
+      // (tail warp 0 only: the others pick their phase-1 block meanwhile)
+      float M = -INFINITY;
+      if (t == 0) {
       const int nX = block_len(a.V, bX);
       const int64_t vX = (int64_t)bX * NOISE_BLK;
       uint32_t first = 0xFFFFFFFFu;
       if (2 * lane < nX && load_x<DT>(rowp, vX + 2 * lane) == X) first = 2 * lane;
       else if (2 * lane + 1 < nX && load_x<DT>(rowp, vX + 2 * lane + 1) == X) first = 2 * lane + 1;
       const uint32_t jstar = __reduce_min_sync(0xffffffffu, first);
-      float M;
       {
         uint32_t wa, wb;
         block_words(bX, pos, s_lo, s_hi, k0, k1, wa, wb);
@@ -378,6 +380,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
           g = element_noise_from_word(k == 0 ? pw.x : k == 1 ? pw.y : k == 2 ? pw.z : pw.w, bn);
         }
         M = perturbed(X, g, T, unit_t);
+      }
       }
       // Exact evaluation of block b by the whole warp (lane = 2 consecutive
       // tokens, coalesced); the best (z, v) and M are raised as it goes.
@@ -436,19 +439,21 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         for (int32_t cb = t; cb < nchunk; cb += NT) {
           const int32_t b = cb * 32 + lane;
           if (b < a.nblk) {
-            const float ub = U[b];
-            if (ub >= M) {
-              const uint32_t k = fkey(ub);
-              if (k > bu) { bu = k; bi = b; }
-            }
+            const uint32_t k = fkey(U[b]);
+            if (k > bu) { bu = k; bi = b; }
           }
         }
         const uint32_t wbu = __reduce_max_sync(0xffffffffu, bu);
         const int32_t wbi = __reduce_min_sync(0xffffffffu, (wbu && bu == wbu) ? bi : INT_MAX);
+        float2 xx1 = make_float2(NAN, NAN);
         if (wbu) {
           b1 = wbi;
-          eval_block(b1, load_block(b1));
+          xx1 = load_block(b1);  // in flight across the barrier
         }
+        share_M();  // z(i*) from warp 0
+        asm volatile("bar.sync 1, %0;" ::"r"(NT * 32) : "memory");
+        share_M();
+        if (b1 >= 0 && U[b1] >= M) eval_block(b1, xx1);
       }
       share_M();
       asm volatile("bar.sync 1, %0;" ::"r"(NT * 32) : "memory");
