@@ -46,6 +46,12 @@ CONFIGS = {
     # BJ:configs[3]
     "ppo": dict(V=152064, prompts=256, samples=1, active=256, Bmax=64, D=128, L=16, median=1200,
                 cap=4096, act_cap=4096, prior_epochs=3, node_capacity=1 << 28),
+    # BJ:configs[4] per rank: 8 ranks x 256 prompts x 16 samples = 2048 x 16, 4096
+    # sequences decoded per rank, trees hash-sharded, span all-gather + draft
+    # return every step (run with torchrun --nproc-per-node 8, or --sharded at N=1)
+    "b200x8": dict(V=151936, prompts=256, samples=16, active=4096, Bmax=32, D=32, L=8,
+                   median=1200, cap=8192, act_cap=8192, prior_epochs=1, node_capacity=1 << 29,
+                   slot_capacity=1 << 29),
     # BJ:configs[2] (1024 of the 8192 sequences concurrently).  D = 16: the warm
     # cache (8192 prior rollouts, 57M tokens) has > 1.07B distinct windows at
     # D = 32 (measured: node capacity 2^30 overflowed during the warm-up); at
