@@ -2,7 +2,7 @@
 # list, ncu --set full captures of the scan and of the tree kernels.
 # Usage: bash tools/profile_round.sh <tag>
 set -x
-T=${1:-v5}
+T=${1:-v6}
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_$T.log 2>&1
 BENCH_ROWS_LOG=1 python bench.py --no-cpu-baseline --e2e-steps 0 --steps 2 --warmup 4 > gpurun_out/rows_$T.log 2>&1
