@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(CURSOR_WARPS * 32)
 k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
                 const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
                 const int32_t* __restrict__ to, const int32_t* __restrict__ floor_, int32_t short_max,
-                uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats, int skip) {
+                uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
   extern __shared__ __align__(16) unsigned char cur_smem[];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
@@ -690,15 +690,15 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       if (g >= ngroups) break;  // (warp-uniform)
       const bool a = act[g];
       const uint32_t h = hnew[g];
-      if (a && !(skip & 1)) {
+      if (a) {
         atomicAdd(&c.cnt[h], 1u);
         atomicAdd(&rec_of(c, par[g])->w, 1u);
         ++incs;
         if (cre[g]) c.tok[h] = tk;
         else if (is_slot_word(aux[g])) atomicAdd(&c.scnt[aux[g]], 1u);
       }
-      const unsigned mc = (skip & 2) ? 0u : __ballot_sync(0xffffffffu, a && cre[g]);
-      const unsigned mp = (skip & 2) ? 0u : __ballot_sync(0xffffffffu, a && !cre[g] && aux[g] == NONE);
+      const unsigned mc = __ballot_sync(0xffffffffu, a && cre[g]);
+      const unsigned mp = __ballot_sync(0xffffffffu, a && !cre[g] && aux[g] == NONE);
       if (mc | mp) {
         int bc = 0, bp = 0;
         if (lane == 0) {
@@ -856,10 +856,8 @@ cudaError_t launch_insert_cursor(const DevCache& c, int32_t n, const int32_t* pr
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  static int skip = -1;  // development knob (tools/insert_probe.py): skip parts of the work
-  if (skip < 0) skip = getenv("SRT_INS_SKIP") ? atoi(getenv("SRT_INS_SKIP")) : 0;
   kern<<<(n + CURSOR_WARPS - 1) / CURSOR_WARPS, CURSOR_WARPS * 32, smem, stream>>>(
-      c, n, prompt_id, seq_tok, stride, from, to, floor_, short_max, cursor, tag, stats, skip);
+      c, n, prompt_id, seq_tok, stride, from, to, floor_, short_max, cursor, tag, stats);
   return cudaGetLastError();
 }
 
