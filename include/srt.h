@@ -413,7 +413,8 @@ typedef enum {
   SRT_K_ROW_OFFSETS = 3,
   SRT_K_SCAN = 4,
   SRT_K_ACCEPT = 5,
-  SRT_K_INSERT_CURSOR = 6
+  SRT_K_INSERT_CURSOR = 6,
+  SRT_K_HUB_REFRESH = 7  /* the hub child lists an insert call rebuilds */
 } srt_kernel_id;
 
 typedef struct {

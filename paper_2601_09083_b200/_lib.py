@@ -27,7 +27,8 @@ EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache
            "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile", "srt_debug_insert_profile",
            "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
-                5: "accept", 6: "insert_cursor"}
+                5: "accept", 6: "insert_cursor",
+                7: "hub_refresh"}
 
 
 class SrtConfig(ctypes.Structure):

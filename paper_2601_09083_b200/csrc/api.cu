@@ -23,6 +23,7 @@ struct srt_cache {
   int64_t row_cap = 0;          // rows the two buffers above can hold
   void* path = nullptr;         // srt_verify_path: row lists and walk state
   size_t path_cap = 0;
+  uint32_t* hubwork = nullptr;  // hub refresh work list [DIRTY_CAP + 1]
   int device;
   uint32_t tag;  // identifies this cache in insert cursors (never 0)
   // per-kernel timing (srt_profile_enable)
@@ -109,6 +110,11 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
   const size_t o_status = off;  off = align_up(off + 4);
   const size_t o_gb = off;      off = align_up(off + (2 * NOISE_BUCKETS + 1) * 4);
+  // hub child lists: ~1 slot per 16 nodes' worth of hash, at least 2^12
+  size_t HC = 4096;
+  while (HC < H / 512 && HC < (1u << 18)) HC <<= 1;
+  const size_t o_hub = off;     off = align_up(off + HC * (4 * 4 + 8 + (size_t)HUB_K * 12));
+  const size_t o_dirty = off;   off = align_up(off + ((size_t)DIRTY_CAP + 2) * 4);
   srt_cache* c = new srt_cache();
   c->cfg = *cfg;
   cudaGetDevice(&c->device);
@@ -141,6 +147,20 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.ctr = (unsigned long long*)(b + o_ctr);
   d.status = (uint32_t*)(b + o_status);
   d.gbound = (float*)(b + o_gb);
+  d.HC = (uint32_t)HC;
+  {
+    char* hb = b + o_hub;
+    d.hub_claim = (unsigned long long*)hb;  hb += HC * 8;
+    d.hub_node = (uint32_t*)hb;             hb += HC * 4;
+    d.hub_nch = (uint32_t*)hb;              hb += HC * 4;
+    d.hub_csum = (uint32_t*)hb;             hb += HC * 4;
+    d.hub_len = (uint32_t*)hb;              hb += HC * 4;
+    d.hub_child = (uint32_t*)hb;            hb += HC * HUB_K * 4;
+    d.hub_tok = (int32_t*)hb;               hb += HC * HUB_K * 4;
+    d.hub_cnt = (uint32_t*)hb;
+  }
+  d.dirty = (uint32_t*)(b + o_dirty);
+  d.dirty_n = d.dirty + DIRTY_CAP;
   c->scratch = nullptr;
   c->scratch_cap = 0;
   if ((e = launch_init_cache(d, stream)) != cudaSuccess ||
@@ -161,6 +181,7 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   if (c->rowinfo) cudaFreeAsync(c->rowinfo, (cudaStream_t)stream);
   if (c->result) cudaFreeAsync(c->result, (cudaStream_t)stream);
   if (c->path) cudaFreeAsync(c->path, (cudaStream_t)stream);
+  if (c->hubwork) cudaFreeAsync(c->hubwork, (cudaStream_t)stream);
   delete c;
   return SRT_OK;
 }
@@ -176,6 +197,10 @@ srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const 
     SRT_CUDA(cudaMallocAsync(&c->scratch, cap * sizeof(long long), stream), "cudaMallocAsync(scratch)");
     c->scratch_cap = cap;
   }
+  if (!c->hubwork)
+    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
+             "cudaMallocAsync(hub work)");
+  SRT_CUDA(cudaMemsetAsync(c->dev.dirty_n, 0, 4, stream), "insert");
   // cursor path: spans of <= D new positions; longer ones (run-ahead) walk
   const int32_t short_max = cursor ? c->cfg.max_depth : -1;
   SRT_CUDA(timed(c, SRT_K_INSERT_PLAN, stream,
@@ -198,6 +223,12 @@ srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const 
                                                  stream);
                    }),
              "insert cursor");
+  SRT_CUDA(timed(c, SRT_K_HUB_REFRESH, stream,
+                 [&] {
+                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + DIRTY_CAP,
+                                             stream);
+                 }),
+           "hub refresh");
   return SRT_OK;
 }
 }  // namespace
@@ -455,6 +486,7 @@ srt_status srt_cache_prune(srt_cache* c, int32_t p, uint32_t theta, int64_t* rem
   SRT_CUDA(cudaMemcpyAsync(c->dev.ctr, &h_ctr, 8, cudaMemcpyHostToDevice, stream), "prune");
   SRT_CUDA(cudaStreamSynchronize(stream), "prune");
   c->tag = next_tag(c->tag);  // cursors may name removed nodes: invalidate all
+  SRT_CUDA(cudaMemsetAsync(c->dev.hub_node, 0xFF, (size_t)c->dev.HC * 4, stream), "prune");
   if (removed_out) *removed_out = (int64_t)h_removed;
   return SRT_OK;
 }
@@ -533,6 +565,7 @@ srt_status srt_cache_load(srt_cache* c, int32_t p, const srt_dump_record* recs, 
     SRT_CUDA(cudaStreamSynchronize(stream), "load");  // the host arrays are reused
     cur ^= 1;
   }
+  SRT_CUDA(cudaMemsetAsync(c->dev.hub_node, 0xFF, (size_t)c->dev.HC * 4, stream), "load");
   SRT_CUDA(cudaStreamSynchronize(stream), "load");
   return SRT_OK;
 }

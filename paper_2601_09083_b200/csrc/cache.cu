@@ -34,6 +34,9 @@ cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
   if ((e = cudaMemsetAsync(c.slots, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.stok, 0xFF, c.W * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(c.scnt, 0, c.W * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.hub_node, 0xFF, (size_t)c.HC * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.hub_claim, 0, (size_t)c.HC * 8, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.dirty_n, 0, 8, stream)) != cudaSuccess) return e;
   k_init_counters<<<1, 1, 0, stream>>>(c);
   return cudaGetLastError();
 }

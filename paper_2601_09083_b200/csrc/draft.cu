@@ -162,6 +162,40 @@ __device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, doub
   pf.pops += 1ll << 20;
   const double dsum = (double)r.w;  // exact (< 2^32)
   const unsigned long long meta0 = make_meta(depth_u + 1, 0, parent_idx);
+  if (nch > HUB_MIN && dsum > 0.0 && score_u > 1e-250) {
+    // (a normal, nonzero score_u keeps the sibling score strictly increasing
+    // in the count, so the list's order is the O8 order)
+    // a hub: its top children by (count desc, token asc) are listed while its
+    // child count and csum are unchanged (hub.cu); siblings rank by exactly
+    // that order (O6, O8), so the first cap of them are all that can enter
+    const uint32_t slot = hub_slot(c, u);
+    const bool ok = c.hub_node[slot] == u && c.hub_nch[slot] == nch && c.hub_csum[slot] == r.w;
+    if (ok) {
+      const uint32_t len = min(c.hub_len[slot], (uint32_t)cap);
+      const size_t e = (size_t)slot * HUB_K;
+      for (uint32_t kb = 0; kb < len; kb += 32) {
+        const uint32_t k = kb + lane;
+        Ent cd{-1.0, META_NONE, NONE};
+        if (k < len) {
+          cd.node = c.hub_child[e + k];
+          cd.score = child_score(score_u, dsum, c.hub_cnt[e + k]);
+          cd.meta = meta0 | ((unsigned long long)(uint32_t)c.hub_tok[e + k] << 7);
+        }
+        bool stop = false;
+        for (int src = 0; src < 32 && kb + src < len; ++src) {  // in order: stop at the first loser
+          const Ent b = ent_shfl(cd, src);
+          const Ent bar = F.size == cap ? F.at(cap - 1) : Ent{-1.0, META_NONE, NONE};
+          if (!better(b, bar)) {
+            stop = true;
+            break;
+          }
+          F.insert(b, cap, lane);
+        }
+        if (stop) break;
+      }
+      return;
+    }
+  }
   // block bases of blocks 0..nb-1 (children 1..nch-1), one lane each
   const uint32_t nb = blk_index(nch - 2) + 1;
   t0 = clock64();

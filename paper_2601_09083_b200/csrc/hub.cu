@@ -1,0 +1,235 @@
+// hub.cu — the hub child lists: for every node with more than
+// HUB_MIN children that an insert touched, its top HUB_K children by (count
+// desc, token asc), so that srt_draft expands a hub in O(cap) instead of
+// ranking thousands of children at every pop.  Siblings rank by count (score
+// is strictly monotone in it, O6) with ties by token (O8), so the first cap
+// entries of the list are exactly the children that can enter a frontier of
+// cap entries.  A list is used only while its node's child count and csum are
+// unchanged (counts only grow), so it is never stale.
+//
+// After every insert call: the inserts logged the shallow parents whose csum
+// they changed (the dirty list); k_hub_claim / k_hub_pick elect one refresher
+// per cache slot (a node listed several times, or two hubs sharing a slot,
+// refresh once), and k_hub_refresh rebuilds each elected list with one CTA:
+// every warp keeps a sorted top-HUB_K of its share of the children, warp 0
+// merges them.
+#include "srt_internal.cuh"
+
+namespace srt {
+
+namespace {
+
+constexpr int REFRESH_WARPS = 8;
+
+__device__ __forceinline__ unsigned long long child_key(uint32_t cnt, int32_t tok) {
+  return ((unsigned long long)cnt << 32) | (0xFFFFFFFFu - (uint32_t)tok);  // larger = better
+}
+
+// A sorted (descending) warp list of up to 64 keys: lane i holds entries i and i + 32.
+struct KeyList {
+  unsigned long long k0, k1;
+  uint32_t v0, v1;
+  int size;
+  __device__ __forceinline__ unsigned long long key_at(int j) const {
+    return j < 32 ? __shfl_sync(0xffffffffu, k0, j) : __shfl_sync(0xffffffffu, k1, j - 32);
+  }
+  __device__ __forceinline__ void insert(unsigned long long k, uint32_t v, int lane, int K) {
+    const int pos = __popc(__ballot_sync(0xffffffffu, lane < size && k0 > k)) +
+                    __popc(__ballot_sync(0xffffffffu, lane + 32 < size && k1 > k));
+    if (pos >= K) return;
+    const unsigned long long uk0 = __shfl_up_sync(0xffffffffu, k0, 1);
+    const uint32_t uv0 = __shfl_up_sync(0xffffffffu, v0, 1);
+    const unsigned long long uk1 = __shfl_up_sync(0xffffffffu, k1, 1);
+    const uint32_t uv1 = __shfl_up_sync(0xffffffffu, v1, 1);
+    const unsigned long long lk = __shfl_sync(0xffffffffu, k0, 31);
+    const uint32_t lv = __shfl_sync(0xffffffffu, v0, 31);
+    if (lane + 32 >= pos) {
+      if (lane + 32 == pos) { k1 = k; v1 = v; }
+      else if (lane == 0) { k1 = lk; v1 = lv; }
+      else { k1 = uk1; v1 = uv1; }
+    }
+    if (lane >= pos) {
+      if (lane == pos) { k0 = k; v0 = v; }
+      else { k0 = uk0; v0 = uv0; }
+    }
+    size = min(size + 1, K);
+  }
+  // offer 32 candidates (one per lane): the ones that beat the current last entry enter
+  __device__ __forceinline__ void offer(bool valid, unsigned long long k, uint32_t v, int lane,
+                                       int K) {
+    const unsigned long long bar = size == K ? key_at(K - 1) : 0ull;
+    unsigned pending = __ballot_sync(0xffffffffu, valid && (size < K || k > bar));
+    while (pending) {
+      const int src = __ffs(pending) - 1;
+      pending &= pending - 1;
+      const unsigned long long kk = __shfl_sync(0xffffffffu, k, src);
+      const uint32_t vv = __shfl_sync(0xffffffffu, v, src);
+      if (size == K && kk <= key_at(K - 1)) continue;
+      insert(kk, vv, lane, K);
+    }
+  }
+};
+
+// Each dirty hub bids for its cache slot: the largest (call, node) wins.
+__global__ void k_hub_claim(DevCache c) {
+  const uint32_t call = c.dirty_n[1] + 1;  // this refresh's generation
+  const uint32_t n = min(*c.dirty_n, DIRTY_CAP);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t u = c.dirty[i];
+    if (u >= c.H) continue;  // roots are never expanded
+    if (rec_of(c, u)->x <= HUB_MIN) continue;
+    atomicMax(&c.hub_claim[hub_slot(c, u)], ((unsigned long long)call << 32) | u);
+  }
+}
+
+// The winner of each slot (once, however often it was listed) joins the work list.
+__global__ void k_hub_pick(DevCache c, uint32_t* work, uint32_t* work_n) {
+  const uint32_t call = c.dirty_n[1] + 1;
+  const uint32_t n = min(*c.dirty_n, DIRTY_CAP);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t u = c.dirty[i];
+    if (u >= c.H) continue;
+    const uint4 r = *rec_of(c, u);
+    if (r.x <= HUB_MIN) continue;
+    const uint32_t slot = hub_slot(c, u);
+    const unsigned long long key = ((unsigned long long)call << 32) | u;
+    if (atomicCAS(&c.hub_claim[slot], key, key | 0x80000000ull) != key) continue;
+    // (a list that is still valid needs no rebuild)
+    if (c.hub_node[slot] == u && c.hub_nch[slot] == r.x && c.hub_csum[slot] == r.w) continue;
+    work[atomicAdd(work_n, 1u)] = u;
+  }
+}
+
+__global__ void __launch_bounds__(REFRESH_WARPS * 32)
+k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* work_n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.dirty_n[1] += 1;  // next refresh's generation
+  __shared__ unsigned long long sk[REFRESH_WARPS][HUB_K];
+  __shared__ uint32_t sv[REFRESH_WARPS][HUB_K];
+  __shared__ int sn[REFRESH_WARPS];
+  __shared__ uint32_t sthr[REFRESH_WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int K = min(HUB_K, c.Bmax);  // the draft never needs more than Bmax of them
+  const uint32_t nw = *work_n;
+  for (uint32_t it = blockIdx.x; it < nw; it += gridDim.x) {
+    const uint32_t u = work[it];
+    const uint4 r = *rec_of(c, u);
+    const uint32_t nch = r.x;
+    const uint32_t nb = blk_index(nch - 2) + 1;
+    const uint32_t mybase = lane < (int)nb ? block_base(c, u, lane) : 0u;
+    auto load = [&](uint32_t k, uint32_t& id, int32_t& tk, uint32_t& cn) {
+      const uint32_t jj = k >= 1 ? k - 1 : 0;
+      const uint32_t bi = blk_index(jj);
+      const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
+      id = NONE;
+      cn = 0;
+      tk = 0;
+      if (k == 0) {
+        id = r.y;
+        tk = (int32_t)r.z;
+        cn = c.cnt[id];
+      } else if (k < nch) {
+        const uint32_t pos = base + (jj - blk_start(bi));
+        id = c.slots[pos];
+        tk = c.stok[pos];
+        cn = c.scnt[pos];
+      }
+    };
+    // pass 1: every lane keeps the two largest counts of its children; a warp's
+    // K-th largest of those 64 has >= K children at or above it, so children
+    // below the largest such threshold over the warps can never be in the list
+    uint32_t t1 = 0, t2 = 0;
+    constexpr int U4 = 4;  // slices in flight per warp
+    constexpr uint32_t STEP = REFRESH_WARPS * 32;
+    for (uint32_t kb = (uint32_t)w * 32; kb < nch; kb += U4 * STEP) {
+      uint32_t cv[U4];
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * STEP + lane;
+        uint32_t id;
+        int32_t tk;
+        load(k, id, tk, cv[q]);
+        if (k >= nch) cv[q] = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t cn = cv[q];
+        if (cn > t1) { t2 = t1; t1 = cn; }
+        else if (cn > t2) t2 = cn;
+      }
+    }
+    uint32_t thr = 0;
+    for (int i = 0; i < K; ++i) {
+      thr = __reduce_max_sync(0xffffffffu, t1);
+      const unsigned who = __ballot_sync(0xffffffffu, t1 == thr);
+      if (lane == __ffs(who) - 1) { t1 = t2; t2 = 0; }
+    }
+    if (lane == 0) sthr[w] = thr;
+    __syncthreads();
+    thr = 0;
+    for (int o = 0; o < REFRESH_WARPS; ++o) thr = max(thr, sthr[o]);
+    // pass 2: rank only the children at or above the threshold
+    KeyList L{0ull, 0ull, NONE, NONE, 0};
+    for (uint32_t kb = (uint32_t)w * 32; kb < nch; kb += U4 * STEP) {
+      uint32_t idv[U4], cv[U4];
+      int32_t tkv[U4];
+#pragma unroll
+      for (int q = 0; q < U4; ++q) load(kb + q * STEP + lane, idv[q], tkv[q], cv[q]);
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * STEP + lane;
+        if (__any_sync(0xffffffffu, k < nch && cv[q] >= thr))
+          L.offer(k < nch && cv[q] >= thr, child_key(cv[q], tkv[q]), idv[q], lane, K);
+      }
+    }
+    sk[w][lane] = L.k0;
+    sv[w][lane] = L.v0;
+    sk[w][lane + 32] = L.k1;
+    sv[w][lane + 32] = L.v1;
+    if (lane == 0) sn[w] = L.size;
+    __syncthreads();
+    if (w == 0) {
+      for (int o = 1; o < REFRESH_WARPS; ++o)  // merge the sorted lists (stop at the first loser)
+        for (int i = 0; i < sn[o]; ++i) {
+          const unsigned long long kk = sk[o][i];
+          if (L.size == K && kk <= L.key_at(K - 1)) break;
+          L.insert(kk, sv[o][i], lane, K);
+        }
+      const uint32_t slot = hub_slot(c, u);
+      const size_t e = (size_t)slot * HUB_K;
+      const int len = L.size;
+      if (lane < len) {
+        c.hub_child[e + lane] = L.v0;
+        c.hub_tok[e + lane] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k0);
+        c.hub_cnt[e + lane] = (uint32_t)(L.k0 >> 32);
+      }
+      if (lane + 32 < len) {
+        c.hub_child[e + lane + 32] = L.v1;
+        c.hub_tok[e + lane + 32] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k1);
+        c.hub_cnt[e + lane + 32] = (uint32_t)(L.k1 >> 32);
+      }
+      if (lane == 0) {
+        c.hub_len[slot] = (uint32_t)len;
+        c.hub_nch[slot] = nch;
+        c.hub_csum[slot] = r.w;
+        c.hub_node[slot] = u;  // (read by later kernels only)
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_hub_refresh(const DevCache& c, uint32_t call, uint32_t* work, uint32_t* work_n,
+                               cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(work_n, 0, 4, stream);
+  if (e != cudaSuccess) return e;
+  const int g = num_sms() * 4;
+  (void)call;
+  k_hub_claim<<<g, 256, 0, stream>>>(c);
+  k_hub_pick<<<g, 256, 0, stream>>>(c, work, work_n);
+  k_hub_refresh<<<num_sms() * 8, REFRESH_WARPS * 32, 0, stream>>>(c, work, work_n);
+  return cudaGetLastError();
+}
+
+}  // namespace srt

@@ -371,6 +371,10 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         if (is_slot_word(pos)) atomicAdd(&c.scnt[pos], 1u);
         atomicAdd(&rec_of(c, u)->w, 1u);
         ++incs;
+        if (j - i >= 1 && j - i <= HUB_DIRTY_DEPTH) {  // a shallow parent's csum changed
+          const uint32_t e = atomicAdd(c.dirty_n, 1u);
+          if (e < DIRTY_CAP) c.dirty[e] = u;
+        }
       }
       u = ch;
     }
@@ -696,6 +700,10 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         ++incs;
         if (cre[g]) c.tok[h] = tk;
         else if (is_slot_word(aux[g])) atomicAdd(&c.scnt[aux[g]], 1u);
+      }
+      if (g == 0) {  // shallow parents whose csum changed: their hub lists are rebuilt after the call
+        const int32_t l = lane + 1;
+        log_dirty(c, a && l >= 2 && l <= 1 + HUB_DIRTY_DEPTH, par[g]);
       }
       const unsigned mc = __ballot_sync(0xffffffffu, a && cre[g]);
       const unsigned mp = __ballot_sync(0xffffffffu, a && !cre[g] && aux[g] == NONE);

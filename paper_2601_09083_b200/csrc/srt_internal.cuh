@@ -72,7 +72,29 @@ struct DevCache {
   unsigned long long* ctr;  // [0] nodes created (+ P roots), [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
   float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima
+  // Hub child lists: for a node with more than HUB_MIN
+  // children, its top HUB_K children by (count desc, token asc), valid while
+  // the node's child count and csum are what they were when the list was
+  // built (counts only grow: an unchanged csum means unchanged counts).
+  // Direct-mapped by mix64(node) & (HC - 1); rebuilt after every insert for
+  // the hubs the insert touched (the dirty list).
+  uint32_t HC;
+  uint32_t* hub_node;   // [HC] NONE = empty
+  uint32_t* hub_nch;    // [HC]
+  uint32_t* hub_csum;   // [HC]
+  uint32_t* hub_len;    // [HC]
+  uint32_t* hub_child;  // [HC][HUB_K] child ids, best first
+  int32_t* hub_tok;     // [HC][HUB_K]
+  uint32_t* hub_cnt;    // [HC][HUB_K]
+  unsigned long long* hub_claim;  // [HC] (insert call << 32 | node) of the last refresh claim
+  uint32_t* dirty;      // [DIRTY_CAP] parents whose csum an insert changed (shallow ones)
+  uint32_t* dirty_n;    // [0] entries, [1] refresh generation (a device counter: graph-safe)
 };
+
+constexpr uint32_t HUB_MIN = 256;  // more children than one draft round
+constexpr int HUB_K = 64;          // >= Bmax
+constexpr uint32_t DIRTY_CAP = 1u << 20;
+constexpr int HUB_DIRTY_DEPTH = 2;  // parents at depth 1..2 are logged as dirty
 
 // Candidate (z, v) packed so that a larger u64 is the better candidate under
 // "larger z, then smaller v" (first maximum): order-preserving float key in the
@@ -331,6 +353,22 @@ cudaError_t launch_count_hist(const DevCache& c, unsigned long long* hist, int32
 cudaError_t launch_load_level(const DevCache& c, const uint32_t* parent_ids, const int32_t* par_idx,
                               const int32_t* tok, const unsigned long long* cnt, int32_t n,
                               uint32_t* out_ids, cudaStream_t stream);
+cudaError_t launch_hub_refresh(const DevCache& c, uint32_t call, uint32_t* work, uint32_t* work_n,
+                               cudaStream_t stream);
+__device__ __forceinline__ uint32_t hub_slot(const DevCache& c, uint32_t u) {
+  return (uint32_t)(mix64(0x4855420000000000ull ^ u) & (c.HC - 1));
+}
+// Log a parent whose csum just changed (warp-collective: every lane calls it).
+__device__ __forceinline__ void log_dirty(const DevCache& c, bool want, uint32_t u) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(c.dirty_n, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  const uint32_t e = base + __popc(m & lanemask_lt());
+  if (want && e < DIRTY_CAP) c.dirty[e] = u;
+}
 cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
                               uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,
                               uint32_t* out_cnt, uint32_t* out_nchild, unsigned int* out_n,
