@@ -8,11 +8,11 @@
 // unchanged (counts only grow), so it is never stale.
 //
 // After every insert call: the inserts logged the shallow parents whose csum
-// they changed (the dirty list); k_hub_claim / k_hub_pick elect one refresher
-// per cache slot (a node listed several times, or two hubs sharing a slot,
-// refresh once), and k_hub_refresh rebuilds each elected list with one CTA:
-// every warp keeps a sorted top-HUB_K of its share of the children, warp 0
-// merges them.
+// they changed (the dirty list); k_hub_pick elects one refresher per cache
+// slot (a node listed several times, or two hubs sharing a slot, refresh
+// once), and k_hub_refresh rebuilds each elected list with one CTA: a count
+// threshold first (lane-wise top-2 counts), then every warp keeps a sorted
+// top-K of its share of the children at or above it, warp 0 merges them.
 #include "srt_internal.cuh"
 
 namespace srt {
@@ -70,32 +70,24 @@ struct KeyList {
   }
 };
 
-// Each dirty hub bids for its cache slot: the largest (call, node) wins.
-__global__ void k_hub_claim(DevCache c) {
+// Each dirty hub whose list is stale claims its cache slot for this refresh
+// generation with one CAS: the first claim of a slot wins (a node listed
+// several times refreshes once; of two hubs sharing a slot one refreshes, the
+// other keeps the full scan until a later refresh) and joins the work list.
+__global__ void k_hub_pick(DevCache c, uint32_t* work, uint32_t* work_n) {
   const uint32_t call = c.dirty_n[1] + 1;  // this refresh's generation
   const uint32_t n = min(*c.dirty_n, DIRTY_CAP);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t u = c.dirty[i];
     if (u >= c.H) continue;  // roots are never expanded
-    if (rec_of(c, u)->x <= HUB_MIN) continue;
-    atomicMax(&c.hub_claim[hub_slot(c, u)], ((unsigned long long)call << 32) | u);
-  }
-}
-
-// The winner of each slot (once, however often it was listed) joins the work list.
-__global__ void k_hub_pick(DevCache c, uint32_t* work, uint32_t* work_n) {
-  const uint32_t call = c.dirty_n[1] + 1;
-  const uint32_t n = min(*c.dirty_n, DIRTY_CAP);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t u = c.dirty[i];
-    if (u >= c.H) continue;
     const uint4 r = *rec_of(c, u);
     if (r.x <= HUB_MIN) continue;
     const uint32_t slot = hub_slot(c, u);
-    const unsigned long long key = ((unsigned long long)call << 32) | u;
-    if (atomicCAS(&c.hub_claim[slot], key, key | 0x80000000ull) != key) continue;
     // (a list that is still valid needs no rebuild)
     if (c.hub_node[slot] == u && c.hub_nch[slot] == r.x && c.hub_csum[slot] == r.w) continue;
+    const unsigned long long c0 = c.hub_claim[slot];
+    if ((uint32_t)(c0 >> 32) == call) continue;  // claimed in this generation already
+    if (atomicCAS(&c.hub_claim[slot], c0, ((unsigned long long)call << 32) | u) != c0) continue;
     work[atomicAdd(work_n, 1u)] = u;
   }
 }
@@ -226,7 +218,6 @@ cudaError_t launch_hub_refresh(const DevCache& c, uint32_t call, uint32_t* work,
   if (e != cudaSuccess) return e;
   const int g = num_sms() * 4;
   (void)call;
-  k_hub_claim<<<g, 256, 0, stream>>>(c);
   k_hub_pick<<<g, 256, 0, stream>>>(c, work, work_n);
   k_hub_refresh<<<num_sms() * 8, REFRESH_WARPS * 32, 0, stream>>>(c, work, work_n);
   return cudaGetLastError();
