@@ -737,7 +737,7 @@ def main():
                   f"value scaled by {n_s}/{cfg['active']}")
         print(json.dumps({
             "impl": "reference", "metric": metric, "value": value, "unit": "steps/s",
-            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload, "profile": args.profile},
