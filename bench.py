@@ -251,7 +251,8 @@ class Group:
             if G != 1:
                 raise ValueError("run-ahead spans need --groups 1")
             self.ra = runahead_schedule(wl.w.runahead, cfg["runahead"], cfg["cap"], seed, dev)
-            self.ra_k = 0
+            self.ra_k = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.ra_cur = torch.zeros(2, self.ra["frm"].shape[1], dtype=torch.int32, device=dev)
         # ---- this group's rows of the logits buffer: rows_max + 1 dummy row
         self.rows_max = n * (B + 1)
         self.logits = logits[row0:row0 + self.rows_max + 1]
@@ -317,15 +318,19 @@ class Group:
     def runahead_inserted(self):
         """Host view: tokens of each look-ahead rollout inserted so far."""
         ra = self.ra
-        k = min(self.ra_k, ra["frm"].shape[0]) - 1
+        k = min(int(self.ra_k.item()), ra["frm"].shape[0]) - 1
         return ra["to_host"][k] if k >= 0 else np.zeros(len(ra["prompt_host"]), np.int32)
 
     def runahead_insert(self):
         """This step's run-ahead spans: [frm, to) of each look-ahead rollout
-        (empty for the rollouts not scheduled this step), walk insertion."""
+        (empty for the rollouts not scheduled this step), walk insertion.  The
+        step index lives on the device, so the step can be a CUDA graph."""
+        torch = self.torch
         ra = self.ra
-        k = min(self.ra_k, ra["frm"].shape[0] - 1)  # past the schedule: empty spans
-        self.cache.insert(ra["prompt"], ra["tok"], ra["frm"][k], ra["to"][k])
+        k = torch.clamp(self.ra_k, max=ra["frm"].shape[0] - 1)  # past the schedule: empty spans
+        torch.index_select(ra["frm"], 0, k, out=self.ra_cur[0:1])
+        torch.index_select(ra["to"], 0, k, out=self.ra_cur[1:2])
+        self.cache.insert(ra["prompt"], ra["tok"], self.ra_cur[0], self.ra_cur[1])
         self.ra_k += 1
 
 
@@ -796,8 +801,7 @@ def main():
     acc_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     com_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     logs = [torch.zeros(3, K, dtype=torch.int64, device=run.dev) for _ in range(G)]
-    use_graph = (args.graph and not pipelined and wl is not None and G == 1
-                 and run.groups[0].ra is None)
+    use_graph = args.graph and not pipelined and wl is not None and G == 1
     if use_graph:
         # capture one step's two segments (the stand-in stays eager between them)
         gr0 = run.groups[0]
