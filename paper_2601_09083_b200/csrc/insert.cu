@@ -324,6 +324,110 @@ __device__ __forceinline__ uint32_t get_or_create(const DevCache& c, uint32_t u,
   return id;
 }
 
+// Resolve the edge keys key[g] of the lanes' active probes (creating the
+// missing edges): hnew = the child's id (its slot), cre = this lane created
+// it, aux = its slot word as read (NONE if unknown or pending).  A lane whose
+// table is full ends with act = false and hnew = BAD.  Warp-collective.
+template <int NG>
+__device__ __forceinline__ int probe_edges(const DevCache& c, const unsigned long long (&key)[NG],
+                                           bool (&act)[NG], uint32_t (&hnew)[NG],
+                                           bool (&cre)[NG], uint32_t (&aux)[NG]) {
+  const int lane = threadIdx.x & 31;
+  (void)lane;
+  const unsigned long long mask = c.H - 1;
+  int rounds = 0;
+  // Probe every depth's edge as a warp-convergent state machine: in each
+  // round every unresolved probe issues its next memory operation (a slot
+  // pair load and/or a CAS) before any result is used, so a position costs
+  // max-over-lanes probe rounds instead of the sum of divergent paths.
+  // Round 0 claims the home slot with a CAS while loading the home pair.
+  // Each load reads 4 consecutive slots (two 32-byte loads) so that an
+  // occupied home almost never costs more than one extra round (the CAS at
+  // the first EMPTY slot seen).
+  SlotPair qa[NG], qb[NG];
+  unsigned long long ps[NG], cs[NG], rk[NG];
+  int op[NG];  // bit 0: load slots ps .. ps+3, bit 1: CAS at cs; 0 = resolved
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    cre[g] = false;
+    hnew[g] = NONE;
+    aux[g] = NONE;
+    op[g] = 0;
+    if (!act[g]) continue;
+    ps[g] = cs[g] = home_slot(c, key[g]);
+    op[g] = 3;
+  }
+  for (int round = 0;; ++round) {
+    bool live = false;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) live |= op[g] != 0;
+    if (!__any_sync(0xffffffffu, live)) break;
+    ++rounds;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {  // issue
+      if (op[g] & 1) {
+        qa[g] = ld_pair(c.hash + ps[g]);
+        qb[g] = ld_pair(c.hash + ((ps[g] + 2) & mask));
+      }
+      if (op[g] & 2) rk[g] = atomicCAS(&c.hash[cs[g]].key, EMPTY_KEY, key[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {  // resolve (registers only)
+      if (!op[g]) continue;
+      int from = 0;  // index among the 4 loaded slots to scan from
+      if (op[g] & 2) {
+        const int ci = (int)((cs[g] - ps[g]) & mask);  // 0..3: the CAS slot
+        if (rk[g] == EMPTY_KEY) {
+          op[g] = 0;
+          cre[g] = true;
+          hnew[g] = (uint32_t)cs[g];
+          continue;
+        }
+        if (rk[g] == key[g]) {
+          op[g] = 0;
+          hnew[g] = (uint32_t)cs[g];
+          const SlotPair& qq = ci < 2 ? qa[g] : qb[g];
+          const unsigned long long kk = (ci & 1) ? qq.k1 : qq.k0;
+          aux[g] = kk == key[g] ? ((ci & 1) ? qq.a1 : qq.a0) : NONE;
+          continue;
+        }
+        from = ci + 1;  // slot cs holds another key
+      }
+      int next = 0;  // -1: found, 2: CAS slot ps + i, 0: load the next 4 slots
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < from || next) continue;
+        const SlotPair& qq = i < 2 ? qa[g] : qb[g];
+        const unsigned long long kk = (i & 1) ? qq.k1 : qq.k0;
+        if (kk == key[g]) {
+          hnew[g] = (uint32_t)((ps[g] + i) & mask);
+          aux[g] = (i & 1) ? qq.a1 : qq.a0;
+          next = -1;
+        } else if (kk == EMPTY_KEY) {
+          cs[g] = (ps[g] + i) & mask;
+          next = 2;
+        }
+      }
+      if (next == -1) {
+        op[g] = 0;
+      } else if (next == 2) {
+        op[g] = 2;
+      } else {
+        ps[g] = (ps[g] + 4) & mask;
+        cs[g] = ps[g];
+        op[g] = 1;
+      }
+      if (round > 1 << 20) {  // never: the table would be full
+        op[g] = 0;
+        act[g] = false;
+        hnew[g] = BAD;
+        set_error(c, SRT_DEV_CAPACITY);
+      }
+    }
+  }
+  return rounds;
+}
+
 // Nodes created by this warp join the node count; more than N is a capacity
 // error (the count, unlike ids, is deterministic).
 __device__ __forceinline__ void count_created(const DevCache& c, unsigned created) {
@@ -332,66 +436,6 @@ __device__ __forceinline__ void count_created(const DevCache& c, unsigned create
   if ((threadIdx.x & 31) == 0 && d) {
     const unsigned long long before = atomicAdd(&c.ctr[0], d);
     if (before + d > c.N) set_error(c, SRT_DEV_CAPACITY);
-  }
-}
-
-__global__ void __launch_bounds__(256)
-k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
-              const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
-              const int32_t* __restrict__ to, const int32_t* __restrict__ floor_,
-              const long long* __restrict__ offs, srt_insert_stats* stats) {
-  const long long total = offs[n];
-  unsigned windows = 0, incs = 0, created = 0;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    // span s: offs[s] <= idx < offs[s+1]
-    int32_t lo_s = 0, hi_s = n - 1;
-    while (lo_s < hi_s) {
-      const int32_t mid = (lo_s + hi_s + 1) >> 1;
-      if (offs[mid] <= idx) lo_s = mid; else hi_s = mid - 1;
-    }
-    const int32_t s = lo_s;
-    const int32_t f = from[s], t_end = to[s];
-    const int32_t i = span_lo(f, floor_ ? floor_[s] : 0, c.D) + (int32_t)(idx - offs[s]);
-    const int32_t* toks = seq_tok + (int64_t)s * stride;
-    uint32_t u = root_id(c, prompt_id[s]);
-    const int32_t end = min(i + c.D, t_end);
-    ++windows;
-    for (int32_t j = i; j < end; ++j) {
-      const int32_t tk = toks[j];
-      if (tk < 0 || tk >= c.V) {
-        set_error(c, SRT_DEV_OOV);
-        break;
-      }
-      uint32_t pos;
-      const uint32_t ch = get_or_create(c, u, tk, &pos, created);
-      if (ch >= BAD) break;
-      if (j >= f) {  // a window ends at a new position: count it (and its parent's csum)
-        atomicAdd(&c.cnt[ch], 1u);
-        if (is_slot_word(pos)) atomicAdd(&c.scnt[pos], 1u);
-        atomicAdd(&rec_of(c, u)->w, 1u);
-        ++incs;
-        if (j - i >= 1 && j - i <= HUB_DIRTY_DEPTH) {  // a shallow parent's csum changed
-          const uint32_t e = atomicAdd(c.dirty_n, 1u);
-          if (e < DIRTY_CAP) c.dirty[e] = u;
-        }
-      }
-      u = ch;
-    }
-  }
-  count_created(c, created);
-  if (stats) {
-    unsigned long long a = windows, b = incs, d = created;
-    for (int o = 16; o; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-      d += __shfl_xor_sync(0xffffffffu, d, o);
-    }
-    if ((threadIdx.x & 31) == 0 && (a | b | d)) {
-      atomicAdd(&stats->windows, a);
-      atomicAdd(&stats->increments, b);
-      atomicAdd(&stats->nodes_created, d);
-    }
   }
 }
 
@@ -463,7 +507,9 @@ __device__ void cursor_flush(const DevCache& c, const CursorSmem& S, int lane) {
       const int e = b + i * 32 + lane;
       if (e >= nc) continue;
       const uint32_t h = S.log_h[e], u = S.log_par[e];
-      const int32_t tk = S.log_tok[e];
+      const int32_t tkf = S.log_tok[e];
+      const bool counted = tkf >= 0;  // (walk hops before `from` create without counting)
+      const int32_t tk = tkf & 0x7FFFFFFF;
       uint32_t pos;
       if (k0[i] == 0) {  // inline child 0 (read only by later kernels)
         uint4* r = rec_of(c, u);
@@ -474,7 +520,7 @@ __device__ void cursor_flush(const DevCache& c, const CursorSmem& S, int lane) {
         pos = place_child(c, u, k0[i] - 1, h, tk);
       }
       st_relaxed_u32(&c.hash[h].aux, pos);
-      if (is_slot_word(pos)) atomicAdd(&c.scnt[pos], 1u);
+      if (counted && is_slot_word(pos)) atomicAdd(&c.scnt[pos], 1u);
     }
   }
   __syncwarp();
@@ -591,101 +637,15 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     uint32_t par[NG], hnew[NG], aux[NG];
     bool act[NG], cre[NG];
     unsigned long long key[NG];
-    // Probe every depth's edge as a warp-convergent state machine: in each
-    // round every unresolved probe issues its next memory operation (a slot
-    // pair load and/or a CAS) before any result is used, so a position costs
-    // max-over-lanes probe rounds instead of the sum of divergent paths.
-    // Round 0 claims the home slot with a CAS while loading the home pair.
-    // Each load reads 4 consecutive slots (two 32-byte loads) so that an
-    // occupied home almost never costs more than one extra round (the CAS at
-    // the first EMPTY slot seen).
-    SlotPair qa[NG], qb[NG];
-    unsigned long long ps[NG], cs[NG], rk[NG];
-    int op[NG];  // bit 0: load slots ps .. ps+3, bit 1: CAS at cs; 0 = resolved
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
-      act[g] = false;
-      cre[g] = false;
-      hnew[g] = NONE;
-      aux[g] = NONE;
-      op[g] = 0;
       const int32_t l = 32 * g + lane + 1;
       par[g] = l <= D ? S.A[l - 1] : NONE;
       act[g] = l <= D && !oov && l <= lim && par[g] < BAD;
-      if (!act[g]) continue;
-      key[g] = edge_key(par[g], (uint32_t)tk);
-      ps[g] = cs[g] = home_slot(c, key[g]);
-      op[g] = 3;
+      key[g] = act[g] ? edge_key(par[g], (uint32_t)tk) : 0ull;
     }
     const long long tr = clock64();
-    for (int round = 0;; ++round) {
-      bool live = false;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) live |= op[g] != 0;
-      if (!__any_sync(0xffffffffu, live)) break;
-      ++rounds;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {  // issue
-        if (op[g] & 1) {
-          qa[g] = ld_pair(c.hash + ps[g]);
-          qb[g] = ld_pair(c.hash + ((ps[g] + 2) & mask));
-        }
-        if (op[g] & 2) rk[g] = atomicCAS(&c.hash[cs[g]].key, EMPTY_KEY, key[g]);
-      }
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {  // resolve (registers only)
-        if (!op[g]) continue;
-        int from = 0;  // index among the 4 loaded slots to scan from
-        if (op[g] & 2) {
-          const int ci = (int)((cs[g] - ps[g]) & mask);  // 0..3: the CAS slot
-          if (rk[g] == EMPTY_KEY) {
-            op[g] = 0;
-            cre[g] = true;
-            hnew[g] = (uint32_t)cs[g];
-            continue;
-          }
-          if (rk[g] == key[g]) {
-            op[g] = 0;
-            hnew[g] = (uint32_t)cs[g];
-            const SlotPair& qq = ci < 2 ? qa[g] : qb[g];
-            const unsigned long long kk = (ci & 1) ? qq.k1 : qq.k0;
-            aux[g] = kk == key[g] ? ((ci & 1) ? qq.a1 : qq.a0) : NONE;
-            continue;
-          }
-          from = ci + 1;  // slot cs holds another key
-        }
-        int next = 0;  // -1: found, 2: CAS slot ps + i, 0: load the next 4 slots
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < from || next) continue;
-          const SlotPair& qq = i < 2 ? qa[g] : qb[g];
-          const unsigned long long kk = (i & 1) ? qq.k1 : qq.k0;
-          if (kk == key[g]) {
-            hnew[g] = (uint32_t)((ps[g] + i) & mask);
-            aux[g] = (i & 1) ? qq.a1 : qq.a0;
-            next = -1;
-          } else if (kk == EMPTY_KEY) {
-            cs[g] = (ps[g] + i) & mask;
-            next = 2;
-          }
-        }
-        if (next == -1) {
-          op[g] = 0;
-        } else if (next == 2) {
-          op[g] = 2;
-        } else {
-          ps[g] = (ps[g] + 4) & mask;
-          cs[g] = ps[g];
-          op[g] = 1;
-        }
-        if (round > 1 << 20) {  // never: the table would be full
-          op[g] = 0;
-          act[g] = false;
-          hnew[g] = BAD;
-          set_error(c, SRT_DEV_CAPACITY);
-        }
-      }
-    }
+    rounds += probe_edges<NG>(c, key, act, hnew, cre, aux);
     // counts (fire and forget) and the batch logs (warp-aggregated appends)
     const long long tc = clock64();
     tp_res += tc - tr;
@@ -786,6 +746,137 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   }
 }
 
+// Walk insertion (spans longer than D, run-ahead spans, no cursor): every
+// window start is one lane's walk from the root along tokens[i .. i+D) (new
+// nodes created, windows ending at a new position counted).  A warp's 32
+// walks advance one hop per step with the convergent probe (probe_edges);
+// linking new nodes and the mirror counts of pending ones are logged and
+// batched per warp exactly as in the cursor kernel.  Window starts are
+// flattened over the spans by an exclusive scan (k_insert_plan) so a
+// 2k-token run-ahead span spreads over the whole grid.
+__global__ void __launch_bounds__(CURSOR_WARPS * 32)
+k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
+              const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
+              const int32_t* __restrict__ to, const int32_t* __restrict__ floor_,
+              const long long* __restrict__ offs, srt_insert_stats* stats) {
+  extern __shared__ __align__(16) unsigned char cur_smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  CursorSmem S;
+  {
+    unsigned char* b = cur_smem + (size_t)w * cursor_warp_bytes(c.D);
+    b += ((size_t)(c.D + 1) * 4 + 15) & ~size_t(15);
+    b += ((size_t)(c.D + 1) + 15) & ~size_t(15);
+    S.A = nullptr;
+    S.fresh = nullptr;
+    S.log_h = reinterpret_cast<uint32_t*>(b);
+    S.log_par = S.log_h + LOGCAP;
+    S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
+    S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
+    S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
+  }
+  if (lane == 0) S.nlog[0] = S.nlog[1] = 0;
+  __syncwarp();
+  const long long total = offs[n];
+  unsigned windows = 0, incs = 0, created = 0;
+  const long long stride_w = (long long)gridDim.x * CURSOR_WARPS * 32;
+  for (long long base = ((long long)blockIdx.x * CURSOR_WARPS + w) * 32; base < total;
+       base += stride_w) {
+    const long long idx = base + lane;
+    int32_t i = 0, j = 0, end = 0, f = 0;
+    uint32_t u = NONE;
+    const int32_t* toks = nullptr;
+    if (idx < total) {
+      int32_t lo_s = 0, hi_s = n - 1;  // span s: offs[s] <= idx < offs[s+1]
+      while (lo_s < hi_s) {
+        const int32_t mid = (lo_s + hi_s + 1) >> 1;
+        if (offs[mid] <= idx) lo_s = mid; else hi_s = mid - 1;
+      }
+      const int32_t s = lo_s;
+      f = from[s];
+      i = span_lo(f, floor_ ? floor_[s] : 0, c.D) + (int32_t)(idx - offs[s]);
+      toks = seq_tok + (int64_t)s * stride;
+      u = root_id(c, prompt_id[s]);
+      end = min(i + c.D, to[s]);
+      j = i;
+      ++windows;
+    }
+    bool live = idx < total && j < end;
+    while (__any_sync(0xffffffffu, live)) {
+      int32_t tk = 0;
+      if (live) {
+        tk = toks[j];
+        if (tk < 0 || tk >= c.V) {
+          set_error(c, SRT_DEV_OOV);
+          live = false;
+        }
+      }
+      const unsigned long long key[1] = {live ? edge_key(u, (uint32_t)tk) : 0ull};
+      bool act[1] = {live};
+      uint32_t hnew[1], aux[1];
+      bool cre[1];
+      probe_edges<1>(c, key, act, hnew, cre, aux);
+      const bool a = act[0];
+      const uint32_t h = hnew[0];
+      const bool counted = a && j >= f;  // a window ends at a new position
+      if (a) {
+        if (cre[0]) c.tok[h] = tk;
+        if (counted) {
+          atomicAdd(&c.cnt[h], 1u);
+          atomicAdd(&rec_of(c, u)->w, 1u);
+          ++incs;
+          if (!cre[0] && is_slot_word(aux[0])) atomicAdd(&c.scnt[aux[0]], 1u);
+        }
+      }
+      log_dirty(c, counted && j - i >= 1 && j - i <= HUB_DIRTY_DEPTH, u);
+      const unsigned mc = __ballot_sync(0xffffffffu, a && cre[0]);
+      const unsigned mp = __ballot_sync(0xffffffffu, counted && !cre[0] && aux[0] == NONE);
+      if (mc | mp) {
+        int bc = 0, bp = 0;
+        if (lane == 0) {
+          bc = S.nlog[0];
+          bp = S.nlog[1];
+          S.nlog[0] = bc + __popc(mc);
+          S.nlog[1] = bp + __popc(mp);
+        }
+        bc = __shfl_sync(0xffffffffu, bc, 0);
+        bp = __shfl_sync(0xffffffffu, bp, 0);
+        const unsigned lt = lanemask_lt();
+        if (mc >> lane & 1) {
+          const int e = bc + __popc(mc & lt);
+          S.log_h[e] = h;
+          S.log_par[e] = u;
+          S.log_tok[e] = counted ? tk : (int32_t)((uint32_t)tk | 0x80000000u);
+          ++created;
+        }
+        if (mp >> lane & 1) S.pend[bp + __popc(mp & lt)] = h;
+      }
+      __syncwarp();
+      if (a) {
+        u = h;
+        ++j;
+      }
+      live = a && j < end;
+      if (S.nlog[0] > LOGCAP - 32 || S.nlog[1] > LOGCAP - 32) cursor_flush(c, S, lane);
+    }
+  }
+  cursor_flush(c, S, lane);
+  count_created(c, created);
+  if (stats) {
+    unsigned long long a = windows, b = incs, d = created;
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    if (lane == 0 && (a | b | d)) {
+      atomicAdd(&stats->windows, a);
+      atomicAdd(&stats->increments, b);
+      atomicAdd(&stats->nodes_created, d);
+    }
+  }
+}
+
 // One dump record per thread (srt_cache_load): the child of its parent (the
 // previous level's node par_idx) labelled tok is created if missing and its
 // count, mirror count and the parent's csum grow by the record's count.
@@ -843,9 +934,14 @@ cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prom
                                const int32_t* seq_tok, int64_t stride, const int32_t* from,
                                const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
                                const long long* scratch, cudaStream_t stream) {
-  carveout_once<k_insert_walk>();
-  k_insert_walk<<<num_sms() * 8, 256, 0, stream>>>(c, n, prompt_id, seq_tok, stride, from, to,
-                                                   floor_, scratch, stats);
+  const size_t smem = insert_cursor_smem(c.D);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_insert_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_insert_walk<<<num_sms() * 4, CURSOR_WARPS * 32, smem, stream>>>(c, n, prompt_id, seq_tok, stride,
+                                                                    from, to, floor_, scratch, stats);
   return cudaGetLastError();
 }
 
