@@ -108,69 +108,76 @@ k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* wor
     const uint32_t nch = r.x;
     const uint32_t nb = blk_index(nch - 2) + 1;
     const uint32_t mybase = lane < (int)nb ? block_base(c, u, lane) : 0u;
-    auto load = [&](uint32_t k, uint32_t& id, int32_t& tk, uint32_t& cn) {
-      const uint32_t jj = k >= 1 ? k - 1 : 0;
-      const uint32_t bi = blk_index(jj);
-      const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
-      id = NONE;
-      cn = 0;
-      tk = 0;
-      if (k == 0) {
-        id = r.y;
-        tk = (int32_t)r.z;
-        cn = c.cnt[id];
-      } else if (k < nch) {
-        const uint32_t pos = base + (jj - blk_start(bi));
-        id = c.slots[pos];
-        tk = c.stok[pos];
-        cn = c.scnt[pos];
-      }
-    };
-    // pass 1: every lane keeps the two largest counts of its children; a warp's
-    // K-th largest of those 64 has >= K children at or above it, so children
-    // below the largest such threshold over the warps can never be in the list
-    uint32_t t1 = 0, t2 = 0;
     constexpr int U4 = 4;  // slices in flight per warp
     constexpr uint32_t STEP = REFRESH_WARPS * 32;
-    for (uint32_t kb = (uint32_t)w * 32; kb < nch; kb += U4 * STEP) {
-      uint32_t cv[U4];
-#pragma unroll
-      for (int q = 0; q < U4; ++q) {
-        const uint32_t k = kb + q * STEP + lane;
-        uint32_t id;
-        int32_t tk;
-        load(k, id, tk, cv[q]);
-        if (k >= nch) cv[q] = 0;
-      }
-#pragma unroll
-      for (int q = 0; q < U4; ++q) {
-        const uint32_t cn = cv[q];
-        if (cn > t1) { t2 = t1; t1 = cn; }
-        else if (cn > t2) t2 = cn;
-      }
-    }
+    // child k (0 = the inline first child) -> its count; its id and token are
+    // loaded only for the few children at or above the threshold
+    auto pos_of = [&](uint32_t k) {
+      const uint32_t jj = k - 1;
+      const uint32_t bi = blk_index(jj);
+      const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
+      return base + (jj - blk_start(bi));
+    };
+    auto load_cnt = [&](uint32_t k) -> uint32_t {
+      const uint32_t pos = pos_of(k >= 1 ? k : 1);
+      return k == 0 ? c.cnt[r.y] : k < nch ? c.scnt[pos] : 0u;
+    };
+    // The previous list of this node (if any) bounds the threshold from below:
+    // counts only grow, so its K children still have counts >= its last
+    // entry's, and no child below that count can enter the new list.
+    const uint32_t slot = hub_slot(c, u);
     uint32_t thr = 0;
-    for (int i = 0; i < K; ++i) {
-      thr = __reduce_max_sync(0xffffffffu, t1);
-      const unsigned who = __ballot_sync(0xffffffffu, t1 == thr);
-      if (lane == __ffs(who) - 1) { t1 = t2; t2 = 0; }
+    if (c.hub_node[slot] == u && c.hub_len[slot] == (uint32_t)K) {
+      thr = c.hub_cnt[(size_t)slot * HUB_K + K - 1];
+    } else {
+      // pass 1: every lane keeps the two largest counts of its children; a warp's
+      // K-th largest of those 64 has >= K children at or above it, so children
+      // below the largest such threshold over the warps can never be in the list
+      uint32_t t1 = 0, t2 = 0;
+      for (uint32_t kb = (uint32_t)w * 32; kb < nch; kb += U4 * STEP) {
+        uint32_t cv[U4];
+#pragma unroll
+        for (int q = 0; q < U4; ++q) cv[q] = load_cnt(kb + q * STEP + lane);
+#pragma unroll
+        for (int q = 0; q < U4; ++q) {
+          const uint32_t cn = cv[q];
+          if (cn > t1) { t2 = t1; t1 = cn; }
+          else if (cn > t2) t2 = cn;
+        }
+      }
+      for (int i = 0; i < K; ++i) {
+        thr = __reduce_max_sync(0xffffffffu, t1);
+        const unsigned who = __ballot_sync(0xffffffffu, t1 == thr);
+        if (lane == __ffs(who) - 1) { t1 = t2; t2 = 0; }
+      }
+      if (lane == 0) sthr[w] = thr;
+      __syncthreads();
+      thr = 0;
+      for (int o = 0; o < REFRESH_WARPS; ++o) thr = max(thr, sthr[o]);
     }
-    if (lane == 0) sthr[w] = thr;
-    __syncthreads();
-    thr = 0;
-    for (int o = 0; o < REFRESH_WARPS; ++o) thr = max(thr, sthr[o]);
     // pass 2: rank only the children at or above the threshold
     KeyList L{0ull, 0ull, NONE, NONE, 0};
     for (uint32_t kb = (uint32_t)w * 32; kb < nch; kb += U4 * STEP) {
-      uint32_t idv[U4], cv[U4];
-      int32_t tkv[U4];
-#pragma unroll
-      for (int q = 0; q < U4; ++q) load(kb + q * STEP + lane, idv[q], tkv[q], cv[q]);
+      uint32_t cv[U4], pv[U4];
 #pragma unroll
       for (int q = 0; q < U4; ++q) {
         const uint32_t k = kb + q * STEP + lane;
-        if (__any_sync(0xffffffffu, k < nch && cv[q] >= thr))
-          L.offer(k < nch && cv[q] >= thr, child_key(cv[q], tkv[q]), idv[q], lane, K);
+        pv[q] = pos_of(k >= 1 ? k : 1);
+        cv[q] = k == 0 ? c.cnt[r.y] : k < nch ? c.scnt[pv[q]] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * STEP + lane;
+        const bool in = k < nch && cv[q] >= thr;
+        if (__any_sync(0xffffffffu, in)) {
+          uint32_t id = NONE;
+          int32_t tk = 0;
+          if (in) {
+            if (k == 0) { id = r.y; tk = (int32_t)r.z; }
+            else { id = c.slots[pv[q]]; tk = c.stok[pv[q]]; }
+          }
+          L.offer(in, child_key(cv[q], tk), id, lane, K);
+        }
       }
     }
     sk[w][lane] = L.k0;
@@ -186,7 +193,6 @@ k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* wor
           if (L.size == K && kk <= L.key_at(K - 1)) break;
           L.insert(kk, sv[o][i], lane, K);
         }
-      const uint32_t slot = hub_slot(c, u);
       const size_t e = (size_t)slot * HUB_K;
       const int len = L.size;
       if (lane < len) {
