@@ -478,13 +478,45 @@ struct CursorSmem {
   uint32_t* log_par;  // [LOGCAP] ... their parents
   int32_t* log_tok;   // [LOGCAP] ... their tokens
   uint32_t* pend;     // [LOGCAP] nodes whose slot word was not published yet
-  int* nlog;          // [2] created, pending
+  int* nlog;          // [4] created, pending, dirty
+  uint32_t* dbuf;     // [DBUF] shallow parents whose csum changed (hub refresh), flushed in batches
 };
+constexpr int DBUF = 96;
 
 __host__ __device__ __forceinline__ size_t cursor_warp_bytes(int32_t D) {
   const size_t a = ((size_t)(D + 1) * 4 + 15) & ~size_t(15);
   const size_t f = ((size_t)(D + 1) + 15) & ~size_t(15);
-  return a + f + (size_t)LOGCAP * 16 + 16;
+  return a + f + (size_t)LOGCAP * 16 + 16 + (size_t)DBUF * 4;
+}
+
+// The dirty log (parents whose csum changed, for the hub refresh) is kept in
+// shared memory and appended to the global list once per batch: a global
+// append per position would put an atomic round trip on the insert's
+// critical path.
+__device__ __forceinline__ void dirty_flush(const DevCache& c, const CursorSmem& S, int lane) {
+  __syncwarp();
+  const int nd = S.nlog[2];
+  if (nd) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(c.dirty_n, (uint32_t)nd);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int i = lane; i < nd; i += 32)
+      if (base + i < DIRTY_CAP) c.dirty[base + i] = S.dbuf[i];
+  }
+  __syncwarp();
+  if (lane == 0) S.nlog[2] = 0;
+  __syncwarp();
+}
+__device__ __forceinline__ void dirty_push(const DevCache& c, const CursorSmem& S, bool want,
+                                           uint32_t u, int lane) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  if (S.nlog[2] + __popc(m) > DBUF) dirty_flush(c, S, lane);
+  const int nd = S.nlog[2];
+  if (want) S.dbuf[nd + __popc(m & lanemask_lt())] = u;
+  __syncwarp();
+  if (lane == 0) S.nlog[2] = nd + __popc(m);
+  __syncwarp();
 }
 
 // Link the logged nodes, publish their slot words and add the mirror counts;
@@ -568,6 +600,7 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
     S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
     S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
+    S.dbuf = reinterpret_cast<uint32_t*>(S.nlog + 4);
   }
   uint32_t* cur = cursor + (size_t)s * (D + 4);
   const int32_t p = prompt_id[s];
@@ -590,7 +623,7 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   if (lane == 0) {
     S.A[0] = root_id(c, p);
     S.fresh[0] = 0;
-    S.nlog[0] = S.nlog[1] = 0;
+    S.nlog[0] = S.nlog[1] = S.nlog[2] = 0;
   }
   if (valid) {
     for (int32_t l = 1 + lane; l <= D; l += 32) {
@@ -628,9 +661,11 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   tp_cur = clock64() - tp0;
   constexpr int ngroups = NG;
   const unsigned long long mask = c.H - 1;
+  int32_t ybuf = 0;  // the span's tokens, 32 positions per load (lane i: position j + i)
   for (int32_t j = P; j < t_end; ++j) {
     const long long tj = clock64();
-    const int32_t tk = y[j];
+    if (((j - P) & 31) == 0) ybuf = j + lane < t_end ? y[j + lane] : 0;
+    const int32_t tk = __shfl_sync(0xffffffffu, ybuf, (j - P) & 31);
     const bool oov = tk < 0 || tk >= c.V;
     if (oov && lane == 0) set_error(c, SRT_DEV_OOV);
     const int32_t lim = min(D, j - max(fl, 0) + 1);  // windows ending at j start >= floor
@@ -663,7 +698,7 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       }
       if (g == 0) {  // shallow parents whose csum changed: their hub lists are rebuilt after the call
         const int32_t l = lane + 1;
-        log_dirty(c, a && l >= 2 && l <= 1 + HUB_DIRTY_DEPTH, par[g]);
+        dirty_push(c, S, a && l >= 2 && l <= 1 + HUB_DIRTY_DEPTH, par[g], lane);
       }
       const unsigned mc = __ballot_sync(0xffffffffu, a && cre[g]);
       const unsigned mp = __ballot_sync(0xffffffffu, a && !cre[g] && aux[g] == NONE);
@@ -705,6 +740,7 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   {
     const long long tb = clock64();
     cursor_flush(c, S, lane);
+    dirty_flush(c, S, lane);
     tp_batch = clock64() - tb;
   }
   for (int32_t l = 1 + lane; l <= D; l += 32) cur[4 + l - 1] = S.A[l];
@@ -774,8 +810,9 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
     S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
     S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
+    S.dbuf = reinterpret_cast<uint32_t*>(S.nlog + 4);
   }
-  if (lane == 0) S.nlog[0] = S.nlog[1] = 0;
+  if (lane == 0) S.nlog[0] = S.nlog[1] = S.nlog[2] = 0;
   __syncwarp();
   const long long total = offs[n];
   unsigned windows = 0, incs = 0, created = 0;
@@ -802,10 +839,11 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       ++windows;
     }
     bool live = idx < total && j < end;
+    int32_t tk_nx = live ? toks[j] : 0;
     while (__any_sync(0xffffffffu, live)) {
-      int32_t tk = 0;
+      int32_t tk = tk_nx;
       if (live) {
-        tk = toks[j];
+        tk_nx = j + 1 < end ? toks[j + 1] : 0;  // next hop's token, in flight during the probe
         if (tk < 0 || tk >= c.V) {
           set_error(c, SRT_DEV_OOV);
           live = false;
@@ -828,7 +866,7 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
           if (!cre[0] && is_slot_word(aux[0])) atomicAdd(&c.scnt[aux[0]], 1u);
         }
       }
-      log_dirty(c, counted && j - i >= 1 && j - i <= HUB_DIRTY_DEPTH, u);
+      dirty_push(c, S, counted && j - i >= 1 && j - i <= HUB_DIRTY_DEPTH, u, lane);
       const unsigned mc = __ballot_sync(0xffffffffu, a && cre[0]);
       const unsigned mp = __ballot_sync(0xffffffffu, counted && !cre[0] && aux[0] == NONE);
       if (mc | mp) {
@@ -861,6 +899,7 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     }
   }
   cursor_flush(c, S, lane);
+  dirty_flush(c, S, lane);
   count_created(c, created);
   if (stats) {
     unsigned long long a = windows, b = incs, d = created;
