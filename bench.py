@@ -99,6 +99,9 @@ class ClockSampler:
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # block until the sampler is live (its first line), so that a short
+            # timed region still gets samples at the 20 ms cadence
+            self.first = self.p.stdout.readline()
         except Exception:
             self.p = None
         return self
@@ -113,6 +116,8 @@ class ClockSampler:
                 self.p.kill()
                 out = ""
             self.lines = [l for l in out.splitlines() if l.strip()]
+            if not self.lines and getattr(self, "first", "").strip():
+                self.lines = [self.first]  # region shorter than one period: the sample at its start
 
     def summary(self):
         sm, mx, reasons = [], None, set()
