@@ -200,7 +200,6 @@ srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const 
   if (!c->hubwork)
     SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
              "cudaMallocAsync(hub work)");
-  SRT_CUDA(cudaMemsetAsync(c->dev.dirty_n, 0, 4, stream), "insert");
   // cursor path: spans of <= D new positions; longer ones (run-ahead) walk
   const int32_t short_max = cursor ? c->cfg.max_depth : -1;
   SRT_CUDA(timed(c, SRT_K_INSERT_PLAN, stream,

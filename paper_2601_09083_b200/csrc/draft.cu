@@ -195,6 +195,10 @@ __device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, doub
       }
       return;
     }
+    if (lane == 0) {  // no valid list for this hub: the refresh after the next insert builds it
+      const uint32_t e = atomicAdd(c.dirty_n, 1u);
+      if (e < DIRTY_CAP) c.dirty[e] = u;
+    }
   }
   // block bases of blocks 0..nb-1 (children 1..nch-1), one lane each
   const uint32_t nb = blk_index(nch - 2) + 1;

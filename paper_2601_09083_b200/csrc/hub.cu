@@ -8,7 +8,8 @@
 // unchanged (counts only grow), so it is never stale.
 //
 // After every insert call: the inserts logged the shallow parents whose csum
-// they changed (the dirty list); k_hub_pick elects one refresher per cache
+// they changed and srt_draft logged the hubs it had to expand without a valid
+// list (the dirty list); k_hub_pick elects one refresher per cache
 // slot (a node listed several times, or two hubs sharing a slot, refresh
 // once), and k_hub_refresh rebuilds each elected list with one CTA: a count
 // threshold first (lane-wise top-2 counts), then every warp keeps a sorted
@@ -94,7 +95,10 @@ __global__ void k_hub_pick(DevCache c, uint32_t* work, uint32_t* work_n) {
 
 __global__ void __launch_bounds__(REFRESH_WARPS * 32)
 k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* work_n) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) c.dirty_n[1] += 1;  // next refresh's generation
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.dirty_n[1] += 1;  // next refresh's generation
+    c.dirty_n[0] = 0;   // k_hub_pick consumed the list
+  }
   __shared__ unsigned long long sk[REFRESH_WARPS][HUB_K];
   __shared__ uint32_t sv[REFRESH_WARPS][HUB_K];
   __shared__ int sn[REFRESH_WARPS];

@@ -87,7 +87,7 @@ struct DevCache {
   int32_t* hub_tok;     // [HC][HUB_K]
   uint32_t* hub_cnt;    // [HC][HUB_K]
   unsigned long long* hub_claim;  // [HC] (insert call << 32 | node) of the last refresh claim
-  uint32_t* dirty;      // [DIRTY_CAP] parents whose csum an insert changed (shallow ones)
+  uint32_t* dirty;      // [DIRTY_CAP] parents whose csum an insert changed (shallow ones) and hubs a draft found without a valid list
   uint32_t* dirty_n;    // [0] entries, [1] refresh generation (a device counter: graph-safe)
 };
 
