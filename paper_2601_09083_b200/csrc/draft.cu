@@ -104,6 +104,54 @@ struct Frontier {
     if (lane >= pos) e0 = (lane == pos) ? b : u0;
     size = min(size + 1, cap);
   }
+  // Merge na sorted candidates (lane k holds candidate k, best first) into the
+  // frontier in one pass: the result is the top cap of both, exactly what na
+  // inserts in order would leave.  Each side's position in the merged order
+  // is its index plus its rank in the other side (branchless binary searches
+  // over shuffles); the merged entries are exchanged through sm (64 entries).
+  // Returns whether the last candidate made it (if not, later ones cannot).
+  __device__ __forceinline__ bool merge(const Ent& a, int na, int cap, int lane, Ent* sm) {
+    const bool wide = cap > 32;  // (warp-uniform) entries 32.. in e1
+    int ra = 0;                  // frontier entries better than a
+    for (int step = wide ? 64 : 32; step >= 1; step >>= 1) {
+      const int probe = ra + step - 1;
+      const int src = probe & 31;
+      const double s0 = __shfl_sync(0xffffffffu, e0.score, src);
+      const unsigned long long m0 = __shfl_sync(0xffffffffu, e0.meta, src);
+      double sc = s0;
+      unsigned long long mt = m0;
+      if (wide) {
+        const double s1 = __shfl_sync(0xffffffffu, e1.score, src);
+        const unsigned long long m1 = __shfl_sync(0xffffffffu, e1.meta, src);
+        if (probe >= 32) { sc = s1; mt = m1; }
+      }
+      if (probe < size && better(Ent{sc, mt, 0u}, a)) ra += step;
+    }
+    int rb0 = 0, rb1 = 0;  // candidates better than frontier entries lane, lane + 32
+    for (int step = 32; step >= 1; step >>= 1) {
+      const int probe0 = rb0 + step - 1, probe1 = rb1 + step - 1;
+      const double s0 = __shfl_sync(0xffffffffu, a.score, probe0 & 31);
+      const unsigned long long m0 = __shfl_sync(0xffffffffu, a.meta, probe0 & 31);
+      if (probe0 < na && better(Ent{s0, m0, 0u}, e0)) rb0 += step;
+      if (wide) {
+        const double s1 = __shfl_sync(0xffffffffu, a.score, probe1 & 31);
+        const unsigned long long m1 = __shfl_sync(0xffffffffu, a.meta, probe1 & 31);
+        if (probe1 < na && better(Ent{s1, m1, 0u}, e1)) rb1 += step;
+      }
+    }
+    const int pa = lane + ra, p0 = lane + rb0, p1 = lane + 32 + rb1;
+    if (lane < na && pa < cap) sm[pa] = a;
+    if (lane < size && p0 < cap) sm[p0] = e0;
+    if (wide && lane + 32 < size && p1 < cap) sm[p1] = e1;
+    __syncwarp();
+    const bool last_in = __shfl_sync(0xffffffffu, pa, (na - 1) & 31) < cap;
+    size = min(size + na, cap);
+    const Ent none{-1.0, META_NONE, NONE};
+    e0 = lane < size ? sm[lane] : none;
+    if (wide) e1 = lane + 32 < size ? sm[lane + 32] : none;
+    __syncwarp();
+    return last_in;
+  }
   // Remove entry 0 (returned).
   __device__ __forceinline__ Ent pop(int lane) {
     const Ent top = ent_shfl(e0, 0);
@@ -144,7 +192,7 @@ __device__ __forceinline__ long long count_floor(double w, double score_u, doubl
 // frontier.  rec[u] is one 16-byte load; a single child needs nothing else
 // (its C is exactly 1).
 __device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, double score_u,
-                       int32_t depth_u, int32_t parent_idx, int lane, ExpandProf& pf) {
+                       int32_t depth_u, int32_t parent_idx, int lane, ExpandProf& pf, Ent* sm) {
   if (cap <= 0) return;
   long long t0 = clock64();
   const uint4 r = ld_rec(c, u);
@@ -181,17 +229,25 @@ __device__ void expand(const DevCache& c, Frontier& F, int cap, uint32_t u, doub
           cd.score = child_score(score_u, dsum, c.hub_cnt[e + k]);
           cd.meta = meta0 | ((unsigned long long)(uint32_t)c.hub_tok[e + k] << 7);
         }
-        bool stop = false;
-        for (int src = 0; src < 32 && kb + src < len; ++src) {  // in order: stop at the first loser
-          const Ent b = ent_shfl(cd, src);
-          const Ent bar = F.size == cap ? F.at(cap - 1) : Ent{-1.0, META_NONE, NONE};
-          if (!better(b, bar)) {
-            stop = true;
-            break;
+        // candidates (sorted) that beat the current last entry: only they can enter
+        const Ent bar = F.size == cap ? F.at(cap - 1) : Ent{-1.0, META_NONE, NONE};
+        const int nb = __popc(__ballot_sync(0xffffffffu, k < len && better(cd, bar)));
+        if (nb > 4) {  // many: one merge
+          if (!F.merge(cd, nb, cap, lane, sm)) break;
+        } else {  // few: inserts in order, stopping at the first loser
+          bool stop = false;
+          for (int src = 0; src < nb; ++src) {
+            const Ent b = ent_shfl(cd, src);
+            const Ent bar2 = F.size == cap ? F.at(cap - 1) : Ent{-1.0, META_NONE, NONE};
+            if (!better(b, bar2)) {
+              stop = true;
+              break;
+            }
+            F.insert(b, cap, lane);
           }
-          F.insert(b, cap, lane);
+          if (stop) break;
         }
-        if (stop) break;
+        if (nb < 32) break;  // the rest of the list does not beat the last entry either
       }
       return;
     }
@@ -291,6 +347,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         int32_t* __restrict__ draft_parent, int32_t* __restrict__ draft_depth,
         int32_t* __restrict__ draft_pos, uint64_t* __restrict__ draft_mask) {
   __shared__ unsigned long long masks[DRAFT_WARPS][64];  // ancestor-or-self masks (O9)
+  __shared__ Ent merge_buf[DRAFT_WARPS][64];             // frontier merges
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int32_t s = blockIdx.x * DRAFT_WARPS + w;
@@ -359,7 +416,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       maxch = max(maxch, nc);
     }
     Frontier F{Ent{-1.0, META_NONE, NONE}, Ent{-1.0, META_NONE, NONE}, 0};
-    expand(c, F, B, uq, 1.0, 0, -1, lane, pf);
+    expand(c, F, B, uq, 1.0, 0, -1, lane, pf, merge_buf[w]);
     prefetch_frontier(c, F, lane);
     while (popped < B && F.size > 0) {
       if (__shfl_sync(0xffffffffu, F.e0.score, 0) < c.min_score) break;
@@ -383,7 +440,7 @@ k_draft(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
         scanned += nc;
         maxch = max(maxch, nc);
       }
-      expand(c, F, cap, top.node, top.score, dep, i, lane, pf);
+      expand(c, F, cap, top.node, top.score, dep, i, lane, pf, merge_buf[w]);
       prefetch_frontier(c, F, lane);
     }
   }
