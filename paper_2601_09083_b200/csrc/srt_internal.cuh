@@ -91,7 +91,7 @@ struct DevCache {
   uint32_t* dirty_n;    // [0] entries, [1] refresh generation (a device counter: graph-safe)
 };
 
-constexpr uint32_t HUB_MIN = 64;  // more children than one draft round
+constexpr uint32_t HUB_MIN = 64;  // listed above this fan-out (measured: 32 / 128 / 256 slower or equal)
 constexpr int HUB_K = 64;          // >= Bmax
 constexpr uint32_t DIRTY_CAP = 1u << 20;
 constexpr int HUB_DIRTY_DEPTH = 2;  // parents at depth 1..2 are logged as dirty
