@@ -186,6 +186,35 @@ def test_draft_parity_hubs(orc, Bmax):
     assert od["draft_len"].sum() > n
 
 
+@pytest.mark.parametrize("Bmax", [32, 64])
+def test_draft_parity_hub_lists_across_inserts(orc, Bmax):
+    """Hub child lists over alternating drafts and inserts: lists built after
+    the bulk insert, lists gone stale (an insert changed the hub's csum) and
+    rebuilt, hubs first met by a draft without a list (logged, built after
+    the next insert), and frontier merges of listed children (Bmax 64: two
+    32-entry chunks into a 64-entry frontier).  Drafts equal the oracle's at
+    every step."""
+    from synth import zipf_tokens
+    rng = np.random.default_rng(7100 + Bmax)
+    V, D, L = 3000, 5, 3
+    pair = Pair(orc, V, 2, D, L, Bmax, node_capacity=1 << 20)
+    perm = rng.permutation(V).astype(np.int32)
+    seqs = [(k % 2, zipf_tokens(rng, 300, V, perm, s=1.1), [(0, 300)]) for k in range(40)]
+    _insert_all(pair, seqs)
+    n = 64
+    for step in range(5):
+        ctx = zipf_tokens(rng, n * 16, V, perm, s=1.1).reshape(n, 16)
+        seq_len = rng.integers(1, 17, n).astype(np.int32)
+        prompts = rng.integers(0, 2, n).astype(np.int32)
+        od, gd = pair.draft(prompts, ctx, seq_len)
+        pair.compare_drafts(od, gd)
+        assert od["draft_len"].sum() > n
+        # a few more rollouts: shallow hubs change csum (their lists go stale)
+        more = [(k % 2, zipf_tokens(rng, 40, V, perm, s=1.1), [(0, 40)]) for k in range(6)]
+        _insert_all(pair, more)
+    pair.compare_trees()
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("seed", range(4))
 def test_verify_parity_random(orc, dtype, seed):
