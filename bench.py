@@ -64,7 +64,8 @@ CONFIGS = {
                  runahead=dict(first=64, prompts=64, per=4, spans=8, lo=512, hi=2048)),
 }
 
-KERNELS_PER_STEP = 9  # per group: draft, row_offsets, scan, accept, insert_plan/walk/cursor
+KERNELS_PER_STEP = 9  # timed segments per group and step (an upper bound, for the profile buffer)
+SEGMENT_KERNELS = {"scan": 2, "hub_refresh": 2}  # segments that launch two kernels
                       # (+ insert_plan/walk of the run-ahead spans)
 
 
@@ -250,6 +251,7 @@ class Group:
             raise RuntimeError(f"cache error bits {bits} after warm-up inserts ({st})")
         self.tree_stats = st
         self.path_rounds = None  # srt_verify_path rounds (bench --verify path)
+        self.fused = True  # srt_verify_insert_cursor (accept + cursor insert in one kernel)
         # ---- run-ahead spans (DAPO): a fixed schedule, uploaded once
         self.ra = None
         if wl.w.runahead and cfg.get("runahead"):
@@ -313,10 +315,14 @@ class Group:
 
     def verify_insert(self, seed: int, logits=None):
         c = self.cache
-        c.verify(self.logits if logits is None else logits, self.d, self.seq_id, seed, self.seq_tok,
-                 self.seq_len, self.max_new, out=self.v, rows=self.rows_max,
-                 path_rounds=self.path_rounds)
-        c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len, cursor=self.cursor)
+        lg = self.logits if logits is None else logits
+        if self.fused and self.path_rounds is None:
+            c.verify_insert(lg, self.d, self.seq_id, seed, self.seq_tok, self.seq_len, self.max_new,
+                            self.prompt_id, self.cursor, out=self.v, rows=self.rows_max)
+        else:
+            c.verify(lg, self.d, self.seq_id, seed, self.seq_tok, self.seq_len, self.max_new,
+                     out=self.v, rows=self.rows_max, path_rounds=self.path_rounds)
+            c.insert(self.prompt_id, self.seq_tok, self.t_before, self.seq_len, cursor=self.cursor)
         if self.ra is not None:
             self.runahead_insert()
 
@@ -968,10 +974,12 @@ def main():
         "kernels": kern,
         "tree_stage_us_per_batch": {k: kern[k]["mean_us"] for k in
                                     ("draft", "row_offsets", "insert_plan", "insert_walk",
-                                     "insert_cursor", "accept")
+                                     "insert_cursor", "accept", "accept_insert")
                                     if k in kern},
-        "gpu_launches": int(round(len(prof) / KP * K)),
-        "launches_per_step": len(prof) / KP,
+        # kernels per timed segment: the scan segment launches k_rowinfo + k_scan_rows,
+        # the hub refresh k_hub_pick + k_hub_refresh; every other segment one kernel
+        "gpu_launches": int(round(sum(SEGMENT_KERNELS.get(name, 1) for name, _ in prof) / KP * K)),
+        "launches_per_step": sum(SEGMENT_KERNELS.get(name, 1) for name, _ in prof) / KP,
         "tree_nodes": st["nodes_used"],
     }
     cs = clk.summary()

@@ -298,6 +298,28 @@ SRT_API srt_status srt_verify_path(srt_cache* cache, int32_t n, int32_t path_rou
                                    int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
                                    int32_t* accepted_nodes, uint8_t* finished, void* stream);
 
+/*
+ * srt_verify_insert_cursor — srt_verify followed by srt_insert_cursor of the
+ * committed spans, with the accept walk and the insert fused into one kernel
+ * (one warp per sequence commits its tokens, and inserts the windows
+ * ending at them through its cursor right away, "updated online";
+ * DESIGN.md §5 f1).  Arguments: those of srt_verify, then prompt_id[n] (the
+ * tree each sequence inserts into), floor[n] (nullable, as srt_insert),
+ * cursor[n][D + 4] and stats (nullable), as srt_insert_cursor; the span of
+ * sequence s is [seq_len_before, seq_len_after) — every span goes through
+ * the cursor (at most Bmax + 1 tokens).  Results are identical to srt_verify
+ * then srt_insert_cursor(from = the old seq_len, to = the new one): the same
+ * outputs, trees, cursors and hub-list refresh.  Errors as both calls.
+ */
+SRT_API srt_status srt_verify_insert_cursor(
+    srt_cache* cache, int32_t n, const void* logits, const int64_t* row_offsets,
+    const int32_t* draft_len, const int32_t* draft_tok, const int32_t* draft_parent,
+    const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed, float temperature,
+    int32_t eos_id, const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len,
+    int32_t* sampled, int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+    int32_t* accepted_nodes, uint8_t* finished, const int32_t* prompt_id, const int32_t* floor,
+    uint32_t* cursor, srt_insert_stats* stats, void* stream);
+
 /* records[s] <- the draft of sequence s < n (srt_draft's outputs). */
 SRT_API srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
                            const int32_t* draft_len, const int32_t* draft_tok,
@@ -414,7 +436,8 @@ typedef enum {
   SRT_K_SCAN = 4,
   SRT_K_ACCEPT = 5,
   SRT_K_INSERT_CURSOR = 6,
-  SRT_K_HUB_REFRESH = 7  /* the hub child lists an insert call rebuilds */
+  SRT_K_HUB_REFRESH = 7, /* the hub child lists an insert call rebuilds */
+  SRT_K_ACCEPT_INSERT = 8 /* srt_verify_insert_cursor's fused accept + cursor insert */
 } srt_kernel_id;
 
 typedef struct {

@@ -290,6 +290,27 @@ srt_status srt_draft_cursor(srt_cache* c, int32_t n, const int32_t* prompt_id,
   return SRT_OK;
 }
 
+namespace {
+// The verify scan (rows scratch sized without reading row_offsets back: rows
+// <= n * (Bmax + 1)).
+srt_status verify_scan(srt_cache* c, const VerifyArgs& a, cudaStream_t stream) {
+  const int64_t rows_max = (int64_t)a.n * (c->cfg.budget_max + 1);
+  if (c->row_cap < rows_max) {
+    if (c->rowinfo) SRT_CUDA(cudaFreeAsync(c->rowinfo, stream), "cudaFreeAsync(rowinfo)");
+    if (c->result) SRT_CUDA(cudaFreeAsync(c->result, stream), "cudaFreeAsync(result)");
+    const int64_t cap = std::max<int64_t>(rows_max, 4096);
+    SRT_CUDA(cudaMallocAsync(&c->rowinfo, cap * sizeof(int2), stream), "cudaMallocAsync(rowinfo)");
+    SRT_CUDA(cudaMallocAsync(&c->result, cap * sizeof(unsigned long long), stream),
+             "cudaMallocAsync(result)");
+    c->row_cap = cap;
+  }
+  SRT_CUDA(timed(c, SRT_K_SCAN, stream,
+                 [&] { return launch_scan(c->dev, a, false, c->rowinfo, c->result, stream); }),
+           "verify scan");
+  return SRT_OK;
+}
+}  // namespace
+
 srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t* row_offsets,
                       const int32_t* draft_len, const int32_t* draft_tok,
                       const int32_t* draft_parent, const int32_t* draft_depth,
@@ -310,23 +331,52 @@ srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t
                seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
                accepted_nodes, finished};
   cudaStream_t stream = (cudaStream_t)stream_;
-  // rows <= n * (Bmax + 1): size the scratch without reading row_offsets back
-  const int64_t rows_max = (int64_t)n * (c->cfg.budget_max + 1);
-  if (c->row_cap < rows_max) {
-    if (c->rowinfo) SRT_CUDA(cudaFreeAsync(c->rowinfo, stream), "cudaFreeAsync(rowinfo)");
-    if (c->result) SRT_CUDA(cudaFreeAsync(c->result, stream), "cudaFreeAsync(result)");
-    const int64_t cap = std::max<int64_t>(rows_max, 4096);
-    SRT_CUDA(cudaMallocAsync(&c->rowinfo, cap * sizeof(int2), stream), "cudaMallocAsync(rowinfo)");
-    SRT_CUDA(cudaMallocAsync(&c->result, cap * sizeof(unsigned long long), stream),
-             "cudaMallocAsync(result)");
-    c->row_cap = cap;
-  }
-  SRT_CUDA(timed(c, SRT_K_SCAN, stream,
-                 [&] { return launch_scan(c->dev, a, false, c->rowinfo, c->result, stream); }),
-           "verify scan");
+  const srt_status st = verify_scan(c, a, stream);
+  if (st != SRT_OK) return st;
   SRT_CUDA(timed(c, SRT_K_ACCEPT, stream,
                  [&] { return launch_accept(c->dev, a, c->result, stream); }),
            "verify accept");
+  return SRT_OK;
+}
+
+srt_status srt_verify_insert_cursor(
+    srt_cache* c, int32_t n, const void* logits, const int64_t* row_offsets,
+    const int32_t* draft_len, const int32_t* draft_tok, const int32_t* draft_parent,
+    const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed, float temperature,
+    int32_t eos_id, const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len,
+    int32_t* sampled, int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+    int32_t* accepted_nodes, uint8_t* finished, const int32_t* prompt_id, const int32_t* floor_,
+    uint32_t* cursor, srt_insert_stats* stats_dev, void* stream_) {
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!logits || !row_offsets || !draft_len || !draft_tok || !draft_parent || !draft_depth ||
+      !seq_id || !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit ||
+      !commit_tok || !accepted_nodes || !finished || !prompt_id || !cursor)
+    return SRT_ERR_INVALID_ARG;
+  if (insert_cursor_smem(c->cfg.max_depth) > 200 * 1024) return SRT_ERR_INVALID_ARG;
+  VerifyArgs a{n,       logits,     (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
+               draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
+               seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
+               accepted_nodes, finished};
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!c->hubwork)
+    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
+             "cudaMallocAsync(hub work)");
+  const srt_status st = verify_scan(c, a, stream);
+  if (st != SRT_OK) return st;
+  SRT_CUDA(timed(c, SRT_K_ACCEPT_INSERT, stream,
+                 [&] {
+                   return launch_accept_insert(c->dev, a, c->result, prompt_id, floor_, cursor,
+                                               c->tag, stats_dev, stream);
+                 }),
+           "verify accept + insert");
+  SRT_CUDA(timed(c, SRT_K_HUB_REFRESH, stream,
+                 [&] {
+                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + DIRTY_CAP,
+                                             stream);
+                 }),
+           "hub refresh");
   return SRT_OK;
 }
 

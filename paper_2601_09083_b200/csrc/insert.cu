@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "srt_internal.cuh"
+#include "accept.cuh"
 
 namespace srt {
 
@@ -576,36 +577,33 @@ __device__ void cursor_flush(const DevCache& c, const CursorSmem& S, int lane) {
   __syncwarp();
 }
 
-template <int NG>  // depth groups per lane: D <= 32 * NG
-__global__ void __launch_bounds__(CURSOR_WARPS * 32)
-k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
-                const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
-                const int32_t* __restrict__ to, const int32_t* __restrict__ floor_, int32_t short_max,
-                uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
-  extern __shared__ __align__(16) unsigned char cur_smem[];
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const int32_t s = blockIdx.x * CURSOR_WARPS + w;
-  if (s >= n) return;
-  const int32_t D = c.D;
+// This warp's slice of the cursor kernels' dynamic shared memory.
+__device__ __forceinline__ CursorSmem carve_cursor_smem(unsigned char* base, int w, int32_t D) {
   CursorSmem S;
-  {
-    unsigned char* b = cur_smem + (size_t)w * cursor_warp_bytes(D);
-    S.A = reinterpret_cast<uint32_t*>(b);
-    b += ((size_t)(D + 1) * 4 + 15) & ~size_t(15);
-    S.fresh = b;
-    b += ((size_t)(D + 1) + 15) & ~size_t(15);
-    S.log_h = reinterpret_cast<uint32_t*>(b);
-    S.log_par = S.log_h + LOGCAP;
-    S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
-    S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
-    S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
-    S.dbuf = reinterpret_cast<uint32_t*>(S.nlog + 4);
-  }
+  unsigned char* b = base + (size_t)w * cursor_warp_bytes(D);
+  S.A = reinterpret_cast<uint32_t*>(b);
+  b += ((size_t)(D + 1) * 4 + 15) & ~size_t(15);
+  S.fresh = b;
+  b += ((size_t)(D + 1) + 15) & ~size_t(15);
+  S.log_h = reinterpret_cast<uint32_t*>(b);
+  S.log_par = S.log_h + LOGCAP;
+  S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
+  S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
+  S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
+  S.dbuf = reinterpret_cast<uint32_t*>(S.nlog + 4);
+  return S;
+}
+
+// The cursor insertion of sequence s's span [f, t_end) by one warp (prompt p
+// already checked).
+template <int NG>  // depth groups per lane: D <= 32 * NG
+__device__ __forceinline__ void cursor_insert_seq(
+    const DevCache& c, const CursorSmem& S, int32_t s, int32_t p, int32_t f, int32_t t_end,
+    const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ floor_,
+    int32_t short_max, uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
+  const int lane = threadIdx.x & 31;
+  const int32_t D = c.D;
   uint32_t* cur = cursor + (size_t)s * (D + 4);
-  const int32_t p = prompt_id[s];
-  if (p < 0 || p >= c.P) return;  // flagged by the plan kernel
-  const int32_t f = from[s], t_end = to[s];
   const int32_t fl = floor_ ? floor_[s] : 0;
   const int32_t P = max(f, fl);
   if (t_end <= P) return;  // no window ends at a new position: cursor untouched
@@ -780,6 +778,52 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       if (d) atomicAdd(&stats->nodes_created, d);
     }
   }
+}
+
+template <int NG>
+__global__ void __launch_bounds__(CURSOR_WARPS * 32)
+k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
+                const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ from,
+                const int32_t* __restrict__ to, const int32_t* __restrict__ floor_, int32_t short_max,
+                uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
+  extern __shared__ __align__(16) unsigned char cur_smem[];
+  const int w = threadIdx.x >> 5;
+  const int32_t s = blockIdx.x * CURSOR_WARPS + w;
+  if (s >= n) return;
+  const int32_t p = prompt_id[s];
+  if (p < 0 || p >= c.P) return;  // flagged by the plan kernel
+  const CursorSmem S = carve_cursor_smem(cur_smem, w, c.D);
+  cursor_insert_seq<NG>(c, S, s, p, from[s], to[s], seq_tok, stride, floor_, short_max, cursor, tag,
+                        stats);
+}
+
+// Fused accept + cursor insert (srt_verify_insert_cursor): each warp commits
+// its sequence (accept.cuh) and inserts the committed span through its cursor
+// right away — no global round trip and no launch between the two stages.
+// Every span goes through the cursor (a commit is at most Bmax + 1 tokens).
+template <int NG>
+__global__ void __launch_bounds__(CURSOR_WARPS * 32)
+k_accept_insert(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result,
+                const int32_t* __restrict__ prompt_id, const int32_t* __restrict__ floor_,
+                uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
+  extern __shared__ __align__(16) unsigned char cur_smem[];
+  __shared__ int32_t ctok[CURSOR_WARPS][65];
+  __shared__ int32_t acc[CURSOR_WARPS][64];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int32_t s = blockIdx.x * CURSOR_WARPS + w;
+  if (s >= a.n) return;
+  const int32_t t = accept_seq(c, a, result, s, ctok[w], acc[w], lane);
+  __syncwarp();
+  const int32_t t_end = a.seq_len[s];  // (written by lane 0 of this warp)
+  const int32_t p = prompt_id[s];
+  if (p < 0 || p >= c.P) {
+    if (lane == 0) set_error(c, SRT_DEV_BAD_PROMPT);
+    return;
+  }
+  const CursorSmem S = carve_cursor_smem(cur_smem, w, c.D);
+  cursor_insert_seq<NG>(c, S, s, p, t, t_end, a.seq_tok, a.stride, floor_, INT_MAX, cursor, tag,
+                        stats);
 }
 
 // Walk insertion (spans longer than D, run-ahead spans, no cursor): every
@@ -985,6 +1029,23 @@ cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prom
 }
 
 size_t insert_cursor_smem(int32_t D) { return (size_t)CURSOR_WARPS * cursor_warp_bytes(D); }
+
+cudaError_t launch_accept_insert(const DevCache& c, const VerifyArgs& a,
+                                 const unsigned long long* result, const int32_t* prompt_id,
+                                 const int32_t* floor_, uint32_t* cursor, uint32_t tag,
+                                 srt_insert_stats* stats, cudaStream_t stream) {
+  const size_t smem = insert_cursor_smem(c.D);
+  const int ng = (c.D + 31) >> 5;
+  auto kern = ng <= 1 ? k_accept_insert<1> : ng == 2 ? k_accept_insert<2>
+            : ng == 3 ? k_accept_insert<3> : k_accept_insert<4>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<(a.n + CURSOR_WARPS - 1) / CURSOR_WARPS, CURSOR_WARPS * 32, smem, stream>>>(
+      c, a, result, prompt_id, floor_, cursor, tag, stats);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_insert_cursor(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                  const int32_t* seq_tok, int64_t stride, const int32_t* from,

@@ -321,6 +321,10 @@ cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference, 
                         unsigned long long* result, cudaStream_t stream);
 cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, const unsigned long long* result,
                           cudaStream_t stream);
+cudaError_t launch_accept_insert(const DevCache& c, const VerifyArgs& a,
+                                 const unsigned long long* result, const int32_t* prompt_id,
+                                 const int32_t* floor_, uint32_t* cursor, uint32_t tag,
+                                 srt_insert_stats* stats, cudaStream_t stream);
 cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2* rowinfo,
                              const int32_t* row_list, const int64_t* count,
                              unsigned long long* result, cudaStream_t stream);

@@ -11,6 +11,7 @@
 
 #include "noise.cuh"
 #include "srt_internal.cuh"
+#include "accept.cuh"
 
 namespace srt {
 
@@ -124,8 +125,7 @@ k_scan_reference(DevCache c, VerifyArgs a, unsigned long long* result) {
 // ---------------------------------------------------------------------------
 constexpr int ACC_WARPS = 4;
 
-// First decodes the scan's packed per-row winner into sampled[] (0 if the row
-// had no candidate, i.e. every logit NaN), then walks the draft.
+// One warp per sequence (accept.cuh).
 __global__ void __launch_bounds__(ACC_WARPS * 32)
 k_accept(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result) {
   __shared__ int32_t ctok[ACC_WARPS][65];
@@ -133,62 +133,7 @@ k_accept(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int32_t s = blockIdx.x * ACC_WARPS + w;
   if (s >= a.n) return;
-  const int32_t B = c.Bmax;
-  const int32_t ns = a.draft_len[s];
-  const int64_t r0 = a.row_offsets[s];
-  for (int32_t i = lane; i <= ns; i += 32) {  // (~0: a row srt_verify_path did not sample)
-    const unsigned long long rr = result[r0 + i];
-    a.sampled[r0 + i] = rr == ~0ull ? -1 : unpack_index(rr);
-  }
-  __syncwarp();
-  const int32_t t = a.seq_len[s];
-  const int64_t db = (int64_t)s * B;
-  const bool vA = lane < ns, vB = lane + 32 < ns;
-  const int32_t tokA = vA ? a.draft_tok[db + lane] : -1;
-  const int32_t parA = vA ? a.draft_parent[db + lane] : -2;
-  const int32_t smpA = vA ? a.sampled[r0 + 1 + lane] : 0;
-  const int32_t tokB = vB ? a.draft_tok[db + lane + 32] : -1;
-  const int32_t parB = vB ? a.draft_parent[db + lane + 32] : -2;
-  const int32_t smpB = vB ? a.sampled[r0 + 33 + lane] : 0;
-  const int32_t root = a.sampled[r0];
-  int32_t cur = -1, na = 0;
-  while (true) {
-    const int32_t sa = __shfl_sync(0xffffffffu, smpA, cur & 31);
-    const int32_t sb = __shfl_sync(0xffffffffu, smpB, cur & 31);
-    const int32_t tau = cur < 0 ? root : (cur < 32 ? sa : sb);
-    if (lane == 0) ctok[w][na] = tau;
-    const unsigned m0 = __ballot_sync(0xffffffffu, vA && parA == cur && tokA == tau);
-    const unsigned m1 = __ballot_sync(0xffffffffu, vB && parB == cur && tokB == tau);
-    const int32_t next = m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : -1);
-    if (next < 0 || na >= B) break;
-    if (lane == 0) acc[w][na] = next;
-    ++na;
-    cur = next;
-  }
-  __syncwarp();
-  int32_t nc = na + 1;
-  const int32_t cap = max(0, a.max_new[s] - t);
-  nc = min(nc, cap);
-  bool hit = false;
-  if (a.eos_id >= 0) {
-    int32_t first = INT_MAX;
-    for (int32_t k = lane; k < nc; k += 32)
-      if (ctok[w][k] == a.eos_id) first = min(first, k);
-    for (int o = 16; o; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    if (first != INT_MAX) { nc = first + 1; hit = true; }
-  }
-  for (int32_t k = lane; k < B + 1; k += 32) {
-    const int32_t v = k < nc ? ctok[w][k] : -1;
-    a.commit_tok[(int64_t)s * (B + 1) + k] = v;
-    if (k < nc) a.seq_tok[(int64_t)s * a.stride + t + k] = v;
-  }
-  for (int32_t k = lane; k < B; k += 32) a.accepted_nodes[db + k] = k < na ? acc[w][k] : -1;
-  if (lane == 0) {
-    a.accept_len[s] = na;
-    a.n_commit[s] = nc;
-    a.seq_len[s] = t + nc;
-    a.finished[s] = (hit || t + nc >= a.max_new[s]) ? 1 : 0;
-  }
+  accept_seq(c, a, result, s, ctok[w], acc[w], lane);
 }
 
 }  // namespace

@@ -192,6 +192,37 @@ class SrtCache:
                                 _ptr(out.finished, torch.uint8), _stream()), "srt_verify")
         return out
 
+    def verify_insert(self, logits, d: DraftOut, seq_id, seed: int, seq_tok, seq_len, max_new,
+                      prompt_id, cursor, floor=None, stats=None, temperature: float = 1.0,
+                      eos_id: int = -1, out: VerifyOut | None = None,
+                      rows: int | None = None) -> VerifyOut:
+        """srt_verify_insert_cursor: verify, then insert each sequence's committed
+        span through its cursor, fused (same results as verify() then
+        insert(..., cursor=cursor) from the old to the new seq_len)."""
+        n = seq_len.shape[0]
+        if logits.dtype != self.logits_dtype:
+            raise SrtError(f"logits dtype {logits.dtype} != cache's {self.logits_dtype}")
+        if logits.shape[-1] != self.V:
+            raise SrtError("logits row length != V")
+        if cursor.shape != (n, self.cfg.max_depth + 4):
+            raise ValueError(f"cursor must be ({n}, D + 4) int32")
+        if out is None:
+            out = VerifyOut.empty(n, logits.shape[0] if rows is None else rows, self.Bmax,
+                                  seq_tok.device)
+        i32 = torch.int32
+        check(self.L.srt_verify_insert_cursor(
+            self._h, n, _ptr(logits, None, "logits"), _ptr(d.row_offsets, torch.int64),
+            _ptr(d.draft_len, i32), _ptr(d.draft_tok, i32), _ptr(d.draft_parent, i32),
+            _ptr(d.draft_depth, i32), _ptr(seq_id, torch.int64, "seq_id"),
+            ctypes.c_uint64(seed & (2 ** 64 - 1)), float(temperature), int(eos_id),
+            _ptr(max_new, i32, "max_new"), _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+            _ptr(seq_len, i32, "seq_len"), _ptr(out.sampled, i32), _ptr(out.accept_len, i32),
+            _ptr(out.n_commit, i32), _ptr(out.commit_tok, i32), _ptr(out.accepted_nodes, i32),
+            _ptr(out.finished, torch.uint8), _ptr(prompt_id, i32, "prompt_id"),
+            _ptr(floor, i32, "floor"), _ptr(cursor, i32, "cursor"),
+            _ptr(stats, torch.int64, "stats"), _stream()), "srt_verify_insert_cursor")
+        return out
+
     # ---- test / inspection support -----------------------------------------
     def sample_rows_reference(self, logits, d: DraftOut, seq_len, seq_id, seed: int,
                               temperature: float = 1.0, out=None) -> torch.Tensor:

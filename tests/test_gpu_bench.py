@@ -44,6 +44,41 @@ def test_pipelined_groups_match_sequential():
     assert (l1 > wl.t0).all()  # every sequence advanced
 
 
+def test_fused_verify_insert_matches_separate_calls():
+    """srt_verify_insert_cursor (accept + cursor insert fused) leaves exactly
+    what srt_verify then srt_insert_cursor leave: sequence tables, commits,
+    sampled tokens, trees, cursors and the next drafts."""
+    import torch
+    import bench
+    cfg = dict(bench.CONFIGS["grpo"])
+    cfg.update(prompts=6, active=48, V=5000, cap=1024, act_cap=1024, median=300,
+               node_capacity=1 << 20)
+    out = []
+    for fused in (False, True):
+        wl = bench.Workload(cfg, 2)
+        run = bench.GpuRun(wl, "bf16", "rl-mix", 2)
+        gr = run.groups[0]
+        gr.fused = fused
+        rec = []
+        for k in range(6):
+            run.step(bench.step_seed(2, k))
+            R = int(gr.d.row_offsets[-1].item())  # (rows past R are not written)
+            rec.append((gr.v.sampled[:R].cpu().numpy().copy(), gr.v.n_commit.cpu().numpy().copy(),
+                        gr.v.commit_tok.cpu().numpy().copy(), gr.d.draft_tok.cpu().numpy().copy()))
+        torch.cuda.synchronize()
+        assert run.status()[0] == 0
+        out.append((rec, gr.seq_tok.cpu().numpy(), gr.seq_len.cpu().numpy(),
+                    gr.cursor.cpu().numpy(), [gr.cache.dump(p) for p in range(3)]))
+    (ra, ta, la, ca, da), (rb, tb, lb, cb, db) = out
+    for x, y in zip(ra, rb):
+        for u, v in zip(x, y):
+            np.testing.assert_array_equal(u, v)
+    np.testing.assert_array_equal(ta, tb)
+    np.testing.assert_array_equal(la, lb)
+    assert da == db
+    assert (la > 0).all() and sum(int(r[1].sum()) for r in ra) > 48
+
+
 def test_graph_replay_matches_eager():
     """bench.py's CUDA-graph step (draft segment + verify/insert segment
     captured once, replayed) commits exactly what the eager step commits."""
