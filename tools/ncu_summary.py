@@ -30,14 +30,21 @@ def launches(path, tail=None):
         if len(r) <= vi or not r[vi]:
             continue
         agg[kname(r[ki])].append(float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0))
+    setup = {}
     if tail:
-        agg = {k: v[-int(tail):] for k, v in agg.items()}
+        # kernels with fewer launches than the timed steps ran only during setup
+        # (warm-tree build, noise tables): listed apart, not in the shares
+        setup = {k: v for k, v in agg.items() if len(v) < int(tail)}
+        agg = {k: v[-int(tail):] for k, v in agg.items() if len(v) >= int(tail)}
     tot = sum(sum(v) for k, v in agg.items() if k.startswith("k_"))
     print("| kernel | launches | total us | mean us | share of libsrt time |")
     print("|---|---|---|---|---|")
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         share = f"{100 * sum(v) / tot:.1f}%" if k.startswith("k_") else "(torch, bench stand-in)"
         print(f"| {k} | {len(v)} | {sum(v):.1f} | {sum(v) / len(v):.1f} | {share} |")
+    if setup:
+        print("\nSetup-only launches (before the timed steps, excluded above): " +
+              ", ".join(f"{k} x{len(v)} ({sum(v):.0f} us)" for k, v in sorted(setup.items())))
 
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
