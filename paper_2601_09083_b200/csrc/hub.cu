@@ -13,7 +13,7 @@
 // slot (a node listed several times, or two hubs sharing a slot, refresh
 // once), and k_hub_refresh rebuilds each elected list with one CTA: a count
 // threshold first (lane-wise top-2 counts), then every warp keeps a sorted
-// top-K of its share of the children at or above it, warp 0 merges them.
+// top-K of its share of the children at or above it, the lists are merged by rank.
 #include "srt_internal.cuh"
 
 namespace srt {
@@ -190,31 +190,36 @@ k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* wor
     sv[w][lane + 32] = L.v1;
     if (lane == 0) sn[w] = L.size;
     __syncthreads();
-    if (w == 0) {
-      for (int o = 1; o < REFRESH_WARPS; ++o)  // merge the sorted lists (stop at the first loser)
-        for (int i = 0; i < sn[o]; ++i) {
-          const unsigned long long kk = sk[o][i];
-          if (L.size == K && kk <= L.key_at(K - 1)) break;
-          L.insert(kk, sv[o][i], lane, K);
+    // Merge the warps' sorted lists in parallel: an entry's place in the union
+    // is its index in its own list plus the number of larger keys in each of
+    // the others (binary searches in shared memory; keys are unique: one
+    // child each), and the entries that place below K are written there.
+    const size_t e = (size_t)slot * HUB_K;
+    for (int i = lane; i < sn[w]; i += 32) {
+      const unsigned long long kk = sk[w][i];
+      int rank = i;
+      for (int o = 0; o < REFRESH_WARPS; ++o) {
+        if (o == w) continue;
+        int lo = 0, hi = sn[o];
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sk[o][mid] > kk) lo = mid + 1; else hi = mid;
         }
-      const size_t e = (size_t)slot * HUB_K;
-      const int len = L.size;
-      if (lane < len) {
-        c.hub_child[e + lane] = L.v0;
-        c.hub_tok[e + lane] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k0);
-        c.hub_cnt[e + lane] = (uint32_t)(L.k0 >> 32);
+        rank += lo;
       }
-      if (lane + 32 < len) {
-        c.hub_child[e + lane + 32] = L.v1;
-        c.hub_tok[e + lane + 32] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k1);
-        c.hub_cnt[e + lane + 32] = (uint32_t)(L.k1 >> 32);
+      if (rank < K) {
+        c.hub_child[e + rank] = sv[w][i];
+        c.hub_tok[e + rank] = (int32_t)(0xFFFFFFFFu - (uint32_t)kk);
+        c.hub_cnt[e + rank] = (uint32_t)(kk >> 32);
       }
-      if (lane == 0) {
-        c.hub_len[slot] = (uint32_t)len;
-        c.hub_nch[slot] = nch;
-        c.hub_csum[slot] = r.w;
-        c.hub_node[slot] = u;  // (read by later kernels only)
-      }
+    }
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int o = 0; o < REFRESH_WARPS; ++o) tot += sn[o];
+      c.hub_len[slot] = (uint32_t)min(tot, K);
+      c.hub_nch[slot] = nch;
+      c.hub_csum[slot] = r.w;
+      c.hub_node[slot] = u;  // (read by later kernels only)
     }
     __syncthreads();
   }
