@@ -8,6 +8,9 @@
  * One step of the path (reading O14):
  *     srt_draft   -> [policy forward on the drafted rows, outside this library]
  *     srt_verify  -> srt_insert
+ * (srt_draft_cursor / srt_insert_cursor keep per-sequence suffix cursors;
+ * srt_verify_insert_cursor is srt_verify + srt_insert_cursor in one call with
+ * the accept walk and the insert fused.)
  *
  * Conventions common to every call
  * --------------------------------
