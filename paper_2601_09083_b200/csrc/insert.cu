@@ -596,12 +596,17 @@ __device__ __forceinline__ CursorSmem carve_cursor_smem(unsigned char* base, int
 
 // The cursor insertion of sequence s's span [f, t_end) by one warp (prompt p
 // already checked).
-template <int NG>  // depth groups per lane: D <= 32 * NG
+template <int NG, bool MW = false>  // D <= 32 * NG; MW: NG warps per sequence, one group each
 __device__ __forceinline__ void cursor_insert_seq(
     const DevCache& c, const CursorSmem& S, int32_t s, int32_t p, int32_t f, int32_t t_end,
     const int32_t* __restrict__ seq_tok, int64_t stride, const int32_t* __restrict__ floor_,
     int32_t short_max, uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
   const int lane = threadIdx.x & 31;
+  // MW: warp gw of the sequence's NG warps owns depth group gw (S.A is shared
+  // by the warps; logs are per warp), synchronised once per position
+  const int gw = MW ? (int)(threadIdx.x >> 5) : 0;
+  constexpr int NGL = MW ? 1 : NG;  // depth groups per lane
+  constexpr int LSTRIDE = MW ? 32 * NG : 32;
   const int32_t D = c.D;
   uint32_t* cur = cursor + (size_t)s * (D + 4);
   const int32_t fl = floor_ ? floor_[s] : 0;
@@ -624,7 +629,7 @@ __device__ __forceinline__ void cursor_insert_seq(
     S.nlog[0] = S.nlog[1] = S.nlog[2] = 0;
   }
   if (valid) {
-    for (int32_t l = 1 + lane; l <= D; l += 32) {
+    for (int32_t l = 1 + 32 * gw + lane; l <= D; l += LSTRIDE) {
       S.A[l] = cur[4 + l - 1];
       S.fresh[l] = 0;
     }
@@ -632,7 +637,7 @@ __device__ __forceinline__ void cursor_insert_seq(
     // rebuild: A_l for l <= min(D-1, P-floor) by walking y[P-l .. P-1] from the
     // root (creating missing nodes, counting nothing: these windows end < P)
     const int32_t lmax = min(D - 1, P - max(fl, 0));
-    for (int32_t l = 1 + lane; l <= D; l += 32) {
+    for (int32_t l = 1 + 32 * gw + lane; l <= D; l += LSTRIDE) {
       uint32_t u = NONE;
       if (l <= lmax) {
         u = root_id(c, p);
@@ -655,9 +660,9 @@ __device__ __forceinline__ void cursor_insert_seq(
       S.fresh[l] = 0;
     }
   }
-  __syncwarp();
+  if (MW) __syncthreads(); else __syncwarp();
   tp_cur = clock64() - tp0;
-  constexpr int ngroups = NG;
+  constexpr int ngroups = NGL;
   const unsigned long long mask = c.H - 1;
   int32_t ybuf = 0;  // the span's tokens, 32 positions per load (lane i: position j + i)
   for (int32_t j = P; j < t_end; ++j) {
@@ -667,23 +672,23 @@ __device__ __forceinline__ void cursor_insert_seq(
     const bool oov = tk < 0 || tk >= c.V;
     if (oov && lane == 0) set_error(c, SRT_DEV_OOV);
     const int32_t lim = min(D, j - max(fl, 0) + 1);  // windows ending at j start >= floor
-    uint32_t par[NG], hnew[NG], aux[NG];
-    bool act[NG], cre[NG];
-    unsigned long long key[NG];
+    uint32_t par[NGL], hnew[NGL], aux[NGL];
+    bool act[NGL], cre[NGL];
+    unsigned long long key[NGL];
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const int32_t l = 32 * g + lane + 1;
+    for (int g = 0; g < NGL; ++g) {
+      const int32_t l = 32 * (gw + g) + lane + 1;
       par[g] = l <= D ? S.A[l - 1] : NONE;
       act[g] = l <= D && !oov && l <= lim && par[g] < BAD;
       key[g] = act[g] ? edge_key(par[g], (uint32_t)tk) : 0ull;
     }
     const long long tr = clock64();
-    rounds += probe_edges<NG>(c, key, act, hnew, cre, aux);
+    rounds += probe_edges<NGL>(c, key, act, hnew, cre, aux);
     // counts (fire and forget) and the batch logs (warp-aggregated appends)
     const long long tc = clock64();
     tp_res += tc - tr;
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
+    for (int g = 0; g < NGL; ++g) {
       if (g >= ngroups) break;  // (warp-uniform)
       const bool a = act[g];
       const uint32_t h = hnew[g];
@@ -694,7 +699,7 @@ __device__ __forceinline__ void cursor_insert_seq(
         if (cre[g]) c.tok[h] = tk;
         else if (is_slot_word(aux[g])) atomicAdd(&c.scnt[aux[g]], 1u);
       }
-      if (g == 0) {  // shallow parents whose csum changed: their hub lists are rebuilt after the call
+      if (gw + g == 0) {  // shallow parents whose csum changed: their hub lists are rebuilt after the call
         const int32_t l = lane + 1;
         dirty_push(c, S, a && l >= 2 && l <= 1 + HUB_DIRTY_DEPTH, par[g], lane);
       }
@@ -723,15 +728,16 @@ __device__ __forceinline__ void cursor_insert_seq(
     }
     __syncwarp();
     tp_cnt += clock64() - tc;
+    if (MW) __syncthreads();  // every warp has read its parents of this position
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
+    for (int g = 0; g < NGL; ++g) {
       if (g >= ngroups) continue;
-      const int32_t l = 32 * g + lane + 1;
+      const int32_t l = 32 * (gw + g) + lane + 1;
       if (l > D) continue;
       S.A[l] = act[g] ? hnew[g] : NONE;
       S.fresh[l] = act[g] && cre[g];
     }
-    __syncwarp();
+    if (MW) __syncthreads(); else __syncwarp();
     tp_max = max(tp_max, clock64() - tj);
     if (S.nlog[0] > LOGCAP - 32 * MAXG || S.nlog[1] > LOGCAP - 32 * MAXG) cursor_flush(c, S, lane);
   }
@@ -741,8 +747,8 @@ __device__ __forceinline__ void cursor_insert_seq(
     dirty_flush(c, S, lane);
     tp_batch = clock64() - tb;
   }
-  for (int32_t l = 1 + lane; l <= D; l += 32) cur[4 + l - 1] = S.A[l];
-  if (lane == 0) {
+  for (int32_t l = 1 + 32 * gw + lane; l <= D; l += LSTRIDE) cur[4 + l - 1] = S.A[l];
+  if (lane == 0 && gw == 0) {
     cur[0] = tag;
     cur[1] = (uint32_t)t_end;
     cur[2] = (uint32_t)p;
@@ -752,7 +758,7 @@ __device__ __forceinline__ void cursor_insert_seq(
   if (prof) {
     unsigned long long d = created;
     for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    if (lane == 0) {
+    if (lane == 0 && gw == 0) {  // (MW: warp 0's part)
       long long* o = prof + 8 * (int64_t)s;
       o[0] = clock64() - tp0;
       o[1] = tp_cur;
@@ -773,7 +779,7 @@ __device__ __forceinline__ void cursor_insert_seq(
     if (lane == 0) {
       // window starts the walk kernel would have walked for this span
       const int32_t lo = span_lo(f, fl, D);
-      atomicAdd(&stats->windows, (unsigned long long)(t_end - lo));
+      if (gw == 0) atomicAdd(&stats->windows, (unsigned long long)(t_end - lo));
       atomicAdd(&stats->increments, b);
       if (d) atomicAdd(&stats->nodes_created, d);
     }
@@ -795,6 +801,51 @@ k_insert_cursor(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   const CursorSmem S = carve_cursor_smem(cur_smem, w, c.D);
   cursor_insert_seq<NG>(c, S, s, p, from[s], to[s], seq_tok, stride, floor_, short_max, cursor, tag,
                         stats);
+}
+
+// D > 32: NG warps per sequence (one depth group each), one sequence per CTA.
+template <int NG>
+__global__ void __launch_bounds__(128)
+k_insert_cursor_mw(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
+                   const int32_t* __restrict__ seq_tok, int64_t stride,
+                   const int32_t* __restrict__ from, const int32_t* __restrict__ to,
+                   const int32_t* __restrict__ floor_, int32_t short_max,
+                   uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
+  extern __shared__ __align__(16) unsigned char cur_smem[];
+  const int32_t s = blockIdx.x;
+  if (s >= n) return;
+  const int32_t p = prompt_id[s];
+  if (p < 0 || p >= c.P) return;  // flagged by the plan kernel
+  CursorSmem S = carve_cursor_smem(cur_smem, threadIdx.x >> 5, c.D);
+  S.A = carve_cursor_smem(cur_smem, 0, c.D).A;
+  cursor_insert_seq<NG, true>(c, S, s, p, from[s], to[s], seq_tok, stride, floor_, short_max,
+                              cursor, tag, stats);
+}
+
+template <int NG>
+__global__ void __launch_bounds__(128)
+k_accept_insert_mw(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result,
+                   const int32_t* __restrict__ prompt_id, const int32_t* __restrict__ floor_,
+                   uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats) {
+  extern __shared__ __align__(16) unsigned char cur_smem[];
+  __shared__ int32_t ctok[65];
+  __shared__ int32_t acc[64];
+  const int32_t s = blockIdx.x;
+  if (s >= a.n) return;
+  const int32_t t = a.seq_len[s];
+  __syncthreads();
+  if (threadIdx.x < 32) accept_seq(c, a, result, s, ctok, acc, threadIdx.x);
+  __syncthreads();
+  const int32_t t_end = a.seq_len[s];
+  const int32_t p = prompt_id[s];
+  if (p < 0 || p >= c.P) {
+    if (threadIdx.x == 0) set_error(c, SRT_DEV_BAD_PROMPT);
+    return;
+  }
+  CursorSmem S = carve_cursor_smem(cur_smem, threadIdx.x >> 5, c.D);
+  S.A = carve_cursor_smem(cur_smem, 0, c.D).A;
+  cursor_insert_seq<NG, true>(c, S, s, p, t, t_end, a.seq_tok, a.stride, floor_, INT_MAX, cursor,
+                              tag, stats);
 }
 
 // Fused accept + cursor insert (srt_verify_insert_cursor): each warp commits
@@ -1034,10 +1085,20 @@ cudaError_t launch_accept_insert(const DevCache& c, const VerifyArgs& a,
                                  const unsigned long long* result, const int32_t* prompt_id,
                                  const int32_t* floor_, uint32_t* cursor, uint32_t tag,
                                  srt_insert_stats* stats, cudaStream_t stream) {
-  const size_t smem = insert_cursor_smem(c.D);
   const int ng = (c.D + 31) >> 5;
-  auto kern = ng <= 1 ? k_accept_insert<1> : ng == 2 ? k_accept_insert<2>
-            : ng == 3 ? k_accept_insert<3> : k_accept_insert<4>;
+  if (ng >= 2) {  // one sequence per CTA, one warp per depth group
+    const size_t smem = (size_t)ng * cursor_warp_bytes(c.D);
+    auto kern = ng == 2 ? k_accept_insert_mw<2> : ng == 3 ? k_accept_insert_mw<3>
+                                                          : k_accept_insert_mw<4>;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<a.n, ng * 32, smem, stream>>>(c, a, result, prompt_id, floor_, cursor, tag, stats);
+    return cudaGetLastError();
+  }
+  const size_t smem = insert_cursor_smem(c.D);
+  auto kern = k_accept_insert<1>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1052,10 +1113,21 @@ cudaError_t launch_insert_cursor(const DevCache& c, int32_t n, const int32_t* pr
                                  const int32_t* to, const int32_t* floor_, int32_t short_max,
                                  uint32_t* cursor, uint32_t tag, srt_insert_stats* stats,
                                  cudaStream_t stream) {
-  const size_t smem = insert_cursor_smem(c.D);
   const int ng = (c.D + 31) >> 5;
-  auto kern = ng <= 1 ? k_insert_cursor<1> : ng == 2 ? k_insert_cursor<2>
-            : ng == 3 ? k_insert_cursor<3> : k_insert_cursor<4>;
+  if (ng >= 2) {  // one sequence per CTA, one warp per depth group
+    const size_t smem = (size_t)ng * cursor_warp_bytes(c.D);
+    auto kern = ng == 2 ? k_insert_cursor_mw<2> : ng == 3 ? k_insert_cursor_mw<3>
+                                                          : k_insert_cursor_mw<4>;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<n, ng * 32, smem, stream>>>(c, n, prompt_id, seq_tok, stride, from, to, floor_,
+                                       short_max, cursor, tag, stats);
+    return cudaGetLastError();
+  }
+  const size_t smem = insert_cursor_smem(c.D);
+  auto kern = k_insert_cursor<1>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
