@@ -15,9 +15,11 @@ Timing: CUDA events on the launching stream around the draft segment and the
 verify+insert segment of every step (the forward stand-in between them is
 excluded), barrier + synchronize on both sides, max over ranks.  Per-kernel
 device times come from libsrt's own event pairs (srt_profile_*).
-N > 1 (torchrun): prompts are hash-sharded (owner(p) = splitmix64(p) mod N),
-each rank decodes the sequences of the prompts it owns (weak scaling: 1024
-sequences per rank); there is no data-path collective in this placement.
+N > 1: prompts are hash-sharded (owner(p) = splitmix64(p) mod N) and each
+rank decodes a contiguous block of 1024 sequences (weak scaling); every step
+the owners' drafts go back to the decoding ranks (all-to-all of draft
+records) and the committed spans go to the owners (NCCL all-gather of span
+records) before insertion.
 `--impl reference` times the CPU oracle on a bounded sample of the same
 workload (rank 0 only).
 """
@@ -717,6 +719,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-prompts", type=int, default=0, help="oracle sample size in prompts")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--parity-rows", type=int, default=1024,
+                    help="rows of the last timed step the oracle re-samples after the run "
+                         "(tie-break divergence count; 0 = off)")
     ap.add_argument("--sharded", action="store_true",
                     help="N=1: run the multi-GPU exchange path (owner draft, draft return, span "
                          "all-gather) on one rank")
@@ -745,12 +750,17 @@ def main():
         wl = Workload(cfg, args.seed)
         npr = args.cpu_prompts or max(1, min(cfg["prompts"], 64 // cfg["samples"]))
         oracle_sample_steps(wl, args.dtype, 1, npr, args.seed)  # warm
+        t_wall = time.perf_counter()
         t_step, n_s, acc = oracle_sample_steps(wl, args.dtype, max(1, args.steps), npr, args.seed)
+        t_wall = time.perf_counter() - t_wall
         frac = n_s / cfg["active"]
         value = frac / t_step
         cores = cpu_cores_used(n_s)
         sample = (f"{n_s} of {cfg['active']} sequences ({npr} prompts) per step, full V rows; "
-                  f"value scaled by {n_s}/{cfg['active']}")
+                  f"value = (sample steps/s) x {n_s}/{cfg['active']}, i.e. extrapolated "
+                  f"linearly in sequences; the sample's measured oracle time is "
+                  f"{t_step:.2f} s per step ({t_wall:.1f} s wall for {max(1, args.steps)} "
+                  f"steps incl. the untimed forward stand-in)")
         print(json.dumps({
             "impl": "reference", "metric": metric, "value": value, "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -758,7 +768,8 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload, "profile": args.profile},
             "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "sample_s_per_step": t_step,
+                             "sample_wall_s": t_wall, "extrapolated": True},
             "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }), flush=True)
@@ -875,6 +886,9 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    psample = None
+    if not pipelined and rank == 0 and args.parity_rows > 0:
+        psample = capture_parity_sample(run, args.parity_rows, args.seed + 12345)
     if pipelined:
         my_ms = float(ev_a.elapsed_time(ev_b))
         tot_log = sum(logs)
@@ -882,13 +896,17 @@ def main():
     else:
         my_ms = float(sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in evs))
     KP = K
+    prof_rows = None
     if use_graph:  # per-kernel breakdown: a profiled eager pass after the timed region
         KP = min(K, 20)
         for gr in run.groups:
             gr.cache.profile_enable(KP * KERNELS_PER_STEP)
-        for _ in range(KP):
+        prof_rows = torch.zeros(KP, dtype=torch.int64, device=run.dev)
+        for k in range(KP):
             run.step(seed)
+            prof_rows[k] = run.d.row_offsets[-1]
         torch.cuda.synchronize()
+        prof_rows = prof_rows.cpu().numpy()
     prof = [x for gr in run.groups for x in gr.cache.profile_read()]
     bits, st = run.status()
     if bits:
@@ -916,8 +934,12 @@ def main():
     # bytes the scan reads: every drafted row (srt_verify) or the sampled ones (srt_verify_path)
     scan_bytes = float((smp if path_mode else rows).sum()) * cfg["V"] * esz
     peak, peak_kind = load_peaks()
-    # per launch: the timed steps' mean bytes over the profiled launches' mean time
-    achieved = (scan_bytes / K) / (float(np.mean(scan_ms)) / 1000.0) / 1e9 if scan_ms else None
+    # per launch: the algorithmic bytes of the SAME launches the per-kernel
+    # times come from (the timed steps in eager mode; the profiled eager
+    # steps, whose rows are logged, in graph mode) over their mean time
+    prof_bytes = (float(np.mean(prof_rows)) * cfg["V"] * esz
+                  if prof_rows is not None and not path_mode else scan_bytes / K)
+    achieved = prof_bytes / (float(np.mean(scan_ms)) / 1000.0) / 1e9 if scan_ms else None
     traffic = traffic_ratio = None
     tf = os.path.join(ROOT, "profiles", f"scan_traffic_{args.config}_{args.dtype}.json")
     if os.path.exists(tf):
@@ -969,7 +991,8 @@ def main():
                                        "(profiles/scan_traffic_*.json; its launch's rows differ "
                                        "from this run's mean)",
                      "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": scan_bytes / K,
+                     "algorithmic_bytes_per_launch": prof_bytes,
+                     "algorithmic_bytes_per_timed_step": scan_bytes / K,
                      "frac_of_8TBps_spec": (achieved / 8000.0) if achieved else None},
         "kernels": kern,
         "tree_stage_us_per_batch": {k: kern[k]["mean_us"] for k in
@@ -985,6 +1008,18 @@ def main():
     cs = clk.summary()
     if cs:
         out["clocks"] = cs
+    if achieved:
+        try:
+            ro = readonly_stream_gbs(run.logits)
+            out["roofline"]["readonly_stream"] = ro
+            out["roofline"]["frac_of_readonly_stream"] = achieved / ro["gbs"]
+        except Exception as e:  # never lose the GPU line over the probe
+            out["roofline"]["readonly_stream"] = {"error": repr(e)[:200]}
+    if psample is not None and not args.no_cpu_baseline:
+        try:
+            out["parity"] = check_parity_sample(psample, seed)
+        except Exception as e:
+            out["parity"] = {"error": repr(e)[:200]}
     if e2e:
         out["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1 and wl is not None:
@@ -1003,6 +1038,73 @@ def main():
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def capture_parity_sample(run, n_rows: int, seed_rows: int):
+    """Right after the timed region: a bounded random sample of the LAST timed
+    step's logits rows with their sampler keys and the GPU's samples (device ->
+    host, untimed).  The oracle checks them later (cpu leg): north_star's
+    tie-break divergence count."""
+    torch = run.torch
+    gr = run.groups[0]
+    total = int(gr.d.row_offsets[-1].item())
+    if total <= 0 or n_rows <= 0:
+        return None
+    rng = np.random.default_rng(seed_rows)
+    pick = np.sort(rng.choice(total, size=min(n_rows, total), replace=False))
+    row_off = gr.d.row_offsets.cpu().numpy()
+    s_of = np.searchsorted(row_off, pick, side="right") - 1
+    j = pick - row_off[s_of]  # 0 = root row, else draft node j - 1
+    depth = gr.d.draft_depth.cpu().numpy()
+    t_before = gr.t_before.cpu().numpy()
+    pos = t_before[s_of] + np.where(j == 0, 0, depth[s_of, np.maximum(j - 1, 0)])
+    idx = torch.from_numpy(pick).to(gr.logits.device)
+    rows = gr.logits[idx]
+    if rows.dtype == torch.bfloat16:
+        host = rows.view(torch.int16).cpu().numpy().view(np.uint16)
+    else:
+        host = rows.cpu().numpy()
+    return {"rows": host, "seq_id": gr.seq_id.cpu().numpy().view(np.uint64)[s_of],
+            "pos": pos.astype(np.int32), "gpu": gr.v.sampled[idx].cpu().numpy(),
+            "of_rows": total}
+
+
+def check_parity_sample(ps, seed: int):
+    """The oracle's full-V Gumbel-max on the captured rows (same Philox keys):
+    rows whose maximum z is shared by >= 2 indices (decided by the smallest-
+    index rule) and rows where the GPU differs (north_star: must be 0)."""
+    import oracle
+    t = time.perf_counter()
+    tok, ties, nan = oracle.sample_rows(ps["rows"], seed, ps["seq_id"], ps["pos"])
+    return {"checked_rows": int(len(tok)), "of_rows_in_step": ps["of_rows"],
+            "tie_rows": int(np.count_nonzero(ties >= 2)),
+            "divergent_rows": int(np.count_nonzero(tok != ps["gpu"])),
+            "nan_rows": int(np.count_nonzero(nan)),
+            "oracle_s": round(time.perf_counter() - t, 2),
+            "sample": "random rows of the last timed step, full V, oracle sample_row on the "
+                      "same (seed, sequence, position) keys"}
+
+
+def readonly_stream_gbs(buf) -> dict:
+    """The read-only HBM stream (srt_stream_read: persistent TMA ring, one CTA
+    per SM) over the bench's logits buffer, CUDA events, best of 3 shapes."""
+    import torch
+    import paper_2601_09083_b200 as srt
+    nbytes = buf.numel() * buf.element_size()
+    sink = torch.empty(1, dtype=torch.int64, device=buf.device)
+    best = {"gbs": 0.0}
+    for chunk, nbuf in ((32768, 6), (32768, 4), (16384, 12)):
+        srt.stream_read(buf, chunk, nbuf, 1, sink)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            srt.stream_read(buf, chunk, nbuf, 1, sink)
+        e1.record()
+        torch.cuda.synchronize()
+        gbs = 3 * (nbytes // chunk) * chunk / (e0.elapsed_time(e1) / 1000.0) / 1e9
+        if gbs > best["gbs"]:
+            best = {"gbs": gbs, "chunk": chunk, "stages": nbuf, "bytes": nbytes}
+    return best
 
 
 def e2e_leg(run: GpuRun, args, steps: int):

@@ -36,12 +36,13 @@
  *  - Token ids are int32 in [0, V).  Prompt ids are int32 in [0, P).
  *
  * Data layout in HBM (owned by the cache): a node pool shared by
- * all prompts (node id p is the root of prompt p's tree T_p) as
- * structure-of-arrays (token, count, and a 16-byte record {child count, first
- * child, its token, sum of the children's counts}), an open-addressing edge
- * hash ((parent << 32) | token -> child id and its slot), and a pool of child
- * slots in geometric blocks (4, 4, 8, 16, 32, 64, ... slots) holding children
- * 1.. with their tokens and count mirrors for coalesced enumeration.
+ * all prompts (the root of prompt p's tree T_p, is node H + p) as
+ * structure-of-arrays (token, count, and a 32-byte record {child count, first
+ * child, its token, sum of the children's counts, bases of child blocks 0-3}),
+ * an open-addressing edge hash ((parent << 32) | token; a node's id IS the
+ * index of its edge's hash slot), and a pool of child slots in geometric
+ * blocks (4, 4, 8, 16, 32, 64, ... slots) holding children 1.. with their
+ * tokens and count mirrors for coalesced enumeration.
  */
 #ifndef SRT_H_
 #define SRT_H_
@@ -173,6 +174,10 @@ SRT_API srt_status srt_insert(srt_cache* cache, int32_t n, const int32_t* prompt
  * P = to on return (unchanged if the span inserts nothing).
  */
 #define SRT_CURSOR_WORDS(D) ((D) + 4)
+/* The cursor calls (srt_insert_cursor, srt_verify_insert_cursor) need
+ * cfg.max_depth <= SRT_CURSOR_MAX_DEPTH (SRT_ERR_INVALID_ARG otherwise,
+ * returned before anything is enqueued); srt_insert has no such limit. */
+#define SRT_CURSOR_MAX_DEPTH 128
 SRT_API srt_status srt_insert_cursor(srt_cache* cache, int32_t n, const int32_t* prompt_id,
                              const int32_t* seq_tok, int64_t stride, const int32_t* from,
                              const int32_t* to, const int32_t* floor_, uint32_t* cursor,
@@ -231,9 +236,17 @@ SRT_API srt_status srt_draft_cursor(srt_cache* cache, int32_t n, const int32_t* 
  *  scan    : every logits row r of sequence s (row_offsets from srt_draft;
  *            logits has row_offsets[n] rows of V elements of cfg.logits_dtype)
  *            is sampled by Gumbel-max:  sampled[r] = argmax_v RN32(RN32(x_v/T)
- *            + g_v), smallest v on ties, NaN never chosen, with
- *            g_v = -log_det(-log_det(u)), u = (2(w>>9)+1) 2^-24, w = word (v&3)
- *            of Philox4x32-10(ctr = (v>>2, pos, seq_id lo, hi), key = seed lo, hi),
+ *            + g_v), smallest v on ties, NaN never chosen, where g_v is the
+ *            block construction of reading O11: per block b of
+ *            64 tokens (the last may be shorter, n_b), Philox4x32-10(ctr =
+ *            (0x80000000 | b>>1, pos, seq_id lo, hi), key = (seed lo, hi))
+ *            gives words (wa, wb) (words 0,1 for even b, 2,3 for odd b);
+ *            E_b = RN(-log_det(u(wa)) / n_b), G_b = -log_det(E_b) is the
+ *            block's maximum noise, at offset (wb * n_b) >> 32; every other
+ *            v gets g_v = min(G_b, -log_det(RN(E_b + A_v))), A_v =
+ *            -log_det(u(w_v)), w_v = word (v&3) of Philox4x32-10(ctr = (v>>2,
+ *            pos, seq_id lo, hi)), u(w) = (2(w>>9)+1) 2^-24 -- i.e. n_b iid
+ *            Gumbel(0,1) draws, the block maximum drawn first (top-down).
  *            pos = seq_len[s] for the root row, seq_len[s] + draft_depth for a
  *            node row.  T == 1 skips the division.  T must be > 0.
  *  walk    : from the root, accept the draft child whose token equals the
@@ -304,15 +317,19 @@ SRT_API srt_status srt_verify_path(srt_cache* cache, int32_t n, int32_t path_rou
 /*
  * srt_verify_insert_cursor — srt_verify followed by srt_insert_cursor of the
  * committed spans, with the accept walk and the insert fused into one kernel
- * (one warp per sequence commits its tokens, and inserts the windows
- * ending at them through its cursor right away, "updated online";
- * DESIGN.md §5 f1).  Arguments: those of srt_verify, then prompt_id[n] (the
- * tree each sequence inserts into), floor[n] (nullable, as srt_insert),
- * cursor[n][D + 4] and stats (nullable), as srt_insert_cursor; the span of
- * sequence s is [seq_len_before, seq_len_after) — every span goes through
- * the cursor (at most Bmax + 1 tokens).  Results are identical to srt_verify
- * then srt_insert_cursor(from = the old seq_len, to = the new one): the same
- * outputs, trees, cursors and hub-list refresh.  Errors as both calls.
+ * (per sequence, one warp -- D <= 32 -- or one CTA of ceil(D/32) warps, one
+ * per depth group, commits its tokens, and inserts the windows ending
+ * at them through its cursor right away, "updated online"; DESIGN.md
+ * §5 f1).  Arguments: those of srt_verify, then prompt_id[n] (the tree each
+ * sequence inserts into), floor[n] (nullable, as srt_insert), cursor[n][D + 4]
+ * and stats (nullable), as srt_insert_cursor; the span of sequence s is
+ * [seq_len_before, seq_len_after) -- every span goes through the cursor (at
+ * most Bmax + 1 tokens, even when that exceeds D).  Results are identical to
+ * srt_verify then srt_insert_cursor(from = the old seq_len, to = the new
+ * one): the same outputs, trees and hub-list refresh, and the same cursors
+ * except for a span longer than D, after which srt_insert_cursor (walk path)
+ * leaves the record invalid while this call keeps it valid at the new length.
+ * D <= SRT_CURSOR_MAX_DEPTH.  Errors as both calls.
  */
 SRT_API srt_status srt_verify_insert_cursor(
     srt_cache* cache, int32_t n, const void* logits, const int64_t* row_offsets,
@@ -406,11 +423,44 @@ SRT_API srt_status srt_cache_clear_errors(srt_cache* cache, void* stream);
 
 /*
  * srt_noise_table — test support: out[r] = g(r) = -log_det(-log_det((2r+1) 2^-24))
- * for all r in [0, 2^23) (DEVICE pointer, 2^23 floats), computed by the same
- * device code srt_verify uses.  Lets a test compare the whole noise domain
- * bitwise with the oracle (pin P9).
+ * for all r in [0, 2^23) (DEVICE pointer, 2^23 floats): the plain per-word
+ * Gumbel transform of O12 (the scan's noise is the block construction below,
+ * srt_row_noise; this table is the bucket bound input of the block maxima).
  */
 SRT_API srt_status srt_noise_table(float* out, void* stream);
+
+/*
+ * srt_log_det_range — test support: out[i] = log_det(x_i) for the n floats
+ * whose bit patterns are first_bits, first_bits + 1, ... (DEVICE out, n
+ * floats), with the device log_det every noise value goes through (reading
+ * O12).  Lets a test compare log_det with the oracle's over
+ * every positive normal float.  SRT_ERR_INVALID_ARG if the range passes 2^32.
+ */
+SRT_API srt_status srt_log_det_range(uint32_t first_bits, int64_t n, float* out, void* stream);
+
+/*
+ * srt_row_noise — test support: the sampler's noise g_v for every token v of
+ * n row keys (reading O11, the top-down block construction): out[k*V + v] =
+ * g_v for key (seed, seq_id[k], pos[k]) (DEVICE pointers; out has n*V
+ * floats), computed by the device functions srt_verify's scan evaluates.
+ * Lets a test compare every element's noise with the oracle bit for bit.
+ */
+SRT_API srt_status srt_row_noise(int32_t vocab_size, uint64_t seed, int32_t n,
+                                 const uint64_t* seq_id, const int32_t* pos, float* out,
+                                 void* stream);
+
+/*
+ * srt_stream_read — measurement support (not on the path): read the first
+ * floor(bytes / chunk) * chunk bytes of the DEVICE buffer `buf` once through
+ * shared memory (persistent kernel, ctas_per_sm CTAs per SM, nbuf stages of
+ * chunk bytes, 1-D TMA bulk copies, L2 evict_first) and discard them; sink
+ * is a DEVICE word it may write.  Timed by the caller with CUDA events, it is
+ * the read-only HBM stream the verify scan is compared with.
+ * SRT_ERR_INVALID_ARG unless chunk is a multiple of 1 KB and the stages fit
+ * in 227 KB of shared memory per SM.
+ */
+SRT_API srt_status srt_stream_read(const void* buf, int64_t bytes, int32_t chunk, int32_t nbuf,
+                                   int32_t ctas_per_sm, void* sink, void* stream);
 
 /*
  * srt_sample_rows_reference — test support: the UNPRUNED scan (every element's

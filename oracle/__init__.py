@@ -28,7 +28,7 @@ _SRC = _HERE / "srt_oracle.cpp"
 _LIB = _HERE / "liboracle.so"
 
 __all__ = ["build", "lib", "Oracle", "philox4x32_10", "log_det", "gumbel_from_word",
-           "noise_table", "sample_row", "log_det_array"]
+           "noise_table", "sample_row", "log_det_array", "row_noise_many", "sample_rows"]
 
 
 def build(force: bool = False) -> Path:
@@ -68,6 +68,11 @@ def lib():
                                      ctypes.c_uint64, ctypes.c_int32, ctypes.c_float,
                                      ctypes.POINTER(ctypes.c_int)]
         L.orc_sample_row.restype = ctypes.c_int32
+        L.orc_row_noise_many.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, _u64p,
+                                         _i32p, _f32p]
+        L.orc_sample_rows.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int32,
+                                      ctypes.c_uint64, _u64p, _i32p, ctypes.c_float, _i32p, _i32p,
+                                      _i32p]
         L.orc_cache_create.argtypes = [ctypes.c_int32] * 8 + [ctypes.c_double]
         L.orc_cache_create.restype = ctypes.c_void_p
         L.orc_cache_destroy.argtypes = [ctypes.c_void_p]
@@ -83,7 +88,7 @@ def lib():
         L.orc_verify.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int,
                                  _i64p, _i32p, _i32p, _i32p, _i32p, _u64p, ctypes.c_uint64,
                                  ctypes.c_float, ctypes.c_int32, _i32p, _i32p, ctypes.c_int64,
-                                 _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _u8p]
+                                 _i32p, _i32p, _i32p, _i32p, _i32p, _i32p, _u8p, _i32p]
         L.orc_verify.restype = ctypes.c_int
         L.orc_dump.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i32p, _u64p, _i32p, ctypes.c_int64]
         L.orc_dump.restype = ctypes.c_int64
@@ -129,6 +134,30 @@ def row_noise(V: int, seed: int, seq_id: int, pos: int) -> np.ndarray:
     out = np.empty(V, np.float32)
     lib().orc_row_noise(V, seed, seq_id, pos, out)
     return out
+
+
+def row_noise_many(V: int, seed: int, seq_id, pos) -> np.ndarray:
+    """row_noise for n keys at once (OpenMP over keys): [n, V] float32."""
+    seq_id = np.ascontiguousarray(seq_id, np.uint64)
+    pos = np.ascontiguousarray(pos, np.int32)
+    out = np.empty((len(seq_id), V), np.float32)
+    lib().orc_row_noise_many(V, seed, len(seq_id), seq_id, pos, out.reshape(-1))
+    return out
+
+
+def sample_rows(rows: np.ndarray, seed: int, seq_id, pos, temperature: float = 1.0):
+    """sample_row over n rows [n, V] (float32 or bf16 bits as uint16), OpenMP
+    over rows.  Returns (tokens, ties, nan): ties[k] = number of indices whose
+    z equals row k's maximum (>= 2 means the smallest-index rule decided)."""
+    rows = np.ascontiguousarray(rows)
+    n, V = rows.shape
+    tok = np.empty(n, np.int32)
+    ties = np.empty(n, np.int32)
+    nan = np.empty(n, np.int32)
+    lib().orc_sample_rows(rows.ctypes.data, _dtype_code(rows), V, n, seed,
+                          np.ascontiguousarray(seq_id, np.uint64),
+                          np.ascontiguousarray(pos, np.int32), temperature, tok, ties, nan)
+    return tok, ties, nan.astype(bool)
 
 
 def _dtype_code(a: np.ndarray) -> int:
@@ -218,7 +247,8 @@ class Oracle:
         assert logits.shape[0] >= rows and logits.shape[-1] == self.V
         out = dict(sampled=np.zeros(rows, np.int32), accept_len=np.zeros(n, np.int32),
                    n_commit=np.zeros(n, np.int32), commit_tok=np.zeros((n, B + 1), np.int32),
-                   accepted_nodes=np.zeros((n, B), np.int32), finished=np.zeros(n, np.uint8))
+                   accepted_nodes=np.zeros((n, B), np.int32), finished=np.zeros(n, np.uint8),
+                   ties=np.zeros(rows, np.int32))
         nan = lib().orc_verify(self.h, n, logits.ctypes.data, _dtype_code(logits),
                                np.ascontiguousarray(row_offsets, np.int64),
                                np.ascontiguousarray(draft_len, np.int32),
@@ -228,7 +258,8 @@ class Oracle:
                                np.ascontiguousarray(seq_id, np.uint64), seed, temperature, eos_id,
                                np.ascontiguousarray(max_new, np.int32), seq_tok, seq_tok.shape[1],
                                seq_len, out["sampled"], out["accept_len"], out["n_commit"],
-                               out["commit_tok"], out["accepted_nodes"], out["finished"])
+                               out["commit_tok"], out["accepted_nodes"], out["finished"],
+                               out["ties"])
         out["nan_seen"] = bool(nan)
         return out
 

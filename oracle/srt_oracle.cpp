@@ -228,13 +228,16 @@ void row_noise(int64_t V, uint64_t seed, uint64_t seq_id, int32_t pos, float* g)
 //   tau = argmax_v  RN32( RN32(x_v / T) + g_v ),   g_v from row_noise above,
 //   first (smallest) index on ties; NaN logits are not candidates (flagged);
 //   if there is no candidate at all the result is 0.
+// ties (nullable) receives the number of indices whose z equals the maximum
+// (>= 2: a float tie, decided by the smallest-index rule; north_star's tie count).
 int32_t sample_row(const void* row, int dtype, int64_t V, uint64_t seed, uint64_t seq_id,
-                   int32_t pos, float temperature, int* nan_seen) {
+                   int32_t pos, float temperature, int* nan_seen, int32_t* ties = nullptr) {
   std::vector<float> noise((size_t)V);
   row_noise(V, seed, seq_id, pos, noise.data());
   int32_t best = 0;
   float best_z = 0.0f;
   bool have = false;
+  int32_t n_best = 0;
   for (int64_t v = 0; v < V; ++v) {
     const float g = noise[(size_t)v];
     float x = load_logit(row, dtype, v);
@@ -248,8 +251,12 @@ int32_t sample_row(const void* row, int dtype, int64_t V, uint64_t seed, uint64_
       best_z = z;
       best = (int32_t)v;
       have = true;
+      n_best = 1;
+    } else if (z == best_z) {
+      ++n_best;
     }
   }
+  if (ties) *ties = n_best;
   return best;
 }
 
@@ -388,6 +395,29 @@ int32_t orc_sample_row(const void* row, int dtype, int64_t V, uint64_t seed, uin
   return sample_row(row, dtype, V, seed, seq_id, pos, temperature, nan_seen);
 }
 
+// The noise of n row keys (seq_id[k], pos[k]) into out[k*V ...], one key per
+// thread (test support: the element-level GPU comparison).
+void orc_row_noise_many(int64_t V, uint64_t seed, int32_t n, const uint64_t* seq_id,
+                        const int32_t* pos, float* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t k = 0; k < n; ++k) row_noise(V, seed, seq_id[k], pos[k], out + (int64_t)k * V);
+}
+
+// sample_row over n independent rows (rows[k*V ...], key (seq_id[k], pos[k])),
+// one row per thread: tok[k], ties[k] (indices sharing the maximum z), nan[k].
+void orc_sample_rows(const void* rows, int dtype, int64_t V, int32_t n, uint64_t seed,
+                     const uint64_t* seq_id, const int32_t* pos, float temperature, int32_t* tok,
+                     int32_t* ties, int32_t* nan_seen) {
+  const int64_t esz = dtype == 0 ? 2 : 4;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t k = 0; k < n; ++k) {
+    int nan = 0;
+    tok[k] = sample_row((const char*)rows + (int64_t)k * V * esz, dtype, V, seed, seq_id[k], pos[k],
+                        temperature, &nan, &ties[k]);
+    nan_seen[k] = nan;
+  }
+}
+
 void* orc_cache_create(int32_t vocab_size, int32_t max_prompts, int32_t max_depth,
                        int32_t max_match_len, int32_t budget_max, int32_t budget_base,
                        int32_t slope_num, int32_t slope_den, double min_path_score) {
@@ -476,13 +506,15 @@ void orc_draft(void* h, int32_t n, const int32_t* prompt_id, const int32_t* seq_
 // max_new (readings O10, O13).  Appends to the sequence table.
 // Row r = row_offsets[s] is the root of sequence s (position t = seq_len[s]);
 // row row_offsets[s]+1+i is draft node i (position t + draft_depth[i]).
+// ties (nullable): per row, the number of indices sharing the maximum z.
 // Returns 1 if a NaN logit was seen.
 int orc_verify(void* h, int32_t n, const void* logits, int dtype, const int64_t* row_offsets,
                const int32_t* draft_len, const int32_t* draft_tok, const int32_t* draft_parent,
                const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed,
                float temperature, int32_t eos_id, const int32_t* max_new, int32_t* seq_tok,
                int64_t stride, int32_t* seq_len, int32_t* sampled, int32_t* accept_len,
-               int32_t* n_commit, int32_t* commit_tok, int32_t* accepted_nodes, uint8_t* finished) {
+               int32_t* n_commit, int32_t* commit_tok, int32_t* accepted_nodes, uint8_t* finished,
+               int32_t* ties) {
   Cache* c = (Cache*)h;
   const int32_t Bmax = c->cfg.budget_max;
   const int64_t V = c->cfg.vocab_size;
@@ -496,7 +528,9 @@ int orc_verify(void* h, int32_t n, const void* logits, int dtype, const int64_t*
       int32_t pos = t + (i < 0 ? 0 : draft_depth[(int64_t)s * Bmax + i]);
       const char* row = (const char*)logits + r * V * (dtype == 0 ? 2 : 4);
       int nan_seen = 0;
-      sampled[r] = sample_row(row, dtype, V, seed, seq_id[s], pos, temperature, &nan_seen);
+      int32_t nt = 0;
+      sampled[r] = sample_row(row, dtype, V, seed, seq_id[s], pos, temperature, &nan_seen, &nt);
+      if (ties) ties[r] = nt;
       nan_any |= nan_seen;
     }
   }

@@ -23,7 +23,7 @@ SRT_BF16, SRT_F32 = 0, 1
 EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache_destroy",
            "srt_insert", "srt_insert_cursor", "srt_draft", "srt_draft_cursor", "srt_verify", "srt_verify_path", "srt_verify_insert_cursor", "srt_cache_dump",
            "srt_cache_prune", "srt_cache_evict", "srt_cache_load", "srt_cache_status",
-           "srt_cache_clear_errors", "srt_noise_table", "srt_sample_rows_reference",
+           "srt_cache_clear_errors", "srt_noise_table", "srt_log_det_range", "srt_row_noise", "srt_stream_read", "srt_sample_rows_reference",
            "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile", "srt_debug_insert_profile",
            "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
@@ -104,6 +104,9 @@ def load() -> ctypes.CDLL:
                                    ctypes.POINTER(SrtCacheStats), vp]
     L.srt_cache_clear_errors.argtypes = [vp, vp]
     L.srt_noise_table.argtypes = [vp, vp]
+    L.srt_log_det_range.argtypes = [ctypes.c_uint32, i64, vp, vp]
+    L.srt_row_noise.argtypes = [i32, u64, i32, vp, vp, vp, vp]
+    L.srt_stream_read.argtypes = [vp, i64, i32, i32, i32, vp, vp]
     L.srt_sample_rows_reference.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, f32, vp, vp]
     L.srt_profile_enable.argtypes = [vp, i64]
     L.srt_debug_draft_profile.argtypes = [vp]

@@ -8,6 +8,8 @@
 #include <map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "srt_internal.cuh"
 
 using namespace srt;
@@ -46,6 +48,14 @@ srt_status cuda_fail(cudaError_t e, const char* what) {
     cudaError_t e_ = (call);                         \
     if (e_ != cudaSuccess) return cuda_fail(e_, what); \
   } while (0)
+
+// An NVTX range around every public call (visible in nsys / ncu --nvtx
+// timelines; a no-op without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define SRT_NVTX(name) NvtxRange nvtx_range_(name)
 
 bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
@@ -93,6 +103,7 @@ int srt_abi_version(void) { return SRT_ABI_VERSION; }
 const char* srt_error_string(void) { return g_err; }
 
 srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** out) {
+  SRT_NVTX("srt_cache_create");
   if (!out) return SRT_ERR_INVALID_ARG;
   srt_status st = validate(cfg);
   if (st != SRT_OK) return st;
@@ -174,6 +185,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
 }
 
 srt_status srt_cache_destroy(srt_cache* c, void* stream) {
+  SRT_NVTX("srt_cache_destroy");
   if (!c) return SRT_OK;
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   cudaFreeAsync(c->pool, (cudaStream_t)stream);
@@ -235,6 +247,7 @@ srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const 
 srt_status srt_insert(srt_cache* c, int32_t n, const int32_t* prompt_id, const int32_t* seq_tok,
                       int64_t stride, const int32_t* from, const int32_t* to,
                       const int32_t* floor_, srt_insert_stats* stats_dev, void* stream_) {
+  SRT_NVTX("srt_insert");
   if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
   if (!prompt_id || !seq_tok || !from || !to) return SRT_ERR_INVALID_ARG;
@@ -246,9 +259,11 @@ srt_status srt_insert_cursor(srt_cache* c, int32_t n, const int32_t* prompt_id,
                              const int32_t* seq_tok, int64_t stride, const int32_t* from,
                              const int32_t* to, const int32_t* floor_, uint32_t* cursor,
                              srt_insert_stats* stats_dev, void* stream_) {
+  SRT_NVTX("srt_insert_cursor");
   if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
   if (!prompt_id || !seq_tok || !from || !to || !cursor) return SRT_ERR_INVALID_ARG;
+  if (c->cfg.max_depth > SRT_CURSOR_MAX_DEPTH) return SRT_ERR_INVALID_ARG;
   if (insert_cursor_smem(c->cfg.max_depth) > 200 * 1024) return SRT_ERR_INVALID_ARG;
   return insert_impl(c, n, prompt_id, seq_tok, stride, from, to, floor_, cursor, stats_dev,
                      (cudaStream_t)stream_);
@@ -259,6 +274,7 @@ srt_status srt_draft(srt_cache* c, int32_t n, const int32_t* prompt_id, const in
                      int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
                      int32_t* draft_parent, int32_t* draft_depth, int32_t* draft_pos,
                      uint64_t* draft_mask, int64_t* row_offsets, void* stream) {
+  SRT_NVTX("srt_draft");
   return srt_draft_cursor(c, n, prompt_id, seq_tok, stride, seq_len, pos_base, nullptr, match_len,
                           draft_len, draft_tok, draft_parent, draft_depth, draft_pos, draft_mask,
                           row_offsets, stream);
@@ -270,6 +286,7 @@ srt_status srt_draft_cursor(srt_cache* c, int32_t n, const int32_t* prompt_id,
                             int32_t* draft_len, int32_t* draft_tok, int32_t* draft_parent,
                             int32_t* draft_depth, int32_t* draft_pos, uint64_t* draft_mask,
                             int64_t* row_offsets, void* stream) {
+  SRT_NVTX("srt_draft_cursor");
   if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (!row_offsets) return SRT_ERR_INVALID_ARG;
   if (n > 0 && (!prompt_id || !seq_tok || !seq_len || !match_len || !draft_len || !draft_tok ||
@@ -319,6 +336,7 @@ srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t
                       int32_t* sampled, int32_t* accept_len, int32_t* n_commit,
                       int32_t* commit_tok, int32_t* accepted_nodes, uint8_t* finished,
                       void* stream_) {
+  SRT_NVTX("srt_verify");
   if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
@@ -347,6 +365,7 @@ srt_status srt_verify_insert_cursor(
     int32_t* sampled, int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
     int32_t* accepted_nodes, uint8_t* finished, const int32_t* prompt_id, const int32_t* floor_,
     uint32_t* cursor, srt_insert_stats* stats_dev, void* stream_) {
+  SRT_NVTX("srt_verify_insert_cursor");
   if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
@@ -354,6 +373,7 @@ srt_status srt_verify_insert_cursor(
       !seq_id || !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit ||
       !commit_tok || !accepted_nodes || !finished || !prompt_id || !cursor)
     return SRT_ERR_INVALID_ARG;
+  if (c->cfg.max_depth > SRT_CURSOR_MAX_DEPTH) return SRT_ERR_INVALID_ARG;
   if (insert_cursor_smem(c->cfg.max_depth) > 200 * 1024) return SRT_ERR_INVALID_ARG;
   VerifyArgs a{n,       logits,     (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
                draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
@@ -388,6 +408,7 @@ srt_status srt_verify_path(srt_cache* c, int32_t n, int32_t path_rounds, const v
                            int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* sampled,
                            int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
                            int32_t* accepted_nodes, uint8_t* finished, void* stream_) {
+  SRT_NVTX("srt_verify_path");
   if (!c || n < 0 || stride < 0 || path_rounds < 0) return SRT_ERR_INVALID_ARG;
   if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
@@ -436,6 +457,7 @@ srt_status srt_sample_rows_reference(srt_cache* c, int32_t n, const void* logits
                                      const int32_t* seq_len, const uint64_t* seq_id,
                                      uint64_t seed, float temperature, int32_t* sampled,
                                      void* stream) {
+  SRT_NVTX("srt_sample_rows_reference");
   if (!c || n < 0) return SRT_ERR_INVALID_ARG;
   if (!(temperature > 0.0f)) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
@@ -452,6 +474,7 @@ srt_status srt_sample_rows_reference(srt_cache* c, int32_t n, const void* logits
 }
 
 srt_status srt_cache_status(srt_cache* c, uint32_t* bits, srt_cache_stats* stats, void* stream_) {
+  SRT_NVTX("srt_cache_status");
   if (!c) return SRT_ERR_INVALID_ARG;
   cudaStream_t stream = (cudaStream_t)stream_;
   uint32_t h_status = 0;
@@ -491,6 +514,7 @@ uint32_t next_tag(uint32_t tag) {
 
 srt_status srt_cache_prune(srt_cache* c, int32_t p, uint32_t theta, int64_t* removed_out,
                            void* stream_) {
+  SRT_NVTX("srt_cache_prune");
   if (!c || p < -1 || p >= c->cfg.max_prompts) return SRT_ERR_INVALID_ARG;
   cudaStream_t stream = (cudaStream_t)stream_;
   uint32_t bits = 0;
@@ -542,6 +566,7 @@ srt_status srt_cache_prune(srt_cache* c, int32_t p, uint32_t theta, int64_t* rem
 
 srt_status srt_cache_evict(srt_cache* c, int64_t max_nodes, int64_t* removed_out,
                            uint32_t* theta_out, void* stream_) {
+  SRT_NVTX("srt_cache_evict");
   if (!c || max_nodes < 0) return SRT_ERR_INVALID_ARG;
   cudaStream_t stream = (cudaStream_t)stream_;
   constexpr int NB = 1 << 16;  // exact counts below 65535, one bin above
@@ -575,6 +600,7 @@ srt_status srt_cache_evict(srt_cache* c, int64_t max_nodes, int64_t* removed_out
 
 srt_status srt_cache_load(srt_cache* c, int32_t p, const srt_dump_record* recs, int64_t n,
                           void* stream_) {
+  SRT_NVTX("srt_cache_load");
   if (!c || p < 0 || p >= c->cfg.max_prompts || n < 1 || !recs || recs[0].token != -1)
     return SRT_ERR_INVALID_ARG;
   cudaStream_t stream = (cudaStream_t)stream_;
@@ -672,6 +698,7 @@ srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
                            const int32_t* draft_len, const int32_t* draft_tok,
                            const int32_t* draft_parent, const int32_t* draft_depth,
                            const uint64_t* draft_mask, int32_t* records, void* stream) {
+  SRT_NVTX("srt_pack_drafts");
   if (n < 0 || Bmax < 1 || Bmax > 64) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
   if (!match_len || !draft_len || !draft_tok || !draft_parent || !draft_depth || !draft_mask ||
@@ -688,6 +715,7 @@ srt_status srt_unpack_drafts(int32_t n, int32_t Bmax, const int32_t* records, co
                              int32_t* draft_tok, int32_t* draft_parent, int32_t* draft_depth,
                              int32_t* draft_pos, uint64_t* draft_mask, int64_t* row_offsets,
                              void* stream) {
+  SRT_NVTX("srt_unpack_drafts");
   if (n < 0 || Bmax < 1 || Bmax > 64 || !row_offsets) return SRT_ERR_INVALID_ARG;
   if (n > 0 && (!records || !src || !match_len || !draft_len || !draft_tok || !draft_parent ||
                 !draft_depth || !draft_pos || !draft_mask))
@@ -703,6 +731,7 @@ srt_status srt_unpack_drafts(int32_t n, int32_t Bmax, const int32_t* records, co
 
 srt_status srt_pack_spans(int32_t n, int32_t Bmax, const int32_t* n_commit,
                           const int32_t* commit_tok, int32_t* records, void* stream) {
+  SRT_NVTX("srt_pack_spans");
   if (n < 0 || Bmax < 1 || Bmax > 64) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
   if (!n_commit || !commit_tok || !records) return SRT_ERR_INVALID_ARG;
@@ -714,6 +743,7 @@ srt_status srt_pack_spans(int32_t n, int32_t Bmax, const int32_t* n_commit,
 srt_status srt_apply_spans(int32_t n, int32_t Bmax, const int32_t* records, const int32_t* src,
                            int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* from,
                            int32_t* to, void* stream) {
+  SRT_NVTX("srt_apply_spans");
   if (n < 0 || Bmax < 1 || Bmax > 64 || stride < 0) return SRT_ERR_INVALID_ARG;
   if (n == 0) return SRT_OK;
   if (!records || !src || !seq_tok || !seq_len || !from || !to) return SRT_ERR_INVALID_ARG;
@@ -729,8 +759,36 @@ srt_status srt_noise_table(float* out, void* stream) {
   return SRT_OK;
 }
 
+srt_status srt_log_det_range(uint32_t first_bits, int64_t n, float* out, void* stream) {
+  if (!out || n < 0 || (uint64_t)first_bits + (uint64_t)n > (1ull << 32)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  SRT_CUDA(launch_log_det_range(first_bits, n, out, (cudaStream_t)stream), "log_det range");
+  return SRT_OK;
+}
+
+srt_status srt_row_noise(int32_t vocab_size, uint64_t seed, int32_t n, const uint64_t* seq_id,
+                         const int32_t* pos, float* out, void* stream) {
+  if (vocab_size < 2 || n < 0 || (n > 0 && (!seq_id || !pos || !out))) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  SRT_CUDA(launch_row_noise(vocab_size, seed, seq_id, pos, n, out, (cudaStream_t)stream),
+           "row noise");
+  return SRT_OK;
+}
+
+srt_status srt_stream_read(const void* buf, int64_t bytes, int32_t chunk, int32_t nbuf,
+                           int32_t ctas_per_sm, void* sink, void* stream) {
+  if (!buf || !sink || bytes < 0 || chunk < 1024 || chunk % 1024 || nbuf < 1 || ctas_per_sm < 1 ||
+      (int64_t)nbuf * chunk * ctas_per_sm > 227 * 1024)
+    return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(launch_stream_read(buf, bytes, chunk, nbuf, ctas_per_sm, (unsigned long long*)sink,
+                              (cudaStream_t)stream),
+           "stream read");
+  return SRT_OK;
+}
+
 srt_status srt_cache_dump(srt_cache* c, int32_t p, srt_dump_record* host_buf, int64_t cap,
                           int64_t* n_records, void* stream_) {
+  SRT_NVTX("srt_cache_dump");
   if (!c || !n_records || p < 0 || p >= c->cfg.max_prompts || cap < 0) return SRT_ERR_INVALID_ARG;
   cudaStream_t stream = (cudaStream_t)stream_;
   uint32_t bits = 0;

@@ -100,6 +100,56 @@ cudaError_t launch_noise_table(float* out, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// log_det of the floats with bit patterns first, first + 1, ... (test hook:
+// the exhaustive device/oracle comparison of O12 over the positive normals).
+__global__ void k_log_det_range(uint32_t first, int64_t n, float* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = log_det(__uint_as_float(first + (uint32_t)i));
+}
+
+cudaError_t launch_log_det_range(uint32_t first, int64_t n, float* out, cudaStream_t stream) {
+  k_log_det_range<<<num_sms() * 8, 256, 0, stream>>>(first, n, out);
+  return cudaGetLastError();
+}
+
+// g_v of every element of the rows keyed (seq_id[k], pos[k]): the O11 block
+// construction through the same device functions the scan evaluates (one
+// block of 64 tokens per warp-pair of lanes; test hook).
+__global__ void k_row_noise(int32_t V, uint64_t seed, const uint64_t* seq_id, const int32_t* pos,
+                            int32_t nkeys, float* out) {
+  const int64_t nblk = ((int64_t)V + NOISE_BLK - 1) / NOISE_BLK;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nkeys * nblk;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t key = (int32_t)(t / nblk);
+    const int64_t b = t % nblk;
+    const uint64_t sid = seq_id[key];
+    const uint32_t ps = (uint32_t)pos[key], slo = (uint32_t)sid, shi = (uint32_t)(sid >> 32);
+    const int n = block_len(V, b);
+    uint32_t wa, wb;
+    block_words((uint32_t)b, ps, slo, shi, k0, k1, wa, wb);
+    const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+    float* g = out + (int64_t)key * V + b * NOISE_BLK;
+    for (int j = 0; j < n; ++j) {
+      if ((uint32_t)j == bn.p) {
+        g[j] = bn.G;
+        continue;
+      }
+      const int64_t v = b * NOISE_BLK + j;
+      const Philox4 pw = philox4x32_10((uint32_t)(v >> 2), ps, slo, shi, k0, k1);
+      const uint32_t q = (uint32_t)(v & 3);
+      g[j] = element_noise_from_word(q == 0 ? pw.x : q == 1 ? pw.y : q == 2 ? pw.z : pw.w, bn);
+    }
+  }
+}
+
+cudaError_t launch_row_noise(int32_t V, uint64_t seed, const uint64_t* seq_id, const int32_t* pos,
+                             int32_t nkeys, float* out, cudaStream_t stream) {
+  k_row_noise<<<num_sms() * 8, 128, 0, stream>>>(V, seed, seq_id, pos, nkeys, out);
+  return cudaGetLastError();
+}
+
 // One thread per frontier node: emit every child (test path only).  Children
 // k >= 1 are read through their slot mirrors (stok, scnt: what srt_draft
 // enumerates) and checked against the node arrays (tok, cnt).

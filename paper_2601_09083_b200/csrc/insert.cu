@@ -465,7 +465,8 @@ __device__ __forceinline__ void count_created(const DevCache& c, unsigned create
 // ---------------------------------------------------------------------------
 constexpr int CURSOR_WARPS = 4;
 constexpr int LOGCAP = 512;  // logged entries per warp before a batch flush
-constexpr int MAXG = 4;      // depth groups per lane (D <= 128)
+constexpr int MAXG = 4;      // depth groups per lane (D <= 128 = SRT_CURSOR_MAX_DEPTH)
+static_assert(32 * MAXG == SRT_CURSOR_MAX_DEPTH, "cursor depth groups");
 
 // Development-only per-sequence profile (srt_debug_insert_profile): when set,
 // k_insert_cursor writes {total cycles, cursor-phase cycles, positions, nodes
@@ -739,7 +740,13 @@ __device__ __forceinline__ void cursor_insert_seq(
     }
     if (MW) __syncthreads(); else __syncwarp();
     tp_max = max(tp_max, clock64() - tj);
-    if (S.nlog[0] > LOGCAP - 32 * MAXG || S.nlog[1] > LOGCAP - 32 * MAXG) cursor_flush(c, S, lane);
+    // Mid-span flush when a log is nearly full.  MW: the decision is
+    // block-wide, so every warp of the sequence publishes its created nodes
+    // before any of them can spin in the pending loop on another CTA's node
+    // (a per-warp decision could park a creator at the position barrier
+    // while its sibling spins: a cross-CTA wait cycle).
+    const bool over = S.nlog[0] > LOGCAP - 32 * MAXG || S.nlog[1] > LOGCAP - 32 * MAXG;
+    if (MW ? __syncthreads_or(over) : over) cursor_flush(c, S, lane);
   }
   {
     const long long tb = clock64();

@@ -264,7 +264,12 @@ inline void carveout_once() {
 cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream);
 cudaError_t launch_noise_bounds(const DevCache& c, cudaStream_t stream);
 cudaError_t launch_noise_table(float* out, cudaStream_t stream);
+cudaError_t launch_log_det_range(uint32_t first, int64_t n, float* out, cudaStream_t stream);
+cudaError_t launch_row_noise(int32_t V, uint64_t seed, const uint64_t* seq_id, const int32_t* pos,
+                             int32_t nkeys, float* out, cudaStream_t stream);
 int num_sms();
+cudaError_t launch_stream_read(const void* buf, int64_t bytes, int32_t chunk, int32_t nbuf,
+                               int32_t ctas_per_sm, unsigned long long* sink, cudaStream_t stream);
 cudaError_t launch_insert_plan(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                const int32_t* from, const int32_t* to, const int32_t* floor_,
                                int32_t short_max, long long* scratch, cudaStream_t stream);

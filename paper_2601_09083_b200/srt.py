@@ -15,7 +15,7 @@ import torch
 from . import _lib
 from ._lib import SrtCacheStats, SrtConfig, SrtDumpRecord, SrtError, check
 
-__all__ = ["SrtCache", "DraftOut", "VerifyOut", "config", "noise_table", "SrtError",
+__all__ = ["SrtCache", "DraftOut", "VerifyOut", "config", "noise_table", "log_det_range", "row_noise", "stream_read", "SrtError",
            "pack_drafts", "unpack_drafts", "pack_spans", "apply_spans", "draft_record_words",
            "span_record_words"]
 
@@ -358,3 +358,36 @@ def noise_table(device=None) -> torch.Tensor:
     out = torch.empty(1 << 23, dtype=torch.float32, device=device or "cuda")
     check(L.srt_noise_table(_ptr(out, torch.float32, "out"), _stream()), "srt_noise_table")
     return out
+
+
+def log_det_range(first_bits: int, n: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """srt_log_det_range (test hook): log_det of the floats with bit patterns
+    first_bits .. first_bits + n - 1, on the device."""
+    L = _lib.load()
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+    check(L.srt_log_det_range(first_bits, n, _ptr(out[:n], torch.float32, "out"), _stream()),
+          "srt_log_det_range")
+    return out[:n]
+
+
+def row_noise(vocab_size: int, seed: int, seq_id: torch.Tensor, pos: torch.Tensor) -> torch.Tensor:
+    """srt_row_noise (test hook): the sampler's noise g_v, [n, V] float32."""
+    L = _lib.load()
+    n = seq_id.shape[0]
+    out = torch.empty(n, vocab_size, dtype=torch.float32, device=seq_id.device)
+    check(L.srt_row_noise(vocab_size, seed & (2**64 - 1), n, _ptr(seq_id, torch.int64, "seq_id"),
+                          _ptr(pos, torch.int32, "pos"), _ptr(out, torch.float32, "out"),
+                          _stream()), "srt_row_noise")
+    return out
+
+
+def stream_read(buf: torch.Tensor, chunk: int = 32768, nbuf: int = 6, ctas_per_sm: int = 1,
+                sink: torch.Tensor | None = None) -> None:
+    """srt_stream_read (measurement hook): read `buf` once through a TMA ring."""
+    L = _lib.load()
+    if sink is None:
+        sink = torch.empty(1, dtype=torch.int64, device=buf.device)
+    check(L.srt_stream_read(_ptr(buf, None, "buf"), buf.numel() * buf.element_size(), chunk, nbuf,
+                            ctas_per_sm, _ptr(sink, torch.int64, "sink"), _stream()),
+          "srt_stream_read")

@@ -117,6 +117,34 @@ def test_insert_cursor_parity(orc, seed):
         assert plain.dump(p) == pair.gpu.dump(p)
 
 
+@pytest.mark.parametrize("D,V", [(64, 8), (128, 8), (128, 3)])
+def test_insert_cursor_deep_siblings_midspan_flush(orc, D, V):
+    """D > 32 (one CTA of D/32 warps per sequence) with many sibling
+    sequences of the same prompts inserting spans of ~D new positions at once:
+    each warp creates up to 32 nodes per position, so its log passes the
+    mid-span flush threshold after ~12 positions, while siblings on other CTAs
+    wait for each other's node publications (the flush decision is
+    block-wide).  Trees equal the oracle's; the call terminates."""
+    rng = np.random.default_rng(D + V)
+    P, n, T = 2, 64, 4 * D
+    pair = Pair(orc, V, P, D, 8, 8, node_capacity=1 << 20)
+    base = rng.integers(0, V, (P, T)).astype(np.int32)
+    prompt = (np.arange(n) % P).astype(np.int32)
+    # siblings share their prompt's template with 30% substitutions: nodes
+    # created by one CTA are met (pending) by others in the same call
+    toks = np.where(rng.random((n, T)) < 0.3, rng.integers(0, V, (n, T)), base[prompt]).astype(np.int32)
+    cur = pair.gpu.new_cursors(n)
+    pos = np.zeros(n, np.int32)
+    for step in range(4):
+        grow = rng.integers(D - 8, D + 1, n)  # <= D: the cursor path
+        to = np.minimum(pos + grow, T).astype(np.int32)
+        pair.insert(prompt, toks, pos, to, cursor=cur)
+        pos = to
+        pair.compare_trees()
+    bits, _ = pair.gpu.status()
+    assert bits == 0
+
+
 def test_insert_repeat_is_deterministic(orc):
     """Concurrent CAS/atomics: the logical tree is identical across runs."""
     rng = np.random.default_rng(5)
