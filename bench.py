@@ -489,7 +489,8 @@ class ShardedRun:
                  gather=None):
         import torch
         import paper_2601_09083_b200 as srt
-        from paper_2601_09083_b200.dist import GpuOps, ShardPlan, ShardedStep, all_gather_rows
+        from paper_2601_09083_b200.dist import (GpuOps, ShardPlan, ShardedStep, all_gather_rows,
+                                                 all_to_all_rows)
         self.torch = torch
         self.cfg = cfg
         t = time.time()
@@ -588,7 +589,9 @@ class ShardedRun:
         # ---- the exchange
         ops = GpuOps(self.cache, B, self.m_prompt, self.m_tok, self.m_len, self.m_cursor,
                      self.m_draft, self.d, self.seq_len, self.v)
-        self.ex = ShardedStep(plan, rank, ops, gather or all_gather_rows, B, device=dev)
+        a2a = ((lambda t, sc, rc: t[:int(sum(sc))]) if world == 1 and gather is not None
+               else all_to_all_rows)
+        self.ex = ShardedStep(plan, rank, ops, gather or all_gather_rows, B, device=dev, a2a=a2a)
         bits, st = self.cache.status()
         if bits:
             raise RuntimeError(f"cache error bits {bits} after warm-up inserts ({st})")
@@ -628,6 +631,19 @@ class ShardedRun:
 
     def status(self):
         return self.cache.status()
+
+
+def spawn_ranks(n: int) -> int:
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    log(f"[bench] spawning {n} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
 
 
 def owner_of_global(p: int, world: int) -> int:
@@ -736,6 +752,10 @@ def main():
     ap.add_argument("--groups", type=int, default=1,
                     help="prompt groups pipelined on separate streams (1 = sequential; >1 measured slower: the latency-bound tree kernels stall behind the scan's HBM traffic)")
     args = ap.parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        # `bench.py --gpus N` without a launcher: re-run this command under
+        # torchrun, one process per GPU (rank 0 prints the JSON line)
+        sys.exit(spawn_ranks(args.gpus))
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -823,21 +843,27 @@ def main():
     acc_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     com_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     logs = [torch.zeros(3, K, dtype=torch.int64, device=run.dev) for _ in range(G)]
-    use_graph = args.graph and not pipelined and wl is not None and G == 1
+    use_graph = bool(args.graph) and not pipelined and G == 1
     if use_graph:
-        # capture one step's two segments (the stand-in stays eager between them)
+        # capture one step's two segments (the stand-in stays eager between
+        # them); the sharded path's segments include its NCCL collectives
         gr0 = run.groups[0]
-        g_draft, g_vi = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_draft):
-            gr0.draft()
-        with torch.cuda.graph(g_vi):
-            gr0.verify_insert(seed)
-        for _ in range(2):  # graph warm-up steps
-            g_draft.replay()
-            gr0.standin()
-            g_vi.replay()
-        torch.cuda.synchronize()
-    else:
+        try:
+            g_draft, g_vi = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_draft):
+                gr0.draft()
+            with torch.cuda.graph(g_vi):
+                gr0.verify_insert(seed)
+            for _ in range(2):  # graph warm-up steps
+                g_draft.replay()
+                gr0.standin()
+                g_vi.replay()
+            torch.cuda.synchronize()
+        except Exception as e:  # capture unsupported here: time the eager step instead
+            log(f"[bench] CUDA-graph capture failed ({e!r}); timing eager steps")
+            use_graph = False
+            torch.cuda.synchronize()
+    if not use_graph:
         for gr in run.groups:
             gr.cache.profile_enable(K * KERNELS_PER_STEP)
     if world > 1:
@@ -961,8 +987,9 @@ def main():
                          f"{run.logits.numel() * esz / 1e9:.1f} GB)",
                    "groups": G,
                    "placement": ("hash-sharded trees (owner = splitmix64(p) mod N), sequences "
-                                 "decoded on a contiguous split; per step an all-gather of draft "
-                                 "records (draft return) and of span records (before insertion)"
+                                 "decoded on a contiguous split; per step an all-to-all of draft "
+                                 "records (draft return) and an all-gather of span records "
+                                 "(before insertion)"
                                  if (world > 1 or args.sharded) else "single rank"),
                    "timed": (f"whole step loop on the device (CUDA events, {G} prompt groups "
                              f"pipelined on {G} streams); forward stand-in and bookkeeping "

@@ -8,13 +8,17 @@ of the response tokens of p's sequences.  Sequences are decoded where the
 rollout engine puts them: here a contiguous split of the prompt-major batch
 (verl-style), so siblings mostly share a rank, which is usually not owner(p).
 
-One step, per rank r (every collective is a fixed-size all-gather):
-  1. owner side   srt_draft over r's mirror sequences; pack the draft records;
-  2. all-gather   draft records ("draft return");
+One step, per rank r:
+  1. owner side   srt_draft_cursor over r's mirror sequences; pack the draft
+                  records (mirror order = ascending global id, so the records
+                  are already grouped by the rank that decodes them);
+  2. all-to-all   draft records ("draft return"): each owner sends every
+                  decoding rank exactly its sequences' records;
   3. decode side  unpack the records of r's local sequences (+ row offsets);
                   [policy forward on the drafted rows]; srt_verify;
                   pack the committed spans;
-  4. all-gather   span records;
+  4. all-gather   span records (BJ:configs[4], "NCCL all-gather of decoded
+                  spans per step");
   5. owner side   append the spans to r's mirror table; srt_insert_cursor.
 The result is identical to G = 1 (same trees per prompt, same drafts, same
 commits): the G-invariance tests check it.
@@ -59,7 +63,9 @@ class ShardPlan:
     mirror[r]   global ids of the sequences whose prompt rank r owns
     prompts[r]  global prompt ids owned by rank r (sorted); a mirror sequence's
                 prompt index in r's cache is its prompt's position here
-    draft_src[r][i]  row of the gathered draft records holding local[r][i]'s draft
+    draft_send[r][d] records owner r sends to decoding rank d (all-to-all splits)
+    draft_recv[r][o] records decoding rank r receives from owner o
+    draft_src[r][i]  row of rank r's all-to-all receive buffer holding local[r][i]'s draft
     span_src[r][j]   row of the gathered span records holding mirror[r][j]'s span
     """
     world: int
@@ -68,6 +74,8 @@ class ShardPlan:
     mirror: list = field(default_factory=list)
     prompts: list = field(default_factory=list)
     mirror_prompt: list = field(default_factory=list)
+    draft_send: list = field(default_factory=list)
+    draft_recv: list = field(default_factory=list)
     draft_src: list = field(default_factory=list)
     span_src: list = field(default_factory=list)
     n_local_max: int = 0
@@ -98,11 +106,50 @@ class ShardPlan:
             dec_rank[plan.local[r]] = r
             dec_idx[plan.local[r]] = np.arange(len(plan.local[r]))
             own_idx[plan.mirror[r]] = np.arange(len(plan.mirror[r]))
-        plan.draft_src = [(owner[plan.local[r]] * plan.n_mirror_max + own_idx[plan.local[r]])
-                          .astype(np.int32) for r in range(G)]
+        # draft return (all-to-all): owner o's mirror list is ascending in the
+        # global id and every decoding rank holds a contiguous id range, so o
+        # sends rank d the slice of its records whose sequences d decodes, in
+        # ascending id; rank d's receive buffer is those slices in owner order
+        plan.draft_send = [[int(np.count_nonzero(dec_rank[plan.mirror[o]] == d)) for d in range(G)]
+                           for o in range(G)]
+        plan.draft_recv = [[plan.draft_send[o][d] for o in range(G)] for d in range(G)]
+        plan.draft_src = []
+        for d in range(G):
+            loc = plan.local[d]
+            own = owner[loc]
+            base = np.concatenate([[0], np.cumsum(plan.draft_recv[d])])[:-1]
+            rank_in = np.zeros(len(loc), np.int64)
+            for o in range(G):
+                sel = np.nonzero(own == o)[0]  # ascending id within the owner's slice
+                rank_in[sel] = np.arange(len(sel))
+            plan.draft_src.append((base[own] + rank_in).astype(np.int32))
         plan.span_src = [(dec_rank[plan.mirror[r]] * plan.n_local_max + dec_idx[plan.mirror[r]])
                          .astype(np.int32) for r in range(G)]
         return plan
+
+
+def all_to_all_rows(send, send_counts, recv_counts, group=None):
+    """Rows send[sum(send_counts[:d]) : ...] go to rank d; returns the rows
+    received from every rank, in rank order (torch all_to_all_single with
+    uneven splits: NCCL send/recv pairs, graph-capturable)."""
+    import torch
+    import torch.distributed as dist
+    out = torch.empty((int(sum(recv_counts)),) + tuple(send.shape[1:]), dtype=send.dtype,
+                      device=send.device)
+    dist.all_to_all_single(out, send[:int(sum(send_counts))].contiguous(),
+                           output_split_sizes=list(recv_counts),
+                           input_split_sizes=list(send_counts), group=group)
+    return out
+
+
+def virtual_all_to_all(plan: "ShardPlan", sends):
+    """In-process stand-in for all_to_all_rows over G virtual ranks:
+    sends[o] is owner o's send buffer; returns every rank's receive buffer."""
+    import torch
+    G = plan.world
+    offs = [np.concatenate([[0], np.cumsum(plan.draft_send[o])]) for o in range(G)]
+    return [torch.cat([sends[o][int(offs[o][d]):int(offs[o][d + 1])] for o in range(G)])
+            for d in range(G)]
 
 
 def all_gather_rows(t, group=None):
@@ -128,11 +175,15 @@ class ShardedStep:
       ops.apply_and_insert(recv, src) -> None (append to the mirror table, insert)
 
     `gather` concatenates a [rows, W] buffer across ranks (all_gather_rows, or
-    an in-process stand-in for virtual ranks)."""
+    an in-process stand-in for virtual ranks); `a2a(send, send_counts,
+    recv_counts)` is the draft return (all_to_all_rows).  Virtual-rank
+    drivers call the phases (draft_send / draft_recv / commit_send /
+    commit_recv) across the ranks themselves."""
 
-    def __init__(self, plan: ShardPlan, rank: int, ops, gather, Bmax: int, device=None):
+    def __init__(self, plan: ShardPlan, rank: int, ops, gather, Bmax: int, device=None,
+                 a2a=None):
         import torch
-        self.plan, self.rank, self.ops, self.gather = plan, rank, ops, gather
+        self.plan, self.rank, self.ops, self.gather, self.a2a = plan, rank, ops, gather, a2a
         kw = dict(dtype=torch.int32, device=device)
         self.draft_buf = torch.full((plan.n_mirror_max, 2 + 5 * Bmax), -1, **kw)
         self.span_buf = torch.zeros((plan.n_local_max, Bmax + 2), **kw)
@@ -156,8 +207,10 @@ class ShardedStep:
         self.ops.apply_and_insert(recv, self.span_src)
 
     def draft(self):
-        """Steps 1-3a: owner drafts, draft return, local unpack."""
-        self.draft_recv(self.gather(self.draft_send()))
+        """Steps 1-3a: owner drafts, draft return (all-to-all), local unpack."""
+        r = self.rank
+        self.draft_recv(self.a2a(self.draft_send(), self.plan.draft_send[r],
+                                 self.plan.draft_recv[r]))
 
     def commit(self):
         """Steps 3c-5 (after srt_verify): span all-gather, owner append + insert."""
@@ -183,9 +236,9 @@ class GpuOps:
         self.to = torch.zeros(n, dtype=torch.int32, device=mirror_len.device)
 
     def draft_mirror(self):
-        if self.mirror_len.shape[0]:
+        if self.mirror_len.shape[0]:  # the match reads the insert cursors (srt_draft_cursor)
             self.cache.draft(self.mirror_prompt, self.mirror_tok, self.mirror_len, self.mirror_len,
-                             out=self.mirror_draft)
+                             out=self.mirror_draft, cursor=self.mirror_cursor)
 
     def pack_drafts(self, send):
         if self.mirror_len.shape[0]:

@@ -1,7 +1,7 @@
 """Multi-GPU exchange protocol (paper_2601_09083_b200.dist) on
 CPU: world_size 2 over gloo, with the oracle standing in for libsrt's kernels
 (tests only).  Each rank owns the trees of its hash-sharded prompts, drafts
-for their mirrored sequences, returns the drafts by all-gather, verifies its
+for their mirrored sequences, returns the drafts by all-to-all, verifies its
 own contiguous share of the sequences and all-gathers the committed spans to
 the owners.  G-invariance: every rank's committed tokens and owned trees must
 equal a single-process run of the same workload, bit for bit."""
@@ -139,7 +139,7 @@ def _worker(rank, world, port, result_dir):
     import torch
     import torch.distributed as dist
     import oracle
-    from paper_2601_09083_b200.dist import ShardPlan, ShardedStep, all_gather_rows
+    from paper_2601_09083_b200.dist import ShardPlan, ShardedStep, all_gather_rows, all_to_all_rows
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -155,7 +155,7 @@ def _worker(rank, world, port, result_dir):
         ops = OracleOps(o, w, plan, rank, t0, max_new)
         if len(ops.mirror):
             o.insert(ops.mprompt, ops.mtab, np.zeros(len(ops.mirror), np.int32), ops.mlen)
-        step = ShardedStep(plan, rank, ops, all_gather_rows, B)
+        step = ShardedStep(plan, rank, ops, all_gather_rows, B, a2a=all_to_all_rows)
         for k in range(STEPS):
             step.draft()
             ops.verify()
@@ -191,12 +191,17 @@ def test_plan_routing_is_a_bijection():
         assert sorted(np.concatenate(plan.mirror).tolist()) == list(range(S))
         for r in range(G):
             assert all(owner_of(int(seq_prompt[s]), G) == r for s in plan.mirror[r])
-            # the draft of local[r][i] comes from its owner's mirror slot
+            # the draft of local[r][i] comes from its owner's mirror slot: rank
+            # r's all-to-all receive buffer is, owner by owner, the slice of
+            # each owner's mirror records that r decodes
+            recv = []
+            for o in range(G):
+                offs = np.concatenate([[0], np.cumsum(plan.draft_send[o])])
+                recv += list(plan.mirror[o][offs[r]:offs[r + 1]])
+                assert plan.draft_recv[r][o] == plan.draft_send[o][r]
+            assert len(recv) == len(plan.local[r]) == sum(plan.draft_recv[r])
             for i, s in enumerate(plan.local[r]):
-                o = owner_of(int(seq_prompt[s]), G)
-                src = int(plan.draft_src[r][i])
-                assert src // plan.n_mirror_max == o
-                assert plan.mirror[o][src % plan.n_mirror_max] == s
+                assert recv[int(plan.draft_src[r][i])] == s
             for j, s in enumerate(plan.mirror[r]):
                 src = int(plan.span_src[r][j])
                 dr = src // plan.n_local_max

@@ -1,7 +1,7 @@
 """The multi-GPU exchange on the GPU path (libsrt's pack / unpack / apply
 kernels + dist.ShardedStep + dist.GpuOps), with G virtual ranks in one
-process on one GPU: the all-gathers are concatenations of the ranks' send
-buffers.  Every rank's committed tokens and owned trees must equal the
+process on one GPU: the span all-gather is a concatenation of the ranks' send
+buffers and the draft return an in-process all-to-all (dist.virtual_all_to_all).  Every rank's committed tokens and owned trees must equal the
 single-process ORACLE run of tests/test_dist_gloo.py (G-invariance and
 parity at once)."""
 import numpy as np
@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 def test_virtual_ranks_match_oracle(orc, G):
     import torch
     import paper_2601_09083_b200 as srt
-    from paper_2601_09083_b200.dist import GpuOps, ShardPlan, ShardedStep
+    from paper_2601_09083_b200.dist import GpuOps, ShardPlan, ShardedStep, virtual_all_to_all
     ref_tab, ref_len, ref_o, w = T._reference(orc)
     _, t0, max_new = T._workload()
     plan = ShardPlan.build(w.seq_prompt, G)
@@ -53,8 +53,8 @@ def test_virtual_ranks_match_oracle(orc, G):
         st["ex"] = ShardedStep(plan, r, ops, None, B, device=dev)
         ranks.append(st)
     for k in range(T.STEPS):
-        recv = torch.cat([st["ex"].draft_send() for st in ranks])
-        for st in ranks:
+        recvs = virtual_all_to_all(plan, [st["ex"].draft_send() for st in ranks])
+        for st, recv in zip(ranks, recvs):
             st["ex"].draft_recv(recv)
         for r, st in enumerate(ranks):
             d = st["l_draft"]
