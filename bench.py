@@ -44,10 +44,10 @@ CONFIGS = {
                  act_cap=256, prior_epochs=1, node_capacity=1 << 16),
     # BJ:configs[1] (headline)
     "grpo": dict(V=151936, prompts=128, samples=8, active=1024, Bmax=32, D=32, L=8, median=1200,
-                 cap=8192, act_cap=8192, prior_epochs=1, node_capacity=1 << 27),
+                 cap=8192, act_cap=8192, prior_epochs=1, node_capacity=1 << 27, hidden=1536),
     # BJ:configs[3]
     "ppo": dict(V=152064, prompts=256, samples=1, active=256, Bmax=64, D=128, L=16, median=1200,
-                cap=4096, act_cap=4096, prior_epochs=3, node_capacity=1 << 28),
+                cap=4096, act_cap=4096, prior_epochs=3, node_capacity=1 << 28, hidden=3584),
     # BJ:configs[4] per rank: 8 ranks x 256 prompts x 16 samples = 2048 x 16, 4096
     # sequences decoded per rank, trees hash-sharded, span all-gather + draft
     # return every step (run with torchrun --nproc-per-node 8, or --sharded at N=1)
@@ -73,6 +73,74 @@ SEGMENT_KERNELS = {"scan": 2, "hub_refresh": 2}  # segments that launch two kern
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def load_tensor_peak():
+    """Dense bf16 tensor peak: the driver's sustained cuBLAS measurement (the
+    kernel runs inside a long step)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops_sustained"]), "measured (cuBLAS bf16, sustained)"
+    except Exception:
+        return 1400.0, "fallback (sustained)"
+
+
+def lmhead_comparison(run, seed: int, args, reps: int = 5) -> dict:
+    """The fused LM-head verify against the unfused pipeline it replaces, on
+    the last step's drafted rows (state cloned, nothing committed): cuBLAS
+    bf16 GEMM writing [rows, V] logits (torch.matmul) + srt_verify's HBM
+    scan, versus srt_verify_lmhead.  Also a parity check: the fused kernel's
+    debug dump of the logits it sampled from, re-sampled by srt_verify, must
+    give the same tokens on every row."""
+    torch = run.torch
+    gr = run.groups[0]
+    lm = gr.lm
+    rows = int(gr.d.row_offsets[-1].item())
+    H, W = lm["H"], lm["W"]
+    logits = gr.logits[:rows]
+    tok0, len0 = gr.seq_tok.clone(), gr.seq_len.clone()
+
+    def clone_state():
+        return tok0.clone(), len0.clone()
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    t = {"gemm": [], "scan": [], "fused": []}
+    for _ in range(reps + 1):
+        tk, ln = clone_state()
+        ev[0].record()
+        torch.matmul(H[:rows], W.T, out=logits)
+        ev[1].record()
+        gr.cache.verify(gr.logits, gr.d, gr.seq_id, seed, tk, ln, gr.max_new, out=gr.v,
+                        rows=gr.rows_max)
+        ev[2].record()
+        tk, ln = clone_state()
+        gr.cache.verify_lmhead(H, W, gr.d, gr.seq_id, seed, tk, ln, gr.max_new, out=gr.v,
+                               rows=gr.rows_max)
+        ev[3].record()
+        torch.cuda.synchronize()
+        t["gemm"].append(ev[0].elapsed_time(ev[1]))
+        t["scan"].append(ev[1].elapsed_time(ev[2]))
+        t["fused"].append(ev[2].elapsed_time(ev[3]))
+    med = {k: float(np.median(v[1:])) for k, v in t.items()}
+    # parity: the fused kernel's dumped logits through srt_verify
+    tk, ln = clone_state()
+    gr.cache.verify_lmhead(H, W, gr.d, gr.seq_id, seed, tk, ln, gr.max_new, out=gr.v,
+                           rows=gr.rows_max, logits_out=gr.logits)
+    fused_s = gr.v.sampled[:rows].clone()
+    tk, ln = clone_state()
+    gr.cache.verify(gr.logits, gr.d, gr.seq_id, seed, tk, ln, gr.max_new, out=gr.v,
+                    rows=gr.rows_max)
+    div = int((gr.v.sampled[:rows] != fused_s).sum().item())
+    flops = 2.0 * rows * run.V * lm["K"]
+    return {"rows": rows, "cublas_gemm_ms": med["gemm"], "srt_verify_ms": med["scan"],
+            "unfused_ms": med["gemm"] + med["scan"], "fused_ms": med["fused"],
+            "speedup": (med["gemm"] + med["scan"]) / med["fused"],
+            "fused_tflops": flops / (med["fused"] / 1000) / 1e12,
+            "cublas_tflops": flops / (med["gemm"] / 1000) / 1e12,
+            "dump_rescan_divergent_rows": div,
+            "note": "verify only (accept included, insert excluded), state cloned; median of "
+                    f"{reps} after 1 warm-up"}
 
 
 def load_peaks():
@@ -269,6 +337,7 @@ class Group:
         self.offs = offs[row0:row0 + self.rows_max + 1]
         self.profile = profile
         self.flat_logits = self.logits.view(-1)
+        self.lm = None  # --verify lmhead: hidden states + LM-head weight (GpuRun.enable_lmhead)
         self.d = srt.DraftOut.empty(n, B, dev)
         self.v = srt.VerifyOut.empty(n, self.rows_max, B, dev)
         self.slot = torch.arange(B + 1, device=dev, dtype=torch.int64)
@@ -311,6 +380,31 @@ class Group:
         self.flat_logits[idx] = val
         self.t_before.copy_(self.seq_len)
 
+    def standin_lmhead(self):
+        """The forward stand-in of --verify lmhead: each drafted row's final
+        hidden state h_r = z_r + gap_r W[head_r] + sum_k (gap_r - off_rk) W[d_rk]
+        with z_r ~ N(0, 2^2 I) (fixed per row) and W ~ N(0, 1/K): the LM head
+        then yields bulk logits ~ N(0, 2^2), the head at ~gap and 3 distractors
+        below it -- the rl-mix rows of the logits stand-in, produced by the GEMM."""
+        torch = self.torch
+        lm, d, n, B, V = self.lm, self.d, self.n, self.Bmax, self.V
+        depth = torch.cat([torch.zeros(n, 1, dtype=torch.int32, device=self.dev), d.draft_depth],
+                          dim=1).to(torch.int64)
+        pos = torch.minimum(self.seq_len.to(torch.int64)[:, None] + depth, self.truth_last[:, None])
+        head = torch.gather(self.truth, 1, pos).to(torch.int64).reshape(-1)
+        valid = (self.slot[None, :] <= d.draft_len.to(torch.int64)[:, None]).reshape(-1)
+        row = (d.row_offsets[:-1, None] + self.slot[None, :]).reshape(-1)
+        row = torch.where(valid, row, torch.full_like(row, self.rows_max))
+        gap = torch.where(valid, self.gaps[row], torch.zeros_like(self.gaps[row]))
+        W = lm["W"]
+        h = lm["Z"][row].float() + gap[:, None] * W[head].float()
+        off = self.offs[row]
+        for k in range(3):
+            dk = (head + 1 + 7919 * (k + 1) + row * 31) % V
+            h += torch.where(valid, gap - off[:, k], torch.zeros_like(gap))[:, None] * W[dk].float()
+        lm["H"][row] = h.to(torch.bfloat16)
+        self.t_before.copy_(self.seq_len)
+
     def draft(self):
         self.cache.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d,
                          cursor=self.cursor)
@@ -318,7 +412,11 @@ class Group:
     def verify_insert(self, seed: int, logits=None):
         c = self.cache
         lg = self.logits if logits is None else logits
-        if self.fused and self.path_rounds is None:
+        if self.lm is not None and logits is None:  # the LM head fused into the sampler
+            c.verify_lmhead(self.lm["H"], self.lm["W"], self.d, self.seq_id, seed, self.seq_tok,
+                            self.seq_len, self.max_new, prompt_id=self.prompt_id,
+                            cursor=self.cursor, out=self.v, rows=self.rows_max)
+        elif self.fused and self.path_rounds is None:
             c.verify_insert(lg, self.d, self.seq_id, seed, self.seq_tok, self.seq_len, self.max_new,
                             self.prompt_id, self.cursor, out=self.v, rows=self.rows_max)
         else:
@@ -431,6 +529,23 @@ class GpuRun:
         log(f"[bench] device setup {time.time() - t:.1f}s; {G} group(s); tree nodes "
             f"{self.tree_stats['nodes_used']:,} (cap {self.tree_stats['node_capacity']:,}); logits "
             f"{self.logits.numel() * self.logits.element_size() / 1e9:.2f} GB")
+
+    def enable_lmhead(self, K: int, seed: int):
+        """--verify lmhead: a bf16 LM-head weight [V, K] (random init of the
+        configuration's shape, W ~ N(0, 1/K)) and per-row hidden states; the
+        logits buffer is then used only by the unfused comparison."""
+        torch = self.torch
+        gen = torch.Generator(device=self.dev)
+        gen.manual_seed(seed + 4242)
+        W = torch.empty(self.V, K, dtype=torch.bfloat16, device=self.dev)
+        for v0 in range(0, self.V, 16384):
+            W[v0:v0 + 16384].normal_(0.0, 1.0 / K ** 0.5, generator=gen)
+        for gr in self.groups:
+            Z = torch.empty(gr.rows_max + 1, K, dtype=torch.bfloat16, device=self.dev)
+            Z.normal_(0.0, 2.0, generator=gen)
+            gr.lm = {"W": W, "Z": Z, "H": Z.clone(), "K": K}
+            gr.standin = gr.standin_lmhead
+        self.lm_K = K
 
     def __getattr__(self, name):
         # single-group convenience for the development probes (tools/)
@@ -581,6 +696,7 @@ class ShardedRun:
         self.offs = torch.from_numpy(offs.astype(np.float32)).to(dev)
         self.profile = profile
         self.flat_logits = self.logits.view(-1)
+        self.lm = None  # --verify lmhead: hidden states + LM-head weight (GpuRun.enable_lmhead)
         self.d = srt.DraftOut.empty(n, B, dev)
         self.v = srt.VerifyOut.empty(n, self.rows_max, B, dev)
         self.slot = torch.arange(B + 1, device=dev, dtype=torch.int64)
@@ -741,9 +857,11 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="N=1: run the multi-GPU exchange path (owner draft, draft return, span "
                          "all-gather) on one rank")
-    ap.add_argument("--verify", default="full", choices=["full", "path"],
+    ap.add_argument("--verify", default="full", choices=["full", "path", "lmhead"],
                     help="full = srt_verify (every draft row sampled, the headline); path = "
-                         "srt_verify_path (only the accepted path's rows, SURVEY f3b)")
+                         "srt_verify_path (only the accepted path's rows, SURVEY f3b); lmhead = "
+                         "srt_verify_lmhead_insert_cursor (the LM-head GEMM fused with the "
+                         "sampler, SURVEY f3a: the step then includes the LM head)")
     ap.add_argument("--path-rounds", type=int, default=3)
     ap.add_argument("--graph", type=int, default=1,
                     help="1: each step's draft segment and verify+insert segment replay as CUDA "
@@ -819,6 +937,8 @@ def main():
         if args.verify == "path":
             for gr in run.groups:
                 gr.path_rounds = args.path_rounds
+        if args.verify == "lmhead":
+            run.enable_lmhead(cfg.get("hidden", 1536), args.seed)
         G = run.G
     pipelined = G > 1
     K, W = args.steps, args.warmup
@@ -913,7 +1033,7 @@ def main():
     if world > 1:
         dist.barrier()
     psample = None
-    if not pipelined and rank == 0 and args.parity_rows > 0:
+    if not pipelined and rank == 0 and args.parity_rows > 0 and args.verify != "lmhead":
         psample = capture_parity_sample(run, args.parity_rows, args.seed + 12345)
     if pipelined:
         my_ms = float(ev_a.elapsed_time(ev_b))
@@ -1035,6 +1155,27 @@ def main():
     cs = clk.summary()
     if cs:
         out["clocks"] = cs
+    lm_mode = args.verify == "lmhead" and wl is not None
+    if lm_mode:
+        lm_ms = per_kernel.get("lmhead", [])
+        K_h = run.lm_K
+        rows_prof = (float(np.mean(prof_rows)) if prof_rows is not None else float(rows.mean()))
+        flops = 2.0 * rows_prof * cfg["V"] * K_h
+        ach_tf = flops / (float(np.mean(lm_ms)) / 1000.0) / 1e12 if lm_ms else None
+        pk, pk_kind = load_tensor_peak()
+        out["verify"] = ("lmhead: srt_verify_lmhead_insert_cursor (LM-head GEMM on tcgen05 + the "
+                         "Gumbel-max sampler as its epilogue; logits never written)")
+        out["config"]["hidden"] = K_h
+        out["roofline"] = {"bound": "tensor", "kernel": "k_lmhead_sample (+k_rowinfo)",
+                           "achieved": ach_tf, "peak": pk, "unit": "TFLOP/s",
+                           "frac": ach_tf / pk if ach_tf else None, "traffic": None,
+                           "peak_kind": pk_kind,
+                           "algorithmic_flops_per_launch": flops}
+        achieved = None  # (no HBM read-only comparison for this kernel)
+        try:
+            out["lmhead_vs_unfused"] = lmhead_comparison(run, seed, args)
+        except Exception as e:
+            out["lmhead_vs_unfused"] = {"error": repr(e)[:300]}
     if achieved:
         try:
             ro = readonly_stream_gbs(run.logits)
@@ -1143,9 +1284,11 @@ def e2e_leg(run: GpuRun, args, steps: int):
         return None
     seed = step_seed(args.seed, 0)
     rows_max = max(gr.rows_max for gr in run.groups)
-    host = torch.empty(run.logits[:rows_max].shape, dtype=run.logits.dtype, pin_memory=True)
-    host.copy_(run.logits[:rows_max])
-    dev_rows = torch.empty_like(run.logits[:rows_max])
+    lm = run.groups[0].lm if args.verify == "lmhead" else None
+    src = lm["H"] if lm is not None else run.logits
+    host = torch.empty(src[:rows_max].shape, dtype=src.dtype, pin_memory=True)
+    host.copy_(src[:rows_max])
+    dev_rows = lm["H"] if lm is not None else torch.empty_like(run.logits[:rows_max])
     nmax = max(gr.n for gr in run.groups)
     out_n = torch.empty(nmax, dtype=torch.int32).pin_memory()
     out_a = torch.empty(nmax, dtype=torch.int32).pin_memory()
@@ -1165,14 +1308,14 @@ def e2e_leg(run: GpuRun, args, steps: int):
             gr.t_before.copy_(gr.seq_len)
             e[2].record()
             dev_rows[:rows].copy_(host[:rows], non_blocking=True)
-            gr.verify_insert(seed, dev_rows)
+            gr.verify_insert(seed, None if lm is not None else dev_rows)
             out_n[:n].copy_(gr.v.n_commit, non_blocking=True)
             out_a[:n].copy_(gr.v.accept_len, non_blocking=True)
             out_c[:n].copy_(gr.v.commit_tok, non_blocking=True)
             e[3].record()
             torch.cuda.synchronize()
             total_ms += e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3])
-            h2d += rows * run.V * host.element_size()
+            h2d += rows * host.shape[1] * host.element_size()
             d2h += 8 + n * 4 * 2 + n * (run.Bmax + 1) * 4
     return {"value": steps / (total_ms / 1000.0), "unit": "steps/s",
             "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,

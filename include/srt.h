@@ -326,7 +326,8 @@ SRT_API srt_status srt_verify_path(srt_cache* cache, int32_t n, int32_t path_rou
  * [seq_len_before, seq_len_after) -- every span goes through the cursor (at
  * most Bmax + 1 tokens, even when that exceeds D).  Results are identical to
  * srt_verify then srt_insert_cursor(from = the old seq_len, to = the new
- * one): the same outputs, trees and hub-list refresh, and the same cursors
+ * one): the same outputs, trees and hub-list refresh, and cursor records for
+ * the same suffixes
  * except for a span longer than D, after which srt_insert_cursor (walk path)
  * leaves the record invalid while this call keeps it valid at the new length.
  * D <= SRT_CURSOR_MAX_DEPTH.  Errors as both calls.
@@ -339,6 +340,52 @@ SRT_API srt_status srt_verify_insert_cursor(
     int32_t* sampled, int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
     int32_t* accepted_nodes, uint8_t* finished, const int32_t* prompt_id, const int32_t* floor,
     uint32_t* cursor, srt_insert_stats* stats, void* stream);
+
+/*
+ * srt_verify_lmhead — srt_verify without materialised logits (
+ * P:L139 "one decode pass", P:L379 decoding is memory-bandwidth bound): the
+ * logits row r is the LM-head product x_r = hidden[r] . weight^T, computed on
+ * the tensor cores (tcgen05, fp32 accumulation) and rounded to
+ * cfg.logits_dtype (bf16: round-to-nearest-even, as a bf16 LM head stores
+ * it); the sampler of srt_verify (reading O11: the same Gumbel-max, keys,
+ * temperature and tie rule) runs as the GEMM's epilogue on those values, so
+ * the [rows, V] logits never reach HBM.  Outputs and their meaning are
+ * exactly srt_verify's run on the rounded logits.
+ *   hidden      DEVICE bf16 [hidden_rows, hidden_dim], row r = the final
+ *               hidden state of logits row r (rows as srt_draft lays them
+ *               out: row_offsets[n] <= hidden_rows), 16-byte aligned;
+ *   weight      DEVICE bf16 [V, hidden_dim] (the LM head / tied embedding),
+ *               16-byte aligned; hidden_dim a multiple of 8;
+ *   logits_out  nullable DEVICE [row_offsets[n], V] of cfg.logits_dtype: if
+ *               given, the rounded logits the sampler saw are also written
+ *               (test / debug support; it costs the write the fusion saves).
+ * The accumulation order of the tensor-core GEMM is the hardware's, so the
+ * logits themselves match an fp32 reference only to a tolerance; the
+ * sampling is bit-exact given them.  SRT_ERR_INVALID_ARG for a bad shape or
+ * alignment, SRT_ERR_CUDA if the tensor maps cannot be built.
+ */
+SRT_API srt_status srt_verify_lmhead(srt_cache* cache, int32_t n, const void* hidden,
+                                     int64_t hidden_rows, int32_t hidden_dim, const void* weight,
+                                     void* logits_out, const int64_t* row_offsets,
+                                     const int32_t* draft_len, const int32_t* draft_tok,
+                                     const int32_t* draft_parent, const int32_t* draft_depth,
+                                     const uint64_t* seq_id, uint64_t seed, float temperature,
+                                     int32_t eos_id, const int32_t* max_new, int32_t* seq_tok,
+                                     int64_t stride, int32_t* seq_len, int32_t* sampled,
+                                     int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+                                     int32_t* accepted_nodes, uint8_t* finished, void* stream);
+
+/* srt_verify_lmhead + the fused accept and cursor insert of
+ * srt_verify_insert_cursor (same extra arguments, same results). */
+SRT_API srt_status srt_verify_lmhead_insert_cursor(
+    srt_cache* cache, int32_t n, const void* hidden, int64_t hidden_rows, int32_t hidden_dim,
+    const void* weight, void* logits_out, const int64_t* row_offsets, const int32_t* draft_len,
+    const int32_t* draft_tok, const int32_t* draft_parent, const int32_t* draft_depth,
+    const uint64_t* seq_id, uint64_t seed, float temperature, int32_t eos_id,
+    const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* sampled,
+    int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok, int32_t* accepted_nodes,
+    uint8_t* finished, const int32_t* prompt_id, const int32_t* floor, uint32_t* cursor,
+    srt_insert_stats* stats, void* stream);
 
 /* records[s] <- the draft of sequence s < n (srt_draft's outputs). */
 SRT_API srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
@@ -490,7 +537,8 @@ typedef enum {
   SRT_K_ACCEPT = 5,
   SRT_K_INSERT_CURSOR = 6,
   SRT_K_HUB_REFRESH = 7, /* the hub child lists an insert call rebuilds */
-  SRT_K_ACCEPT_INSERT = 8 /* srt_verify_insert_cursor's fused accept + cursor insert */
+  SRT_K_ACCEPT_INSERT = 8, /* srt_verify_insert_cursor's fused accept + cursor insert */
+  SRT_K_LMHEAD = 9         /* srt_verify_lmhead*: row info + the fused LM-head GEMM + sampler */
 } srt_kernel_id;
 
 typedef struct {

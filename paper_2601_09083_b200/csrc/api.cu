@@ -310,7 +310,7 @@ srt_status srt_draft_cursor(srt_cache* c, int32_t n, const int32_t* prompt_id,
 namespace {
 // The verify scan (rows scratch sized without reading row_offsets back: rows
 // <= n * (Bmax + 1)).
-srt_status verify_scan(srt_cache* c, const VerifyArgs& a, cudaStream_t stream) {
+srt_status row_buffers(srt_cache* c, const VerifyArgs& a, cudaStream_t stream) {
   const int64_t rows_max = (int64_t)a.n * (c->cfg.budget_max + 1);
   if (c->row_cap < rows_max) {
     if (c->rowinfo) SRT_CUDA(cudaFreeAsync(c->rowinfo, stream), "cudaFreeAsync(rowinfo)");
@@ -321,12 +321,123 @@ srt_status verify_scan(srt_cache* c, const VerifyArgs& a, cudaStream_t stream) {
              "cudaMallocAsync(result)");
     c->row_cap = cap;
   }
+  return SRT_OK;
+}
+
+srt_status verify_scan(srt_cache* c, const VerifyArgs& a, cudaStream_t stream) {
+  const srt_status bs = row_buffers(c, a, stream);
+  if (bs != SRT_OK) return bs;
   SRT_CUDA(timed(c, SRT_K_SCAN, stream,
                  [&] { return launch_scan(c->dev, a, false, c->rowinfo, c->result, stream); }),
            "verify scan");
   return SRT_OK;
 }
+
+// The fused LM-head GEMM + sampler in place of the scan (rows must fit the
+// hidden-state buffer: row_offsets[n] <= hidden_rows, unchecked on the host).
+srt_status verify_lmhead_scan(srt_cache* c, const VerifyArgs& a, const LmHeadArgs& h,
+                              cudaStream_t stream) {
+  const srt_status bs = row_buffers(c, a, stream);
+  if (bs != SRT_OK) return bs;
+  SRT_CUDA(timed(c, SRT_K_LMHEAD, stream,
+                 [&] {
+                   cudaError_t e = launch_rowinfo(c->dev, a, c->rowinfo, c->result, stream);
+                   if (e != cudaSuccess) return e;
+                   return launch_lmhead_sample(c->dev, a, h, c->rowinfo, c->result, stream);
+                 }),
+           "verify lm-head");
+  return SRT_OK;
+}
+
+srt_status lmhead_args(const srt_cache* c, const void* hidden, int64_t hidden_rows, int32_t K,
+                       const void* weight, void* logits_out, LmHeadArgs* h) {
+  if (!hidden || !weight || hidden_rows < 1 || K < 8 || K % 8 ||
+      (uintptr_t)hidden % 16 || (uintptr_t)weight % 16)
+    return SRT_ERR_INVALID_ARG;
+  *h = LmHeadArgs{hidden, hidden_rows, K, weight, logits_out};
+  return SRT_OK;
+}
 }  // namespace
+
+srt_status srt_verify_lmhead(srt_cache* c, int32_t n, const void* hidden, int64_t hidden_rows,
+                             int32_t hidden_dim, const void* weight, void* logits_out,
+                             const int64_t* row_offsets, const int32_t* draft_len,
+                             const int32_t* draft_tok, const int32_t* draft_parent,
+                             const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed,
+                             float temperature, int32_t eos_id, const int32_t* max_new,
+                             int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* sampled,
+                             int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+                             int32_t* accepted_nodes, uint8_t* finished, void* stream_) {
+  SRT_NVTX("srt_verify_lmhead");
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!row_offsets || !draft_len || !draft_tok || !draft_parent || !draft_depth || !seq_id ||
+      !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit || !commit_tok ||
+      !accepted_nodes || !finished)
+    return SRT_ERR_INVALID_ARG;
+  LmHeadArgs h;
+  srt_status st = lmhead_args(c, hidden, hidden_rows, hidden_dim, weight, logits_out, &h);
+  if (st != SRT_OK) return st;
+  VerifyArgs a{n,       nullptr,    (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
+               draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
+               seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
+               accepted_nodes, finished};
+  cudaStream_t stream = (cudaStream_t)stream_;
+  st = verify_lmhead_scan(c, a, h, stream);
+  if (st != SRT_OK) return st;
+  SRT_CUDA(timed(c, SRT_K_ACCEPT, stream,
+                 [&] { return launch_accept(c->dev, a, c->result, stream); }),
+           "verify accept");
+  return SRT_OK;
+}
+
+srt_status srt_verify_lmhead_insert_cursor(
+    srt_cache* c, int32_t n, const void* hidden, int64_t hidden_rows, int32_t hidden_dim,
+    const void* weight, void* logits_out, const int64_t* row_offsets, const int32_t* draft_len,
+    const int32_t* draft_tok, const int32_t* draft_parent, const int32_t* draft_depth,
+    const uint64_t* seq_id, uint64_t seed, float temperature, int32_t eos_id,
+    const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len, int32_t* sampled,
+    int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok, int32_t* accepted_nodes,
+    uint8_t* finished, const int32_t* prompt_id, const int32_t* floor_, uint32_t* cursor,
+    srt_insert_stats* stats_dev, void* stream_) {
+  SRT_NVTX("srt_verify_lmhead_insert_cursor");
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!row_offsets || !draft_len || !draft_tok || !draft_parent || !draft_depth || !seq_id ||
+      !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit || !commit_tok ||
+      !accepted_nodes || !finished || !prompt_id || !cursor)
+    return SRT_ERR_INVALID_ARG;
+  if (c->cfg.max_depth > SRT_CURSOR_MAX_DEPTH) return SRT_ERR_INVALID_ARG;
+  if (insert_cursor_smem(c->cfg.max_depth) > 200 * 1024) return SRT_ERR_INVALID_ARG;
+  LmHeadArgs h;
+  srt_status st = lmhead_args(c, hidden, hidden_rows, hidden_dim, weight, logits_out, &h);
+  if (st != SRT_OK) return st;
+  VerifyArgs a{n,       nullptr,    (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
+               draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
+               seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
+               accepted_nodes, finished};
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!c->hubwork)
+    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
+             "cudaMallocAsync(hub work)");
+  st = verify_lmhead_scan(c, a, h, stream);
+  if (st != SRT_OK) return st;
+  SRT_CUDA(timed(c, SRT_K_ACCEPT_INSERT, stream,
+                 [&] {
+                   return launch_accept_insert(c->dev, a, c->result, prompt_id, floor_, cursor,
+                                               c->tag, stats_dev, stream);
+                 }),
+           "verify accept + insert");
+  SRT_CUDA(timed(c, SRT_K_HUB_REFRESH, stream,
+                 [&] {
+                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + DIRTY_CAP,
+                                             stream);
+                 }),
+           "hub refresh");
+  return SRT_OK;
+}
 
 srt_status srt_verify(srt_cache* c, int32_t n, const void* logits, const int64_t* row_offsets,
                       const int32_t* draft_len, const int32_t* draft_tok,

@@ -1,0 +1,483 @@
+// lmhead.cu — the verification pass without materialised logits (SURVEY
+// §8(f3a)): the LM-head GEMM logits = hidden · W^T on the 5th-generation tensor
+// cores with the exact Gumbel-max sampler of srt_verify (reading O11) as its
+// epilogue, so the [rows, V] logits never reach HBM.  P:L139 ("one decode
+// pass ... verify multiple drafted tokens in parallel"), P:L379 (decoding is
+// memory-bandwidth bound: the 2 x rows x V x 2 B logits write + read is the
+// traffic this removes).
+//
+// Persistent, warp-specialised, one CTA per SM:
+//  * warp 0, one lane: TMA producer — 2-D tensor-map loads (128-byte swizzle)
+//    of a 128 x 64 hidden tile and a 256 x 64 weight tile per K step into an
+//    NST-stage shared-memory ring (mbarrier full/empty pairs);
+//  * warp 1, one lane: tcgen05.mma issuer — 4 x (M128 N256 K16) bf16 MMAs per
+//    stage into an fp32 accumulator in tensor memory (two 256-column
+//    accumulators: the epilogue of tile i overlaps the MMAs of tile i + 1);
+//    tcgen05.commit frees the stage / publishes the accumulator;
+//  * warps 2-5: epilogue — tcgen05.ld of the thread's row (32x32b: thread =
+//    TMEM lane = logits row), the logit's rounding to the cache's logits
+//    dtype (bf16 RN-even, exactly what a bf16 LM head would store), then the
+//    scan's exact branch and bound per 64-token noise block: block maximum,
+//    bound U_b = RN(max/T) + (bucket bound of G_b), exact z only where a
+//    block can still reach the row's best achieved z (shared across tiles of
+//    the row through result[row], whose packed (z, v) IS an achieved z).
+// Tile order is vocabulary-major (tile t: vocab tile t / num_m, row block
+// t % num_m): the CTAs in flight share one weight tile (L2-resident) and a
+// row's vocabulary tiles run one after another, so its bound only tightens.
+// The result is the argmax of the plain definition over the rounded logits
+// (ties to the smaller index): srt_verify on the dumped logits returns the
+// same bits (tests/test_gpu_lmhead.py).
+#include <cstdio>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "noise.cuh"
+#include "srt_internal.cuh"
+
+namespace srt {
+
+namespace {
+
+constexpr int BM = 128;             // rows per tile (UMMA M, TMEM lanes)
+constexpr int BN = 256;             // vocabulary columns per tile (UMMA N)
+constexpr int BK = 64;              // K per stage: 64 bf16 = one 128-byte swizzle row
+constexpr int UK = 16;              // K per tcgen05.mma (kind::f16)
+constexpr int NST = 4;              // smem ring stages
+constexpr int A_BYTES = BM * BK * 2;             // 16 KB
+constexpr int B_BYTES = BN * BK * 2;             // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 48 KB
+constexpr int EPI_WARPS = 4;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
+constexpr int TMEM_COLS = 2 * BN;   // two accumulators
+constexpr int BLK_PER_TILE = BN / NOISE_BLK;     // 4 noise blocks per tile
+
+// ---- PTX: shared-memory addresses, mbarriers, TMA, tcgen05 ---------------
+__device__ __forceinline__ uint32_t sm32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(sm32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                       int32_t c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sm32(dst)),
+      "l"((uint64_t)map), "r"(sm32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, both K-major (one thread issues)
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on `bar` once every tcgen05 op this thread issued so far completes
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   sm32(bar))
+               : "memory");
+}
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor of a K-major tile in the 128-byte swizzle
+// layout TMA writes (rows of 128 B, 8-row groups 1024 B apart): start >> 4,
+// leading byte offset 16 B (unused by swizzled K-major), stride byte offset
+// 1024 B, version 1 (tcgen05), layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = BM
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ uint64_t ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// the logit as the cache's logits dtype stores it (bf16: RN-even), in fp32
+template <int DT>
+__device__ __forceinline__ float as_logit(float acc) {
+  if (DT == SRT_BF16) return __bfloat162float(__float2bfloat16_rn(acc));
+  return acc;
+}
+
+struct LmParams {
+  int32_t V;
+  int32_t nk;                  // K steps (ceil(K / 64))
+  const int64_t* total;        // -> row_offsets[n]
+  const int2* rowinfo;         // per row: (sequence, position)
+  const uint64_t* seq_id;
+  uint64_t seed;
+  float temperature;
+  unsigned long long* result;  // per row: packed best (z, v), atomicMax
+  void* dump;                  // nullable [rows, V] logits
+};
+
+template <int DT>
+__global__ void __launch_bounds__(THREADS, 1)
+k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                DevCache c, LmParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the swizzled tiles
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* ring = smem;                                        // [NST][A | B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * STAGE_BYTES);
+  uint64_t* empty = full + NST;
+  uint64_t* acc_full = empty + NST;   // [2]
+  uint64_t* acc_empty = acc_full + 2; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* tab = reinterpret_cast<float*>(tmem_slot + 4);              // [NOISE_BUCKETS]
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t total = *p.total;
+  const int32_t num_m = (int32_t)((total + BM - 1) / BM);
+  const int32_t num_n = (p.V + BN - 1) / BN;
+  const int64_t tiles = (int64_t)num_m * num_n;
+
+  for (int i = tid; i < NOISE_BUCKETS; i += blockDim.x) tab[i] = c.gbound[i];
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&acc_full[a], 1);
+      bar_init(&acc_empty[a], EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_b) : "memory");
+  }
+  if (wid == 1) {  // the MMA warp owns the tensor memory
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     sm32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (wid == 0) {
+    // ============ TMA producer ============================================
+    if (lane == 0) {
+      uint64_t pol_a, pol_b;  // hidden rows are re-read for every vocab tile; W once per m
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_b));
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int32_t nt = (int32_t)(t / num_m), mb = (int32_t)(t % num_m);
+        for (int32_t kb = 0; kb < p.nk; ++kb, ++it) {
+          const int s = (int)(it % NST);
+          const uint32_t use = it / NST;
+          if (use > 0) bar_wait(&empty[s], (use - 1) & 1);
+          unsigned char* st = ring + s * STAGE_BYTES;
+          bar_expect_tx(&full[s], STAGE_BYTES);
+          tma_2d(st, &map_a, &full[s], kb * BK, mb * BM, pol_a);
+          tma_2d(st + A_BYTES, &map_b, &full[s], kb * BK, nt * BN, pol_b);
+        }
+      }
+    }
+  } else if (wid == 1) {
+    // ============ MMA issuer ==============================================
+    uint32_t it = 0, u = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++u) {
+      const uint32_t a = u & 1, ause = u >> 1;
+      if (ause > 0) bar_wait(&acc_empty[a], (ause - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + a * BN;
+      for (int32_t kb = 0; kb < p.nk; ++kb, ++it) {
+        const int s = (int)(it % NST);
+        bar_wait(&full[s], (it / NST) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = sm32(ring + s * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)  // +32 bytes per K16 step inside the swizzle row
+            tc_mma(d, sw128_desc(sa + k * UK * 2), sw128_desc(sb + k * UK * 2), IDESC,
+                   (kb | k) != 0);
+          tc_commit(&empty[s]);                    // stage free once these MMAs finish
+          if (kb == p.nk - 1) tc_commit(&acc_full[a]);  // accumulator complete
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ============ epilogue: sample from the accumulator ===================
+    const int q = wid & 3;  // TMEM lane quarter this warp may access
+    const float T = p.temperature;
+    const bool unit_t = T == 1.0f;
+    const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+    const int64_t nblk = ((int64_t)p.V + NOISE_BLK - 1) / NOISE_BLK;
+    uint32_t u = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++u) {
+      const uint32_t a = u & 1;
+      bar_wait(&acc_full[a], (u >> 1) & 1);
+      tc_fence_after();
+      const int32_t nt = (int32_t)(t / num_m), mb = (int32_t)(t % num_m);
+      const int64_t r = (int64_t)mb * BM + q * 32 + lane;
+      const bool rv = r < total;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
+      const int64_t b0 = (int64_t)nt * BLK_PER_TILE;  // first noise block of the tile (even)
+      uint32_t pos = 0, slo = 0, shi = 0;
+      unsigned long long cur = 0;
+      if (rv) {
+        const int2 ri = p.rowinfo[r];
+        const uint64_t sid = p.seq_id[ri.x];
+        pos = (uint32_t)ri.y;
+        slo = (uint32_t)sid;
+        shi = (uint32_t)(sid >> 32);
+        cur = ld_relaxed64(&p.result[r]);
+      }
+      float M = cur ? unpack_value(cur) : -INFINITY;  // an achieved z of the row (or none)
+      // ---- pass A: block maxima (first index of the max), optional dump ----
+      float bmax[BLK_PER_TILE];
+      int32_t barg[BLK_PER_TILE];
+      bool nan = false;
+#pragma unroll
+      for (int j = 0; j < BLK_PER_TILE; ++j) {
+        const int n = block_len(p.V, b0 + j);
+        float x[NOISE_BLK];
+        tmem_ld32(taddr + j * NOISE_BLK, x);
+        tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
+        float m = -INFINITY;
+        int32_t am = -1;
+#pragma unroll
+        for (int k = 0; k < NOISE_BLK; ++k) {
+          x[k] = as_logit<DT>(x[k]);
+          if (k < n) {
+            nan |= x[k] != x[k];
+            if (x[k] > m || (am < 0 && x[k] == m)) { m = x[k]; am = k; }
+          }
+        }
+        bmax[j] = m;
+        barg[j] = am;
+        if (p.dump && rv && n > 0) {
+          const int64_t v0 = (b0 + j) * NOISE_BLK;
+          if (DT == SRT_BF16) {
+            __nv_bfloat16* o = (__nv_bfloat16*)p.dump + r * (int64_t)p.V + v0;
+#pragma unroll
+            for (int k = 0; k < NOISE_BLK; ++k)
+              if (k < n) o[k] = __float2bfloat16_rn(x[k]);
+          } else {
+            float* o = (float*)p.dump + r * (int64_t)p.V + v0;
+#pragma unroll
+            for (int k = 0; k < NOISE_BLK; ++k)
+              if (k < n) o[k] = x[k];
+          }
+        }
+      }
+      // ---- the blocks' words and bounds U_b (one Philox per block pair) ----
+      uint32_t wa[BLK_PER_TILE], wb[BLK_PER_TILE];
+      float U[BLK_PER_TILE];
+#pragma unroll
+      for (int pp = 0; pp < BLK_PER_TILE / 2; ++pp) {
+        const int64_t bp = b0 + 2 * pp;
+        Philox4 w{0, 0, 0, 0};
+        if (rv && bp < nblk)
+          w = philox4x32_10(0x80000000u | (uint32_t)(bp >> 1), pos, slo, shi, k0, k1);
+        wa[2 * pp] = w.x;
+        wb[2 * pp] = w.y;
+        wa[2 * pp + 1] = w.z;
+        wb[2 * pp + 1] = w.w;
+      }
+#pragma unroll
+      for (int j = 0; j < BLK_PER_TILE; ++j) {
+        const int n = block_len(p.V, b0 + j);
+        if (!rv || n == 0 || barg[j] < 0) {
+          U[j] = -INFINITY;
+          continue;
+        }
+        const float xs = unit_t ? bmax[j] : __fdiv_rn(bmax[j], T);
+        const float G = n == NOISE_BLK ? tab[wa[j] >> 22] : block_noise(wa[j], wb[j], (uint32_t)n).G;
+        U[j] = __fadd_rn(xs, G);
+      }
+      // ---- the tile's best candidate: z of the block with the largest bound's
+      // maximum first (an exact achieved z), then every block that can still
+      // reach the row's best ----
+      float bz = -INFINITY;
+      int32_t bv = INT_MAX;
+      int jf = 0;
+#pragma unroll
+      for (int j = 1; j < BLK_PER_TILE; ++j)
+        if (U[j] > U[jf]) jf = j;
+      auto block_of = [&](int j, BlockNoise& bn) {
+        bn = block_noise(wa[j], wb[j], (uint32_t)block_len(p.V, b0 + j));
+      };
+      auto elem_g = [&](int64_t v, int32_t k, const BlockNoise& bn) {
+        if ((uint32_t)k == bn.p) return bn.G;
+        const Philox4 w = philox4x32_10((uint32_t)(v >> 2), pos, slo, shi, k0, k1);
+        const uint32_t e = (uint32_t)(v & 3);
+        return element_noise_from_word(e == 0 ? w.x : e == 1 ? w.y : e == 2 ? w.z : w.w, bn);
+      };
+      // z(i*) of block jf's maximum (exact): seeds M on a row's first tiles
+      if (rv && U[jf] >= M && U[jf] > -INFINITY) {
+        BlockNoise bn;
+        block_of(jf, bn);
+        const int64_t v = (b0 + jf) * NOISE_BLK + barg[jf];
+        const float xs = unit_t ? bmax[jf] : __fdiv_rn(bmax[jf], T);
+        const float z = __fadd_rn(xs, elem_g(v, barg[jf], bn));
+        if (cand_better(z, (int32_t)v, bz, bv)) { bz = z; bv = (int32_t)v; }
+        M = fmaxf(M, z);
+      }
+      // exact evaluation of block j (the thread's own row): every element
+      // whose RN(x/T) + G_b can reach M; x re-read from tensor memory
+#pragma unroll 1
+      for (int round = 0; round < 2; ++round) {
+#pragma unroll 1
+        for (int j = 0; j < BLK_PER_TILE; ++j) {
+          const bool need = rv && (round == 0 ? j == jf : j != jf) && U[j] >= M &&
+                            U[j] > -INFINITY;
+          if (!__any_sync(0xffffffffu, need)) continue;
+          float x[NOISE_BLK];
+          tmem_ld32(taddr + j * NOISE_BLK, x);
+          tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
+          if (!need) continue;
+          const int n = block_len(p.V, b0 + j);
+          BlockNoise bn;
+          block_of(j, bn);
+          uint64_t cand = 0;  // bit k: element k can reach M
+#pragma unroll
+          for (int k = 0; k < NOISE_BLK; ++k) {
+            x[k] = as_logit<DT>(x[k]);
+            const float xs = unit_t ? x[k] : __fdiv_rn(x[k], T);
+            if (k < n && __fadd_rn(xs, bn.G) >= M) cand |= 1ull << k;  // (NaN fails)
+          }
+          while (cand) {
+            const int32_t k = __ffsll((long long)cand) - 1;
+            cand &= cand - 1;
+            float xk = 0.0f;
+#pragma unroll
+            for (int i = 0; i < NOISE_BLK; ++i)
+              if (i == k) xk = x[i];
+            const float xs = unit_t ? xk : __fdiv_rn(xk, T);
+            if (__fadd_rn(xs, bn.G) < M) continue;  // M rose meanwhile
+            const int64_t v = (b0 + j) * NOISE_BLK + k;
+            const float z = __fadd_rn(xs, elem_g(v, k, bn));
+            if (cand_better(z, (int32_t)v, bz, bv)) {
+              bz = z;
+              bv = (int32_t)v;
+              M = fmaxf(M, z);
+            }
+          }
+        }
+      }
+      // the accumulator may be overwritten once every epilogue warp is done
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(&acc_empty[a]);
+      if (__any_sync(0xffffffffu, nan) && lane == 0) set_error(c, SRT_DEV_NONFINITE_LOGIT);
+      if (rv && bv != INT_MAX) {
+        const unsigned long long pk = pack_cand(bz, bv);
+        if (pk > cur) atomicMax(&p.result[r], pk);
+      }
+    }
+  }
+  __syncthreads();
+  if (wid == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, K] matrix, box [box_rows, 64],
+// 128-byte swizzle (the UMMA K-major SW128 layout); out-of-range reads are 0
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int32_t K, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const LmHeadArgs& h,
+                                 const int2* rowinfo, unsigned long long* result,
+                                 cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, h.hidden, h.hidden_rows, h.K, BM) || !make_map(&mb, h.weight, c.V, h.K, BN))
+    return cudaErrorInvalidValue;
+  LmParams p;
+  p.V = c.V;
+  p.nk = (h.K + BK - 1) / BK;
+  p.total = a.row_offsets + a.n;
+  p.rowinfo = rowinfo;
+  p.seq_id = a.seq_id;
+  p.seed = a.seed;
+  p.temperature = a.temperature;
+  p.result = result;
+  p.dump = h.dump;
+  const size_t smem = 1024 + (size_t)NST * STAGE_BYTES + 2 * NST * 8 + 4 * 8 + 16 +
+                      NOISE_BUCKETS * 4;
+  auto kern = a.dtype == SRT_BF16 ? k_lmhead_sample<SRT_BF16> : k_lmhead_sample<SRT_F32>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<num_sms(), THREADS, smem, stream>>>(ma, mb, c, p);
+  return cudaGetLastError();
+}
+
+}  // namespace srt

@@ -550,6 +550,12 @@ int scan_cluster_size(int32_t V, int dtype) {
   return nblk * 4 <= 16 * 1024 ? 1 : 0;
 }
 
+cudaError_t launch_rowinfo(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
+                           unsigned long long* result, cudaStream_t stream) {
+  k_rowinfo<<<(a.n * 32 + 255) / 256, 256, 0, stream>>>(a, c.Bmax, rowinfo, result);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
                                 unsigned long long* result, cudaStream_t stream) {
   if (!scan_cluster_size(c.V, a.dtype)) return cudaErrorInvalidValue;

@@ -318,6 +318,21 @@ struct VerifyArgs {
   uint8_t* finished;
 };
 int scan_cluster_size(int32_t V, int dtype);
+// per row: (sequence, position); clears result[row]
+cudaError_t launch_rowinfo(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
+                           unsigned long long* result, cudaStream_t stream);
+// the fused LM-head GEMM + Gumbel-max sampler (lmhead.cu): result[row] for
+// every drafted row, logits never materialised (dump: optional debug copy)
+struct LmHeadArgs {
+  const void* hidden;   // bf16 [hidden_rows, K]
+  int64_t hidden_rows;
+  int32_t K;
+  const void* weight;   // bf16 [V, K]
+  void* dump;           // nullable: [rows, V] logits in cfg.logits_dtype
+};
+cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const LmHeadArgs& h,
+                                 const int2* rowinfo, unsigned long long* result,
+                                 cudaStream_t stream);
 cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
                                 unsigned long long* result, cudaStream_t stream);
 // reference = the unpruned kernel writing sampled[] directly; otherwise the

@@ -223,6 +223,50 @@ class SrtCache:
             _ptr(stats, torch.int64, "stats"), _stream()), "srt_verify_insert_cursor")
         return out
 
+    def verify_lmhead(self, hidden, weight, d: DraftOut, seq_id, seed: int, seq_tok, seq_len,
+                      max_new, prompt_id=None, cursor=None, floor=None, stats=None,
+                      temperature: float = 1.0, eos_id: int = -1, out: VerifyOut | None = None,
+                      rows: int | None = None, logits_out=None) -> VerifyOut:
+        """srt_verify_lmhead (or srt_verify_lmhead_insert_cursor when `cursor` is
+        given): the verify pass with the LM-head GEMM fused in front of the
+        sampler -- hidden [hidden_rows, K] bf16 (row r = logits row r),
+        weight [V, K] bf16; the logits are never written unless logits_out
+        ([rows, V], the cache's logits dtype) is given."""
+        n = seq_len.shape[0]
+        if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+            raise SrtError("hidden and weight must be bfloat16")
+        if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+            raise SrtError("hidden [rows, K] and weight [V, K] expected")
+        if weight.shape[0] != self.V:
+            raise SrtError("weight rows != V")
+        if logits_out is not None and (logits_out.dtype != self.logits_dtype
+                                       or logits_out.shape[-1] != self.V):
+            raise SrtError("logits_out must be [rows, V] of the cache's logits dtype")
+        if out is None:
+            out = VerifyOut.empty(n, hidden.shape[0] if rows is None else rows, self.Bmax,
+                                  seq_tok.device)
+        i32 = torch.int32
+        args = [self._h, n, _ptr(hidden, torch.bfloat16, "hidden"), hidden.shape[0],
+                hidden.shape[1], _ptr(weight, torch.bfloat16, "weight"),
+                _ptr(logits_out, None, "logits_out"), _ptr(d.row_offsets, torch.int64),
+                _ptr(d.draft_len, i32), _ptr(d.draft_tok, i32), _ptr(d.draft_parent, i32),
+                _ptr(d.draft_depth, i32), _ptr(seq_id, torch.int64, "seq_id"),
+                ctypes.c_uint64(seed & (2 ** 64 - 1)), float(temperature), int(eos_id),
+                _ptr(max_new, i32, "max_new"), _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+                _ptr(seq_len, i32, "seq_len"), _ptr(out.sampled, i32), _ptr(out.accept_len, i32),
+                _ptr(out.n_commit, i32), _ptr(out.commit_tok, i32),
+                _ptr(out.accepted_nodes, i32), _ptr(out.finished, torch.uint8)]
+        if cursor is None:
+            check(self.L.srt_verify_lmhead(*args, _stream()), "srt_verify_lmhead")
+        else:
+            if cursor.shape != (n, self.cfg.max_depth + 4):
+                raise ValueError(f"cursor must be ({n}, D + 4) int32")
+            check(self.L.srt_verify_lmhead_insert_cursor(
+                *args, _ptr(prompt_id, i32, "prompt_id"), _ptr(floor, i32, "floor"),
+                _ptr(cursor, i32, "cursor"), _ptr(stats, torch.int64, "stats"), _stream()),
+                "srt_verify_lmhead_insert_cursor")
+        return out
+
     # ---- test / inspection support -----------------------------------------
     def sample_rows_reference(self, logits, d: DraftOut, seq_len, seq_id, seed: int,
                               temperature: float = 1.0, out=None) -> torch.Tensor:
