@@ -14,8 +14,9 @@
 //    stage into an fp32 accumulator in tensor memory (two 256-column
 //    accumulators: the epilogue of tile i overlaps the MMAs of tile i + 1);
 //    tcgen05.commit frees the stage / publishes the accumulator;
-//  * warps 2-5: epilogue — tcgen05.ld of the thread's row (32x32b: thread =
-//    TMEM lane = logits row), the logit's rounding to the cache's logits
+//  * warps 2-9: epilogue — tcgen05.ld of the thread's row (32x32b: thread =
+//    TMEM lane = logits row; two warps per lane quarter, each a pair of the
+//    tile's four noise blocks), the logit's rounding to the cache's logits
 //    dtype (bf16 RN-even, exactly what a bf16 LM head would store), then the
 //    scan's exact branch and bound per 64-token noise block: block maximum,
 //    bound U_b = RN(max/T) + (bucket bound of G_b), exact z only where a
@@ -39,18 +40,19 @@ namespace srt {
 
 namespace {
 
-constexpr int BM = 128;             // rows per tile (UMMA M, TMEM lanes)
+constexpr int BM = 128;             // rows per CTA (TMEM lanes); the CTA pair covers 256
 constexpr int BN = 256;             // vocabulary columns per tile (UMMA N)
 constexpr int BK = 64;              // K per stage: 64 bf16 = one 128-byte swizzle row
 constexpr int UK = 16;              // K per tcgen05.mma (kind::f16)
-constexpr int NST = 4;              // smem ring stages
-constexpr int A_BYTES = BM * BK * 2;             // 16 KB
-constexpr int B_BYTES = BN * BK * 2;             // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 48 KB
-constexpr int EPI_WARPS = 4;
+constexpr int NST = 6;              // smem ring stages
+constexpr int A_BYTES = BM * BK * 2;             // 16 KB: this CTA's 128 rows of hidden
+constexpr int B_BYTES = (BN / 2) * BK * 2;       // 16 KB: this CTA's half of the weight tile
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB
+constexpr int EPI_WARPS = 8;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;   // two accumulators
 constexpr int BLK_PER_TILE = BN / NOISE_BLK;     // 4 noise blocks per tile
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;      // shared::cluster address -> CTA 0 of the pair
 
 // ---- PTX: shared-memory addresses, mbarriers, TMA, tcgen05 ---------------
 __device__ __forceinline__ uint32_t sm32(const void* p) {
@@ -74,13 +76,24 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                       int32_t c1, uint64_t pol) {
+// 2-SM TMA: the bytes land in THIS CTA's shared memory and are counted on
+// CTA 0's barrier (the one the pair's MMA issuer waits on)
+__device__ __forceinline__ void tma_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sm32(dst)),
-      "l"((uint64_t)map), "r"(sm32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sm32(dst)),
+      "l"((uint64_t)map), "r"(sm32(bar) & PEER_MASK), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
+}
+// arrive on CTA 0's copy of `bar`
+__device__ __forceinline__ void bar_arrive_leader(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(sm32(b) & PEER_MASK)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -88,20 +101,25 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// D[tmem] (+)= A[smem] . B[smem]^T, both K-major (one thread issues)
+// D[tmem] (+)= A[smem] . B[smem]^T over the CTA pair (M = 256: each CTA's A
+// rows land in its own TMEM; B's N halves come from both CTAs), both
+// K-major; issued by one thread of CTA 0
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                        uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// arrive on `bar` once every tcgen05 op this thread issued so far completes
+// arrive on `bar` in BOTH CTAs of the pair once every tcgen05 op this thread
+// issued so far completes
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   sm32(bar))
-               : "memory");
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(sm32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
 }
 // 32 consecutive fp32 columns of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -128,9 +146,15 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = BM
+// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 2 BM (pair)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)((2 * BM) >> 4) << 24);
+
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
 
 __device__ __forceinline__ uint64_t ld_relaxed64(const unsigned long long* p) {
   unsigned long long v;
@@ -158,13 +182,13 @@ struct LmParams {
 };
 
 template <int DT>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 DevCache c, LmParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the swizzled tiles
+  // 1024-byte alignment for the swizzled tiles (same offsets in both CTAs)
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* ring = smem;                                        // [NST][A | B]
+  unsigned char* ring = smem;                                        // [NST][A | B half]
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + NST * STAGE_BYTES);
   uint64_t* empty = full + NST;
   uint64_t* acc_full = empty + NST;   // [2]
@@ -173,101 +197,112 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   float* tab = reinterpret_cast<float*>(tmem_slot + 4);              // [NOISE_BUCKETS]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t rank = blockIdx.x & 1;  // in the CTA pair (cluster of 2)
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int64_t total = *p.total;
-  const int32_t num_m = (int32_t)((total + BM - 1) / BM);
+  const int32_t num_m = (int32_t)((total + 2 * BM - 1) / (2 * BM));  // 256-row pair blocks
   const int32_t num_n = (p.V + BN - 1) / BN;
   const int64_t tiles = (int64_t)num_m * num_n;
 
   for (int i = tid; i < NOISE_BUCKETS; i += blockDim.x) tab[i] = c.gbound[i];
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
-      bar_init(&full[s], 1);
-      bar_init(&empty[s], 1);
+      bar_init(&full[s], 1);   // (CTA 0's: the leader's expect_tx; both CTAs' bytes)
+      bar_init(&empty[s], 1);  // the MMA commit, multicast to both CTAs
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&acc_full[a], 1);
-      bar_init(&acc_empty[a], EPI_WARPS);
+      bar_init(&acc_empty[a], 2 * EPI_WARPS);  // (CTA 0's: both CTAs' epilogue warps)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_b) : "memory");
   }
-  if (wid == 1) {  // the MMA warp owns the tensor memory
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+  if (wid == 1) {  // warp 1 of both CTAs allocates the pair's tensor memory
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      sm32(tmem_slot)),
                  "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (wid == 0) {
-    // ============ TMA producer ============================================
+    // ============ TMA producer (both CTAs: own A rows, own half of B) =======
     if (lane == 0) {
       uint64_t pol_a, pol_b;  // hidden rows are re-read for every vocab tile; W once per m
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_a));
       asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_b));
       uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int64_t t = pair; t < tiles; t += npairs) {
         const int32_t nt = (int32_t)(t / num_m), mb = (int32_t)(t % num_m);
         for (int32_t kb = 0; kb < p.nk; ++kb, ++it) {
           const int s = (int)(it % NST);
           const uint32_t use = it / NST;
           if (use > 0) bar_wait(&empty[s], (use - 1) & 1);
           unsigned char* st = ring + s * STAGE_BYTES;
-          bar_expect_tx(&full[s], STAGE_BYTES);
-          tma_2d(st, &map_a, &full[s], kb * BK, mb * BM, pol_a);
-          tma_2d(st + A_BYTES, &map_b, &full[s], kb * BK, nt * BN, pol_b);
+          if (rank == 0) bar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          tma_2d_pair(st, &map_a, &full[s], kb * BK, mb * 2 * BM + (int32_t)rank * BM, pol_a);
+          tma_2d_pair(st + A_BYTES, &map_b, &full[s], kb * BK, nt * BN + (int32_t)rank * (BN / 2),
+                      pol_b);
         }
       }
     }
   } else if (wid == 1) {
-    // ============ MMA issuer ==============================================
-    uint32_t it = 0, u = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++u) {
-      const uint32_t a = u & 1, ause = u >> 1;
-      if (ause > 0) bar_wait(&acc_empty[a], (ause - 1) & 1);
-      tc_fence_after();
-      const uint32_t d = tmem + a * BN;
-      for (int32_t kb = 0; kb < p.nk; ++kb, ++it) {
-        const int s = (int)(it % NST);
-        bar_wait(&full[s], (it / NST) & 1);
+    // ============ MMA issuer (CTA 0 only) =================================
+    if (rank == 0) {
+      uint32_t it = 0, u = 0;
+      for (int64_t t = pair; t < tiles; t += npairs, ++u) {
+        const uint32_t a = u & 1, ause = u >> 1;
+        if (ause > 0) bar_wait(&acc_empty[a], (ause - 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = sm32(ring + s * STAGE_BYTES), sb = sa + A_BYTES;
+        const uint32_t d = tmem + a * BN;
+        for (int32_t kb = 0; kb < p.nk; ++kb, ++it) {
+          const int s = (int)(it % NST);
+          bar_wait(&full[s], (it / NST) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = sm32(ring + s * STAGE_BYTES), sb = sa + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)  // +32 bytes per K16 step inside the swizzle row
-            tc_mma(d, sw128_desc(sa + k * UK * 2), sw128_desc(sb + k * UK * 2), IDESC,
-                   (kb | k) != 0);
-          tc_commit(&empty[s]);                    // stage free once these MMAs finish
-          if (kb == p.nk - 1) tc_commit(&acc_full[a]);  // accumulator complete
+            for (int k = 0; k < BK / UK; ++k)  // +32 bytes per K16 step inside the swizzle row
+              tc_mma(d, sw128_desc(sa + k * UK * 2), sw128_desc(sb + k * UK * 2), IDESC,
+                     (kb | k) != 0);
+            tc_commit(&empty[s]);                         // stage free in both CTAs
+            if (kb == p.nk - 1) tc_commit(&acc_full[a]);  // accumulator complete in both
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else {
     // ============ epilogue: sample from the accumulator ===================
-    const int q = wid & 3;  // TMEM lane quarter this warp may access
+    // 8 warps: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its rows) and the
+    // block pair h = (w - 2) / 4 of the tile's 4 noise blocks (columns
+    // 128 h .. 128 h + 127): one Philox call gives both blocks' words.
+    const int q = wid & 3;
+    const int h = (wid - 2) >> 2;
     const float T = p.temperature;
     const bool unit_t = T == 1.0f;
     const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
     const int64_t nblk = ((int64_t)p.V + NOISE_BLK - 1) / NOISE_BLK;
     uint32_t u = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++u) {
+    for (int64_t t = pair; t < tiles; t += npairs, ++u) {
       const uint32_t a = u & 1;
+      const int32_t nt = (int32_t)(t / num_m), mb = (int32_t)(t % num_m);
+      const int64_t r = (int64_t)mb * 2 * BM + rank * BM + q * 32 + lane;
+      const bool rv = r < total;
+      // the row's key and best-so-far (global loads) before the accumulator wait
+      int2 ri = make_int2(0, 0);
+      if (rv) ri = p.rowinfo[r];
       bar_wait(&acc_full[a], (u >> 1) & 1);
       tc_fence_after();
-      const int32_t nt = (int32_t)(t / num_m), mb = (int32_t)(t % num_m);
-      const int64_t r = (int64_t)mb * BM + q * 32 + lane;
-      const bool rv = r < total;
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
-      const int64_t b0 = (int64_t)nt * BLK_PER_TILE;  // first noise block of the tile (even)
+      const int64_t b0 = (int64_t)nt * BLK_PER_TILE + 2 * h;  // this warp's first block (even)
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN + 2 * h * NOISE_BLK;
       uint32_t pos = 0, slo = 0, shi = 0;
       unsigned long long cur = 0;
       if (rv) {
-        const int2 ri = p.rowinfo[r];
         const uint64_t sid = p.seq_id[ri.x];
         pos = (uint32_t)ri.y;
         slo = (uint32_t)sid;
@@ -275,28 +310,36 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         cur = ld_relaxed64(&p.result[r]);
       }
       float M = cur ? unpack_value(cur) : -INFINITY;  // an achieved z of the row (or none)
-      // ---- pass A: block maxima (first index of the max), optional dump ----
-      float bmax[BLK_PER_TILE];
-      int32_t barg[BLK_PER_TILE];
+      // ---- pass A: block maxima.  Rounding is monotone, so the max of the
+      // rounded logits is the rounded max of the accumulators ----
+      float X[2];
       bool nan = false;
 #pragma unroll
-      for (int j = 0; j < BLK_PER_TILE; ++j) {
+      for (int j = 0; j < 2; ++j) {
         const int n = block_len(p.V, b0 + j);
         float x[NOISE_BLK];
         tmem_ld32(taddr + j * NOISE_BLK, x);
         tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
         float m = -INFINITY;
-        int32_t am = -1;
+        if (n == NOISE_BLK) {
+          float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < NOISE_BLK; ++k) {
-          x[k] = as_logit<DT>(x[k]);
-          if (k < n) {
-            nan |= x[k] != x[k];
-            if (x[k] > m || (am < 0 && x[k] == m)) { m = x[k]; am = k; }
+          for (int k = 0; k < NOISE_BLK; k += 2) {
+            m0 = max_nan(m0, x[k]);
+            m1 = max_nan(m1, x[k + 1]);
           }
+          m = max_nan(m0, m1);
         }
-        bmax[j] = m;
-        barg[j] = am;
+        if (n < NOISE_BLK || m != m) {  // partial block, or a NaN: the careful max
+          m = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < NOISE_BLK; ++k)
+            if (k < n) {
+              nan |= x[k] != x[k];
+              if (x[k] > m) m = x[k];
+            }
+        }
+        X[j] = n > 0 ? as_logit<DT>(m) : -INFINITY;
         if (p.dump && rv && n > 0) {
           const int64_t v0 = (b0 + j) * NOISE_BLK;
           if (DT == SRT_BF16) {
@@ -312,105 +355,99 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           }
         }
       }
-      // ---- the blocks' words and bounds U_b (one Philox per block pair) ----
-      uint32_t wa[BLK_PER_TILE], wb[BLK_PER_TILE];
-      float U[BLK_PER_TILE];
-#pragma unroll
-      for (int pp = 0; pp < BLK_PER_TILE / 2; ++pp) {
-        const int64_t bp = b0 + 2 * pp;
-        Philox4 w{0, 0, 0, 0};
-        if (rv && bp < nblk)
-          w = philox4x32_10(0x80000000u | (uint32_t)(bp >> 1), pos, slo, shi, k0, k1);
-        wa[2 * pp] = w.x;
-        wb[2 * pp] = w.y;
-        wa[2 * pp + 1] = w.z;
-        wb[2 * pp + 1] = w.w;
+      // ---- the pair's words and bounds U_b ----
+      uint32_t wa[2] = {0, 0}, wb[2] = {0, 0};
+      if (rv && b0 < nblk) {
+        const Philox4 w = philox4x32_10(0x80000000u | (uint32_t)(b0 >> 1), pos, slo, shi, k0, k1);
+        wa[0] = w.x;
+        wb[0] = w.y;
+        wa[1] = w.z;
+        wb[1] = w.w;
       }
+      float U[2];
 #pragma unroll
-      for (int j = 0; j < BLK_PER_TILE; ++j) {
+      for (int j = 0; j < 2; ++j) {
         const int n = block_len(p.V, b0 + j);
-        if (!rv || n == 0 || barg[j] < 0) {
+        if (!rv || n == 0 || !(X[j] > -INFINITY)) {
           U[j] = -INFINITY;
           continue;
         }
-        const float xs = unit_t ? bmax[j] : __fdiv_rn(bmax[j], T);
+        const float xs = unit_t ? X[j] : __fdiv_rn(X[j], T);
         const float G = n == NOISE_BLK ? tab[wa[j] >> 22] : block_noise(wa[j], wb[j], (uint32_t)n).G;
         U[j] = __fadd_rn(xs, G);
       }
-      // ---- the tile's best candidate: z of the block with the largest bound's
-      // maximum first (an exact achieved z), then every block that can still
-      // reach the row's best ----
+      const int jf = U[1] > U[0] ? 1 : 0;  // per lane: the block with the larger bound first
       float bz = -INFINITY;
       int32_t bv = INT_MAX;
-      int jf = 0;
-#pragma unroll
-      for (int j = 1; j < BLK_PER_TILE; ++j)
-        if (U[j] > U[jf]) jf = j;
-      auto block_of = [&](int j, BlockNoise& bn) {
-        bn = block_noise(wa[j], wb[j], (uint32_t)block_len(p.V, b0 + j));
-      };
       auto elem_g = [&](int64_t v, int32_t k, const BlockNoise& bn) {
         if ((uint32_t)k == bn.p) return bn.G;
         const Philox4 w = philox4x32_10((uint32_t)(v >> 2), pos, slo, shi, k0, k1);
         const uint32_t e = (uint32_t)(v & 3);
         return element_noise_from_word(e == 0 ? w.x : e == 1 ? w.y : e == 2 ? w.z : w.w, bn);
       };
-      // z(i*) of block jf's maximum (exact): seeds M on a row's first tiles
-      if (rv && U[jf] >= M && U[jf] > -INFINITY) {
-        BlockNoise bn;
-        block_of(jf, bn);
-        const int64_t v = (b0 + jf) * NOISE_BLK + barg[jf];
-        const float xs = unit_t ? bmax[jf] : __fdiv_rn(bmax[jf], T);
-        const float z = __fadd_rn(xs, elem_g(v, barg[jf], bn));
-        if (cand_better(z, (int32_t)v, bz, bv)) { bz = z; bv = (int32_t)v; }
-        M = fmaxf(M, z);
-      }
-      // exact evaluation of block j (the thread's own row): every element
-      // whose RN(x/T) + G_b can reach M; x re-read from tensor memory
+      // exact evaluation (block jf first): every element whose RN(x/T) + G_b
+      // can reach M.  A row with no achieved z yet (its first tiles) first
+      // takes z(i*) of block jf's maximum (first index), which prunes the rest
+      // (the TMEM address of tcgen05.ld must be warp-uniform: the warp walks
+      // the blocks in a fixed order, round 0 serving the lanes whose larger
+      // bound is that block, round 1 the others)
 #pragma unroll 1
-      for (int round = 0; round < 2; ++round) {
-#pragma unroll 1
-        for (int j = 0; j < BLK_PER_TILE; ++j) {
-          const bool need = rv && (round == 0 ? j == jf : j != jf) && U[j] >= M &&
-                            U[j] > -INFINITY;
-          if (!__any_sync(0xffffffffu, need)) continue;
-          float x[NOISE_BLK];
-          tmem_ld32(taddr + j * NOISE_BLK, x);
-          tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
-          if (!need) continue;
-          const int n = block_len(p.V, b0 + j);
-          BlockNoise bn;
-          block_of(j, bn);
-          uint64_t cand = 0;  // bit k: element k can reach M
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = jj & 1;
+        const bool mine = (jj < 2) == (j == jf);
+        // (selects, not runtime indexing: the arrays stay in registers)
+        const float Uj = j ? U[1] : U[0], Xj = j ? X[1] : X[0];
+        const uint32_t waj = j ? wa[1] : wa[0], wbj = j ? wb[1] : wb[0];
+        const bool need = rv && mine && Uj > -INFINITY && Uj >= M;
+        if (!__any_sync(0xffffffffu, need)) continue;
+        float x[NOISE_BLK];
+        tmem_ld32(taddr + j * NOISE_BLK, x);
+        tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
+        if (!need) continue;
+        const int n = block_len(p.V, b0 + j);
+        const BlockNoise bn = block_noise(waj, wbj, (uint32_t)n);
+        const float Xs = unit_t ? Xj : __fdiv_rn(Xj, T);
+        const int64_t vb = (b0 + j) * NOISE_BLK;
+        if (!(M > -INFINITY)) {  // seed: z(i*), i* = the first index of the block max X
+          int32_t ks = 0;
 #pragma unroll
-          for (int k = 0; k < NOISE_BLK; ++k) {
-            x[k] = as_logit<DT>(x[k]);
-            const float xs = unit_t ? x[k] : __fdiv_rn(x[k], T);
-            if (k < n && __fadd_rn(xs, bn.G) >= M) cand |= 1ull << k;  // (NaN fails)
-          }
-          while (cand) {
-            const int32_t k = __ffsll((long long)cand) - 1;
-            cand &= cand - 1;
-            float xk = 0.0f;
+          for (int k = NOISE_BLK - 1; k >= 0; --k)
+            if (k < n && as_logit<DT>(x[k]) == Xj) ks = k;
+          const float z = __fadd_rn(Xs, elem_g(vb + ks, ks, bn));
+          bz = z;
+          bv = (int32_t)(vb + ks);
+          M = z;
+        }
+        uint64_t cand = 0;  // bit k: element k can reach M
 #pragma unroll
-            for (int i = 0; i < NOISE_BLK; ++i)
-              if (i == k) xk = x[i];
-            const float xs = unit_t ? xk : __fdiv_rn(xk, T);
-            if (__fadd_rn(xs, bn.G) < M) continue;  // M rose meanwhile
-            const int64_t v = (b0 + j) * NOISE_BLK + k;
-            const float z = __fadd_rn(xs, elem_g(v, k, bn));
-            if (cand_better(z, (int32_t)v, bz, bv)) {
-              bz = z;
-              bv = (int32_t)v;
-              M = fmaxf(M, z);
-            }
+        for (int k = 0; k < NOISE_BLK; ++k) {
+          const float xr = as_logit<DT>(x[k]);
+          const float xs = unit_t ? xr : __fdiv_rn(xr, T);
+          if (k < n && __fadd_rn(xs, bn.G) >= M) cand |= 1ull << k;  // (NaN fails)
+        }
+        while (cand) {
+          const int32_t k = __ffsll((long long)cand) - 1;
+          cand &= cand - 1;
+          float xk = 0.0f;
+#pragma unroll
+          for (int i = 0; i < NOISE_BLK; ++i)
+            if (i == k) xk = x[i];
+          xk = as_logit<DT>(xk);
+          const float xs = unit_t ? xk : __fdiv_rn(xk, T);
+          if (__fadd_rn(xs, bn.G) < M) continue;  // M rose meanwhile
+          const int64_t v = vb + k;
+          const float z = __fadd_rn(xs, elem_g(v, k, bn));
+          if (cand_better(z, (int32_t)v, bz, bv)) {
+            bz = z;
+            bv = (int32_t)v;
+            M = fmaxf(M, z);
           }
         }
       }
       // the accumulator may be overwritten once every epilogue warp is done
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) bar_arrive(&acc_empty[a]);
+      if (lane == 0) bar_arrive_leader(&acc_empty[a]);
       if (__any_sync(0xffffffffu, nan) && lane == 0) set_error(c, SRT_DEV_NONFINITE_LOGIT);
       if (rv && bv != INT_MAX) {
         const unsigned long long pk = pack_cand(bz, bv);
@@ -418,10 +455,11 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  cluster_sync();  // both CTAs done with the tensor memory and the leader's barriers
   if (wid == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
   }
 }
@@ -459,7 +497,8 @@ cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const L
                                  const int2* rowinfo, unsigned long long* result,
                                  cudaStream_t stream) {
   CUtensorMap ma, mb;
-  if (!make_map(&ma, h.hidden, h.hidden_rows, h.K, BM) || !make_map(&mb, h.weight, c.V, h.K, BN))
+  if (!make_map(&ma, h.hidden, h.hidden_rows, h.K, BM) ||
+      !make_map(&mb, h.weight, c.V, h.K, BN / 2))
     return cudaErrorInvalidValue;
   LmParams p;
   p.V = c.V;
@@ -476,7 +515,7 @@ cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const L
   auto kern = a.dtype == SRT_BF16 ? k_lmhead_sample<SRT_BF16> : k_lmhead_sample<SRT_F32>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<num_sms(), THREADS, smem, stream>>>(ma, mb, c, p);
+  kern<<<num_sms() & ~1, THREADS, smem, stream>>>(ma, mb, c, p);  // CTA pairs (cluster of 2)
   return cudaGetLastError();
 }
 
