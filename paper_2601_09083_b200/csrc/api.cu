@@ -23,6 +23,8 @@ struct srt_cache {
   int2* rowinfo = nullptr;      // verify: per-row (sequence, position)
   unsigned long long* result = nullptr;  // verify: per-row packed winner (pack_cand)
   int64_t row_cap = 0;          // rows the two buffers above can hold
+  LmHeadScratch lm{nullptr, nullptr, nullptr, 0};  // srt_verify_lmhead: deferred blocks
+  int64_t lm_rows = 0;          // rows lm can hold
   void* path = nullptr;         // srt_verify_path: row lists and walk state
   size_t path_cap = 0;
   uint32_t* hubwork = nullptr;  // hub refresh work list [DIRTY_CAP + 1]
@@ -120,7 +122,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_scnt = off;    off = align_up(off + W * 4);
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
   const size_t o_status = off;  off = align_up(off + 4);
-  const size_t o_gb = off;      off = align_up(off + (2 * NOISE_BUCKETS + 1) * 4);
+  const size_t o_gb = off;      off = align_up(off + (3 * NOISE_BUCKETS + 1) * 4);
   // hub child lists: ~1 slot per 16 nodes' worth of hash, at least 2^12
   size_t HC = 4096;
   while (HC < H / 512 && HC < (1u << 18)) HC <<= 1;
@@ -194,6 +196,9 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   if (c->result) cudaFreeAsync(c->result, (cudaStream_t)stream);
   if (c->path) cudaFreeAsync(c->path, (cudaStream_t)stream);
   if (c->hubwork) cudaFreeAsync(c->hubwork, (cudaStream_t)stream);
+  if (c->lm.cand_x) cudaFreeAsync(c->lm.cand_x, (cudaStream_t)stream);
+  if (c->lm.cand_b) cudaFreeAsync(c->lm.cand_b, (cudaStream_t)stream);
+  if (c->lm.cand_n) cudaFreeAsync(c->lm.cand_n, (cudaStream_t)stream);
   delete c;
   return SRT_OK;
 }
@@ -339,11 +344,30 @@ srt_status verify_lmhead_scan(srt_cache* c, const VerifyArgs& a, const LmHeadArg
                               cudaStream_t stream) {
   const srt_status bs = row_buffers(c, a, stream);
   if (bs != SRT_OK) return bs;
+  const int64_t rows_max = (int64_t)a.n * (c->cfg.budget_max + 1);
+  if (c->lm_rows < rows_max) {
+    if (c->lm.cand_x) {
+      SRT_CUDA(cudaFreeAsync(c->lm.cand_x, stream), "cudaFreeAsync(lm)");
+      SRT_CUDA(cudaFreeAsync(c->lm.cand_b, stream), "cudaFreeAsync(lm)");
+      SRT_CUDA(cudaFreeAsync(c->lm.cand_n, stream), "cudaFreeAsync(lm)");
+    }
+    const int64_t cap = std::max<int64_t>(rows_max, 4096);
+    const size_t esz = c->cfg.logits_dtype == SRT_BF16 ? 2 : 4;
+    c->lm.cap = LMHEAD_CAND_CAP;
+    SRT_CUDA(cudaMallocAsync(&c->lm.cand_x, (size_t)cap * LMHEAD_CAND_CAP * 64 * esz, stream),
+             "cudaMallocAsync(lm candidates)");
+    SRT_CUDA(cudaMallocAsync((void**)&c->lm.cand_b, (size_t)cap * LMHEAD_CAND_CAP * 4, stream),
+             "cudaMallocAsync(lm candidates)");
+    SRT_CUDA(cudaMallocAsync((void**)&c->lm.cand_n, (size_t)cap * 4, stream),
+             "cudaMallocAsync(lm candidates)");
+    SRT_CUDA(cudaMemsetAsync(c->lm.cand_n, 0, (size_t)cap * 4, stream), "memset(lm)");
+    c->lm_rows = cap;
+  }
   SRT_CUDA(timed(c, SRT_K_LMHEAD, stream,
                  [&] {
                    cudaError_t e = launch_rowinfo(c->dev, a, c->rowinfo, c->result, stream);
                    if (e != cudaSuccess) return e;
-                   return launch_lmhead_sample(c->dev, a, h, c->rowinfo, c->result, stream);
+                   return launch_lmhead_sample(c->dev, a, h, c->rowinfo, c->result, c->lm, stream);
                  }),
            "verify lm-head");
   return SRT_OK;

@@ -44,36 +44,44 @@ cudaError_t launch_init_cache(const DevCache& c, cudaStream_t stream) {
 // The maximum noise of a FULL 64-token block as a function of its word's
 // r = wa >> 9:  G64(r) = -log_det(RN(-log_det(u(r)) / 64))  (O11).
 // Bucket b covers r in [b << 13, (b+1) << 13): gbound[b] = max G64 over the
-// bucket, gbound[1024] = max over all r, gbound[1025 + b] = min over the
+// bucket, gbound[1024] = max over all r, gbound[2049 + b] = max over the
+// bucket of the single-word Gumbel g(r) = -log_det(-log_det(u(r))) (the
+// fused LM-head sampler's per-element pre-bound), gbound[1025 + b] = min over the
 // bucket.  Computed by enumeration, so the bounds are exact whatever the shape
 // of G64; the scan's block bound is max x + gbound[r >> 13].
 __global__ void __launch_bounds__(256) k_noise_bucket_max(float* gbound) {
   __shared__ float red[8], redmin[8];
   const uint32_t b = blockIdx.x;
-  float m = -INFINITY, mn = INFINITY;
+  __shared__ float redg[8];
+  float m = -INFINITY, mn = INFINITY, mg = -INFINITY;
   for (uint32_t j = threadIdx.x; j < (1u << NOISE_BUCKET_SHIFT); j += blockDim.x) {
     const uint32_t r = (b << NOISE_BUCKET_SHIFT) | j;
     const BlockNoise bn = block_noise(r << 9, 0u, (uint32_t)NOISE_BLK);
     const float g = bn.G;
     m = fmaxf(m, g);
     mn = fminf(mn, g);
+    mg = fmaxf(mg, gumbel_of_r(r));
   }
   for (int o = 16; o; o >>= 1) {
     m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
   }
   if ((threadIdx.x & 31) == 0) {
     red[threadIdx.x >> 5] = m;
     redmin[threadIdx.x >> 5] = mn;
+    redg[threadIdx.x >> 5] = mg;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < 8; ++w) {
       m = fmaxf(m, red[w]);
       mn = fminf(mn, redmin[w]);
+      mg = fmaxf(mg, redg[w]);
     }
     gbound[b] = m;
     gbound[NOISE_BUCKETS + 1 + b] = mn;
+    gbound[2 * NOISE_BUCKETS + 1 + b] = mg;
   }
 }
 

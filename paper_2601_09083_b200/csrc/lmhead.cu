@@ -14,9 +14,10 @@
 //    stage into an fp32 accumulator in tensor memory (two 256-column
 //    accumulators: the epilogue of tile i overlaps the MMAs of tile i + 1);
 //    tcgen05.commit frees the stage / publishes the accumulator;
-//  * warps 2-9: epilogue — tcgen05.ld of the thread's row (32x32b: thread =
-//    TMEM lane = logits row; two warps per lane quarter, each a pair of the
-//    tile's four noise blocks), the logit's rounding to the cache's logits
+//  * warps 2-17: epilogue — tcgen05.ld of the thread's row (32x32b: thread =
+//    TMEM lane = logits row; four warps per lane quarter, one per noise block
+//    of the tile; the accumulator is released as soon as it is in
+//    registers), the logit's rounding to the cache's logits
 //    dtype (bf16 RN-even, exactly what a bf16 LM head would store), then the
 //    scan's exact branch and bound per 64-token noise block: block maximum,
 //    bound U_b = RN(max/T) + (bucket bound of G_b), exact z only where a
@@ -48,7 +49,7 @@ constexpr int NST = 6;              // smem ring stages
 constexpr int A_BYTES = BM * BK * 2;             // 16 KB: this CTA's 128 rows of hidden
 constexpr int B_BYTES = (BN / 2) * BK * 2;       // 16 KB: this CTA's half of the weight tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB
-constexpr int EPI_WARPS = 8;
+constexpr int EPI_WARPS = 16;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;   // two accumulators
 constexpr int BLK_PER_TILE = BN / NOISE_BLK;     // 4 noise blocks per tile
@@ -64,9 +65,6 @@ __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
 __device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm32(b)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void bar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm32(b)) : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
@@ -94,6 +92,21 @@ __device__ __forceinline__ void bar_arrive_leader(uint64_t* b) {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
+}
+// the epilogue's wait: a try_wait with a suspend-time hint parks the warp
+// until the phase completes instead of polling (16 polling warps would take
+// issue slots from the producer / MMA warps)
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 20000;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(sm32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -162,12 +175,52 @@ __device__ __forceinline__ uint64_t ld_relaxed64(const unsigned long long* p) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // .x = a (low half)
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // the logit as the cache's logits dtype stores it (bf16: RN-even), in fp32
 template <int DT>
 __device__ __forceinline__ float as_logit(float acc) {
   if (DT == SRT_BF16) return __bfloat162float(__float2bfloat16_rn(acc));
   return acc;
 }
+
+// z of element v (offset k in its block) with the block's noise bn: RN(xs + g_v).
+// Out of line: the exact pass calls it for the few elements that pass the
+// prefilter, from a 64-way unrolled loop.
+// Before the two logarithms, a bound: g_v = min(G_b, -log_det(RN(E_b + A_v)))
+// <= min(G_b, g(r_v)) + (8 ulp of log_det's non-monotonicity, bounded by its
+// <= 4 ulp error vs log, pinned exhaustively) <= min(G_b, gstd[r_v >> 13] +
+// 2^-14), gstd = the bucket maxima of g(r); if even that cannot reach M the
+// element is skipped (returns -inf).
+__device__ __noinline__ float elem_z(float xs, int64_t v, int32_t k, BlockNoise bn, uint32_t pos,
+                                     uint32_t slo, uint32_t shi, uint32_t k0, uint32_t k1,
+                                     float M, const float* gstd) {
+  float g = bn.G;
+  if ((uint32_t)k != bn.p) {
+    const Philox4 w = philox4x32_10((uint32_t)(v >> 2), pos, slo, shi, k0, k1);
+    const uint32_t e = (uint32_t)(v & 3);
+    const uint32_t wv = e == 0 ? w.x : e == 1 ? w.y : e == 2 ? w.z : w.w;
+    const float gb = fminf(bn.G, gstd[wv >> 22] + 6.103515625e-05f);
+    if (__fadd_rn(xs, gb) < M) return -INFINITY;
+    g = element_noise_from_word(wv, bn);
+  }
+  return __fadd_rn(xs, g);
+}
+
+// A raw-accumulator threshold below which RN(RN(RN_logit(x)/T) + G) < M
+// for certain: (M - G) T lowered by a margin covering the logit rounding
+// (2^-8 relative), the division and the addition (a few ulp each).
+__device__ __forceinline__ float prefilter_threshold(float M, float G, float T) {
+  if (!(M > -INFINITY)) return -INFINITY;
+  const float c = (M - G) * T;
+  const float thr = c - (fabsf(c) * 0.0625f + fabsf(M) * 0.0625f * T + 1e-30f);
+  return thr == thr && thr < INFINITY ? thr : -INFINITY;  // (overflow: no prefilter)
+}
+
+__device__ unsigned long long g_lm_stats[4];  // development (SRT_LMHEAD_DEBUG & 64)
 
 struct LmParams {
   int32_t V;
@@ -179,6 +232,12 @@ struct LmParams {
   float temperature;
   unsigned long long* result;  // per row: packed best (z, v), atomicMax
   void* dump;                  // nullable [rows, V] logits
+  void* cand_x;                // [rows][cand_cap][64] deferred blocks' rounded logits
+  int32_t* cand_b;             // [rows][cand_cap] their block indices
+  int32_t* cand_n;             // [rows] deferred blocks (may exceed cand_cap: overflow)
+  int32_t cand_cap;
+  uint32_t debug;              // development: 1 = epilogue skips its work, 2 = no MMAs,
+                               // 4 = bounds only (no exact pass)
 };
 
 template <int DT>
@@ -195,6 +254,7 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   uint64_t* acc_empty = acc_full + 2; // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* tab = reinterpret_cast<float*>(tmem_slot + 4);              // [NOISE_BUCKETS]
+  float* gstd = tab + NOISE_BUCKETS;                                 // [NOISE_BUCKETS]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t rank = blockIdx.x & 1;  // in the CTA pair (cluster of 2)
@@ -204,7 +264,10 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
   const int32_t num_n = (p.V + BN - 1) / BN;
   const int64_t tiles = (int64_t)num_m * num_n;
 
-  for (int i = tid; i < NOISE_BUCKETS; i += blockDim.x) tab[i] = c.gbound[i];
+  for (int i = tid; i < NOISE_BUCKETS; i += blockDim.x) {
+    tab[i] = c.gbound[i];
+    gstd[i] = c.gbound[2 * NOISE_BUCKETS + 1 + i];
+  }
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       bar_init(&full[s], 1);   // (CTA 0's: the leader's expect_tx; both CTAs' bytes)
@@ -267,8 +330,9 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             const uint32_t sa = sm32(ring + s * STAGE_BYTES), sb = sa + A_BYTES;
 #pragma unroll
             for (int k = 0; k < BK / UK; ++k)  // +32 bytes per K16 step inside the swizzle row
-              tc_mma(d, sw128_desc(sa + k * UK * 2), sw128_desc(sb + k * UK * 2), IDESC,
-                     (kb | k) != 0);
+              if (!(p.debug & 2))
+                tc_mma(d, sw128_desc(sa + k * UK * 2), sw128_desc(sb + k * UK * 2), IDESC,
+                       (kb | k) != 0);
             tc_commit(&empty[s]);                         // stage free in both CTAs
             if (kb == p.nk - 1) tc_commit(&acc_full[a]);  // accumulator complete in both
           }
@@ -278,11 +342,10 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     }
   } else {
     // ============ epilogue: sample from the accumulator ===================
-    // 8 warps: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its rows) and the
-    // block pair h = (w - 2) / 4 of the tile's 4 noise blocks (columns
-    // 128 h .. 128 h + 127): one Philox call gives both blocks' words.
+    // 16 warps: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its 32 rows) and
+    // noise block jb = (w - 2) / 4 of the tile's four (columns 64 jb .. + 63).
     const int q = wid & 3;
-    const int h = (wid - 2) >> 2;
+    const int jb = (wid - 2) >> 2;
     const float T = p.temperature;
     const bool unit_t = T == 1.0f;
     const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
@@ -293,161 +356,168 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int32_t nt = (int32_t)(t / num_m), mb = (int32_t)(t % num_m);
       const int64_t r = (int64_t)mb * 2 * BM + rank * BM + q * 32 + lane;
       const bool rv = r < total;
+      const int64_t b = (int64_t)nt * BLK_PER_TILE + jb;  // this warp's noise block
+      const int n = block_len(p.V, b);
       // the row's key and best-so-far (global loads) before the accumulator wait
       int2 ri = make_int2(0, 0);
-      if (rv) ri = p.rowinfo[r];
-      bar_wait(&acc_full[a], (u >> 1) & 1);
-      tc_fence_after();
-      const int64_t b0 = (int64_t)nt * BLK_PER_TILE + 2 * h;  // this warp's first block (even)
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN + 2 * h * NOISE_BLK;
+      if (rv && !(p.debug & 8)) ri = p.rowinfo[r];
       uint32_t pos = 0, slo = 0, shi = 0;
       unsigned long long cur = 0;
-      if (rv) {
+      if (rv && !(p.debug & 8)) {
         const uint64_t sid = p.seq_id[ri.x];
         pos = (uint32_t)ri.y;
         slo = (uint32_t)sid;
         shi = (uint32_t)(sid >> 32);
         cur = ld_relaxed64(&p.result[r]);
       }
-      float M = cur ? unpack_value(cur) : -INFINITY;  // an achieved z of the row (or none)
-      // ---- pass A: block maxima.  Rounding is monotone, so the max of the
-      // rounded logits is the rounded max of the accumulators ----
-      float X[2];
-      bool nan = false;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int n = block_len(p.V, b0 + j);
-        float x[NOISE_BLK];
-        tmem_ld32(taddr + j * NOISE_BLK, x);
-        tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
-        float m = -INFINITY;
-        if (n == NOISE_BLK) {
-          float m0 = -INFINITY, m1 = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < NOISE_BLK; k += 2) {
-            m0 = max_nan(m0, x[k]);
-            m1 = max_nan(m1, x[k + 1]);
-          }
-          m = max_nan(m0, m1);
-        }
-        if (n < NOISE_BLK || m != m) {  // partial block, or a NaN: the careful max
-          m = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < NOISE_BLK; ++k)
-            if (k < n) {
-              nan |= x[k] != x[k];
-              if (x[k] > m) m = x[k];
-            }
-        }
-        X[j] = n > 0 ? as_logit<DT>(m) : -INFINITY;
-        if (p.dump && rv && n > 0) {
-          const int64_t v0 = (b0 + j) * NOISE_BLK;
-          if (DT == SRT_BF16) {
-            __nv_bfloat16* o = (__nv_bfloat16*)p.dump + r * (int64_t)p.V + v0;
-#pragma unroll
-            for (int k = 0; k < NOISE_BLK; ++k)
-              if (k < n) o[k] = __float2bfloat16_rn(x[k]);
-          } else {
-            float* o = (float*)p.dump + r * (int64_t)p.V + v0;
-#pragma unroll
-            for (int k = 0; k < NOISE_BLK; ++k)
-              if (k < n) o[k] = x[k];
-          }
-        }
+      uint32_t wa = 0, wb = 0;  // the block's words (one Philox call per block pair)
+      if (rv && b < nblk) {
+        const Philox4 w = philox4x32_10(0x80000000u | (uint32_t)(b >> 1), pos, slo, shi, k0, k1);
+        wa = (b & 1) ? w.z : w.x;
+        wb = (b & 1) ? w.w : w.y;
       }
-      // ---- the pair's words and bounds U_b ----
-      uint32_t wa[2] = {0, 0}, wb[2] = {0, 0};
-      if (rv && b0 < nblk) {
-        const Philox4 w = philox4x32_10(0x80000000u | (uint32_t)(b0 >> 1), pos, slo, shi, k0, k1);
-        wa[0] = w.x;
-        wb[0] = w.y;
-        wa[1] = w.z;
-        wb[1] = w.w;
+      bar_wait_sleep(&acc_full[a], (u >> 1) & 1);
+      tc_fence_after();
+      if (p.debug & 1) {  // development: the pipeline without the sampler
+        __syncwarp();
+        if (lane == 0) bar_arrive_leader(&acc_empty[a]);
+        continue;
       }
-      float U[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int n = block_len(p.V, b0 + j);
-        if (!rv || n == 0 || !(X[j] > -INFINITY)) {
-          U[j] = -INFINITY;
-          continue;
-        }
-        const float xs = unit_t ? X[j] : __fdiv_rn(X[j], T);
-        const float G = n == NOISE_BLK ? tab[wa[j] >> 22] : block_noise(wa[j], wb[j], (uint32_t)n).G;
-        U[j] = __fadd_rn(xs, G);
-      }
-      const int jf = U[1] > U[0] ? 1 : 0;  // per lane: the block with the larger bound first
-      float bz = -INFINITY;
-      int32_t bv = INT_MAX;
-      auto elem_g = [&](int64_t v, int32_t k, const BlockNoise& bn) {
-        if ((uint32_t)k == bn.p) return bn.G;
-        const Philox4 w = philox4x32_10((uint32_t)(v >> 2), pos, slo, shi, k0, k1);
-        const uint32_t e = (uint32_t)(v & 3);
-        return element_noise_from_word(e == 0 ? w.x : e == 1 ? w.y : e == 2 ? w.z : w.w, bn);
-      };
-      // exact evaluation (block jf first): every element whose RN(x/T) + G_b
-      // can reach M.  A row with no achieved z yet (its first tiles) first
-      // takes z(i*) of block jf's maximum (first index), which prunes the rest
-      // (the TMEM address of tcgen05.ld must be warp-uniform: the warp walks
-      // the blocks in a fixed order, round 0 serving the lanes whose larger
-      // bound is that block, round 1 the others)
-#pragma unroll 1
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = jj & 1;
-        const bool mine = (jj < 2) == (j == jf);
-        // (selects, not runtime indexing: the arrays stay in registers)
-        const float Uj = j ? U[1] : U[0], Xj = j ? X[1] : X[0];
-        const uint32_t waj = j ? wa[1] : wa[0], wbj = j ? wb[1] : wb[0];
-        const bool need = rv && mine && Uj > -INFINITY && Uj >= M;
-        if (!__any_sync(0xffffffffu, need)) continue;
-        float x[NOISE_BLK];
-        tmem_ld32(taddr + j * NOISE_BLK, x);
-        tmem_ld32(taddr + j * NOISE_BLK + 32, x + 32);
-        if (!need) continue;
-        const int n = block_len(p.V, b0 + j);
-        const BlockNoise bn = block_noise(waj, wbj, (uint32_t)n);
-        const float Xs = unit_t ? Xj : __fdiv_rn(Xj, T);
-        const int64_t vb = (b0 + j) * NOISE_BLK;
-        if (!(M > -INFINITY)) {  // seed: z(i*), i* = the first index of the block max X
-          int32_t ks = 0;
-#pragma unroll
-          for (int k = NOISE_BLK - 1; k >= 0; --k)
-            if (k < n && as_logit<DT>(x[k]) == Xj) ks = k;
-          const float z = __fadd_rn(Xs, elem_g(vb + ks, ks, bn));
-          bz = z;
-          bv = (int32_t)(vb + ks);
-          M = z;
-        }
-        uint64_t cand = 0;  // bit k: element k can reach M
-#pragma unroll
-        for (int k = 0; k < NOISE_BLK; ++k) {
-          const float xr = as_logit<DT>(x[k]);
-          const float xs = unit_t ? xr : __fdiv_rn(xr, T);
-          if (k < n && __fadd_rn(xs, bn.G) >= M) cand |= 1ull << k;  // (NaN fails)
-        }
-        while (cand) {
-          const int32_t k = __ffsll((long long)cand) - 1;
-          cand &= cand - 1;
-          float xk = 0.0f;
-#pragma unroll
-          for (int i = 0; i < NOISE_BLK; ++i)
-            if (i == k) xk = x[i];
-          xk = as_logit<DT>(xk);
-          const float xs = unit_t ? xk : __fdiv_rn(xk, T);
-          if (__fadd_rn(xs, bn.G) < M) continue;  // M rose meanwhile
-          const int64_t v = vb + k;
-          const float z = __fadd_rn(xs, elem_g(v, k, bn));
-          if (cand_better(z, (int32_t)v, bz, bv)) {
-            bz = z;
-            bv = (int32_t)v;
-            M = fmaxf(M, z);
-          }
-        }
-      }
-      // the accumulator may be overwritten once every epilogue warp is done
+      float x[NOISE_BLK];
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN + jb * NOISE_BLK;
+      tmem_ld32(taddr, x);
+      tmem_ld32(taddr + 32, x + 32);
+      // the accumulator stays in registers: release it to the MMA right away
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive_leader(&acc_empty[a]);
+      // ---- the block maximum X: rounding is monotone, so the max of the
+      // rounded logits is the rounded max of the accumulators ----
+      bool nan = false;
+      float m = -INFINITY;
+      if (n == NOISE_BLK) {
+        float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < NOISE_BLK; k += 2) {
+          m0 = max_nan(m0, x[k]);
+          m1 = max_nan(m1, x[k + 1]);
+        }
+        m = max_nan(m0, m1);
+      }
+      if (n < NOISE_BLK || m != m) {  // partial block, or a NaN: the careful max
+        m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < NOISE_BLK; ++k)
+          if (k < n) {
+            nan |= x[k] != x[k];
+            if (x[k] > m) m = x[k];
+          }
+      }
+      const float X = n > 0 ? as_logit<DT>(m) : -INFINITY;
+      if (p.dump && rv && n > 0) {
+        const int64_t v0 = b * NOISE_BLK;
+        if (DT == SRT_BF16) {
+          __nv_bfloat16* o = (__nv_bfloat16*)p.dump + r * (int64_t)p.V + v0;
+#pragma unroll
+          for (int k = 0; k < NOISE_BLK; ++k)
+            if (k < n) o[k] = __float2bfloat16_rn(x[k]);
+        } else {
+          float* o = (float*)p.dump + r * (int64_t)p.V + v0;
+#pragma unroll
+          for (int k = 0; k < NOISE_BLK; ++k)
+            if (k < n) o[k] = x[k];
+        }
+      }
+      float M = cur ? unpack_value(cur) : -INFINITY;  // an achieved z of the row (or none)
+      float bz = -INFINITY;
+      int32_t bv = INT_MAX;
+      const float Xs = unit_t ? X : __fdiv_rn(X, T);
+      float U = -INFINITY;  // the block bound RN(X/T) + (bucket bound of G_b)
+      if (rv && n > 0 && X > -INFINITY)
+        U = __fadd_rn(Xs, n == NOISE_BLK ? tab[wa >> 22] : block_noise(wa, wb, (uint32_t)n).G);
+      if (p.debug & 32) U = -INFINITY;
+      if (p.debug & 64) {
+        const unsigned nb = __popc(__ballot_sync(0xffffffffu, U > -INFINITY && U >= M));
+        const unsigned nw = __any_sync(0xffffffffu, U > -INFINITY && U >= M);
+        if (lane == 0) {
+          atomicAdd(&g_lm_stats[0], nb);   // lane-blocks evaluated
+          atomicAdd(&g_lm_stats[1], nw);   // warp-blocks with any evaluation
+          atomicAdd(&g_lm_stats[3], 1ull); // warp-blocks
+        }
+      }
+      if (U > -INFINITY && U >= M && !(p.debug & 16)) {
+        // ---- the block can still hold the row's winner ----
+        const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+        const int64_t vb = b * NOISE_BLK;
+        // z(i*) of an element holding the block maximum (raw max m: its
+        // rounded value is X): an achieved z, which raises the row's bound for
+        // every later tile
+        int32_t ks = 0;
+#pragma unroll
+        for (int k = NOISE_BLK - 1; k >= 0; --k)
+          if (k < n && x[k] == m) ks = k;
+        const float zs = elem_z(Xs, vb + ks, ks, bn, pos, slo, shi, k0, k1, -INFINITY, gstd);
+        bz = zs;
+        bv = (int32_t)(vb + ks);
+        M = fmaxf(M, zs);
+        // can any other element still reach M?  (RN(RN(x/T) + G_b) >= M, a
+        // raw-value prefilter first)
+        const float thr = prefilter_threshold(M, bn.G, T);
+        bool open = false;
+#pragma unroll
+        for (int k = 0; k < NOISE_BLK; ++k) {
+          if (k < n && k != ks && x[k] >= thr) {
+            const float xr = as_logit<DT>(x[k]);
+            const float xs = unit_t ? xr : __fdiv_rn(xr, T);
+            open |= __fadd_rn(xs, bn.G) >= M;
+          }
+        }
+        if (p.debug & 64) atomicAdd(&g_lm_stats[2], (unsigned long long)open);
+        if (open) {
+          // defer the block: its rounded logits go to the row's candidate
+          // list, evaluated exactly by k_lmhead_tail against the row's final
+          // bound; a full list falls back to an inline exact pass
+          const int32_t slot = atomicAdd(&p.cand_n[r], 1);
+          if (slot < p.cand_cap) {
+            const int64_t e = r * (int64_t)p.cand_cap + slot;
+            p.cand_b[e] = (int32_t)b;
+            if (DT == SRT_BF16) {
+              uint4* o = reinterpret_cast<uint4*>((__nv_bfloat16*)p.cand_x + e * NOISE_BLK);
+#pragma unroll
+              for (int k = 0; k < NOISE_BLK; k += 8) {
+                uint4 w;
+                w.x = pack_bf2(x[k], x[k + 1]);
+                w.y = pack_bf2(x[k + 2], x[k + 3]);
+                w.z = pack_bf2(x[k + 4], x[k + 5]);
+                w.w = pack_bf2(x[k + 6], x[k + 7]);
+                o[k / 8] = w;
+              }
+            } else {
+              float4* o = reinterpret_cast<float4*>((float*)p.cand_x + e * NOISE_BLK);
+#pragma unroll
+              for (int k = 0; k < NOISE_BLK; k += 4)
+                o[k / 4] = make_float4(x[k], x[k + 1], x[k + 2], x[k + 3]);
+            }
+          } else {
+#pragma unroll 1
+            for (int k = 0; k < n; ++k) {  // overflow: every element, inline
+              float xk = 0.0f;
+#pragma unroll
+              for (int i = 0; i < NOISE_BLK; ++i)
+                if (i == k) xk = x[i];
+              const float xr = as_logit<DT>(xk);
+              const float xs = unit_t ? xr : __fdiv_rn(xr, T);
+              if (k == ks || __fadd_rn(xs, bn.G) < M) continue;
+              const float z = elem_z(xs, vb + k, k, bn, pos, slo, shi, k0, k1, M, gstd);
+              if (cand_better(z, (int32_t)(vb + k), bz, bv)) {
+                bz = z;
+                bv = (int32_t)(vb + k);
+                M = fmaxf(M, z);
+              }
+            }
+          }
+        }
+      }
       if (__any_sync(0xffffffffu, nan) && lane == 0) set_error(c, SRT_DEV_NONFINITE_LOGIT);
       if (rv && bv != INT_MAX) {
         const unsigned long long pk = pack_cand(bz, bv);
@@ -461,6 +531,69 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
+  }
+}
+
+// The deferred blocks of each row, exactly, against the row's final bound M
+// (the best achieved z over all its tiles -- in practice the head's): one
+// warp per row, two tokens per lane per block.  Every block the GEMM
+// epilogue pruned had U_b < M at the time, and M only grew, so the argmax
+// over the deferred blocks and the epilogue's candidates is the row's.
+template <int DT>
+__global__ void __launch_bounds__(128) k_lmhead_tail(DevCache c, LmParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = *p.total;
+  const float T = p.temperature;
+  const bool unit_t = T == 1.0f;
+  const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+  const float* gstd = c.gbound + 2 * NOISE_BUCKETS + 1;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < total;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t nd = p.cand_n[r];
+    if (nd == 0) continue;
+    const int32_t nc = min(nd, p.cand_cap);
+    const unsigned long long cur = ld_relaxed64(&p.result[r]);
+    float M = cur ? unpack_value(cur) : -INFINITY;
+    const int2 ri = p.rowinfo[r];
+    const uint64_t sid = p.seq_id[ri.x];
+    const uint32_t pos = (uint32_t)ri.y, slo = (uint32_t)sid, shi = (uint32_t)(sid >> 32);
+    float bz = -INFINITY;
+    int32_t bv = INT_MAX;
+    for (int32_t i = 0; i < nc; ++i) {
+      const int64_t e = r * (int64_t)p.cand_cap + i;
+      const int64_t b = p.cand_b[e];
+      const int n = block_len(p.V, b);
+      uint32_t wa, wb;
+      block_words((uint32_t)b, pos, slo, shi, k0, k1, wa, wb);
+      const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 2 * lane + h;
+        if (k >= n) continue;
+        const float x = DT == SRT_BF16
+                            ? __bfloat162float(((const __nv_bfloat16*)p.cand_x)[e * NOISE_BLK + k])
+                            : ((const float*)p.cand_x)[e * NOISE_BLK + k];
+        const float xs = unit_t ? x : __fdiv_rn(x, T);
+        if (!(__fadd_rn(xs, bn.G) >= M)) continue;
+        const int64_t v = b * NOISE_BLK + k;
+        const float z = elem_z(xs, v, k, bn, pos, slo, shi, k0, k1, M, gstd);
+        if (cand_better(z, (int32_t)v, bz, bv)) {
+          bz = z;
+          bv = (int32_t)v;
+        }
+      }
+      M = fmaxf(M, bz);  // (lane-local: a tighter filter for this lane's next elements)
+    }
+    // the warp's best (larger z, then smaller v) -> the row's packed result
+    const unsigned long long mine = bv == INT_MAX ? 0ull : pack_cand(bz, bv);
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(mine >> 32));
+    const uint32_t lo =
+        __reduce_max_sync(0xffffffffu, (uint32_t)(mine >> 32) == hi ? (uint32_t)mine : 0u);
+    const unsigned long long best = ((unsigned long long)hi << 32) | lo;
+    if (lane == 0) {
+      if (best > cur) atomicMax(&p.result[r], best);
+      p.cand_n[r] = 0;  // (clean for the next call)
+    }
   }
 }
 
@@ -495,7 +628,7 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int32_t K, int box
 
 cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const LmHeadArgs& h,
                                  const int2* rowinfo, unsigned long long* result,
-                                 cudaStream_t stream) {
+                                 const LmHeadScratch& sc, cudaStream_t stream) {
   CUtensorMap ma, mb;
   if (!make_map(&ma, h.hidden, h.hidden_rows, h.K, BM) ||
       !make_map(&mb, h.weight, c.V, h.K, BN / 2))
@@ -510,12 +643,40 @@ cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const L
   p.temperature = a.temperature;
   p.result = result;
   p.dump = h.dump;
+  p.cand_x = sc.cand_x;
+  p.cand_b = sc.cand_b;
+  p.cand_n = sc.cand_n;
+  p.cand_cap = sc.cap;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("SRT_LMHEAD_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  p.debug = (uint32_t)dbg;
   const size_t smem = 1024 + (size_t)NST * STAGE_BYTES + 2 * NST * 8 + 4 * 8 + 16 +
-                      NOISE_BUCKETS * 4;
+                      2 * NOISE_BUCKETS * 4;
   auto kern = a.dtype == SRT_BF16 ? k_lmhead_sample<SRT_BF16> : k_lmhead_sample<SRT_F32>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (p.debug & 64) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbolAsync(g_lm_stats, z, sizeof z, 0, cudaMemcpyHostToDevice, stream);
+  }
   kern<<<num_sms() & ~1, THREADS, smem, stream>>>(ma, mb, c, p);  // CTA pairs (cluster of 2)
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (p.debug & 128) {
+  } else if (a.dtype == SRT_BF16)
+    k_lmhead_tail<SRT_BF16><<<num_sms() * 8, 128, 0, stream>>>(c, p);
+  else
+    k_lmhead_tail<SRT_F32><<<num_sms() * 8, 128, 0, stream>>>(c, p);
+  if (p.debug & 64) {
+    unsigned long long z[4];
+    cudaMemcpyFromSymbolAsync(z, g_lm_stats, sizeof z, 0, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    fprintf(stderr, "[lmhead] lane-blocks evaluated %llu, warp-blocks with work %llu of %llu, "
+            "elements evaluated %llu\n", z[0], z[1], z[3], z[2]);
+  }
   return cudaGetLastError();
 }
 

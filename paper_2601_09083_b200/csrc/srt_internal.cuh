@@ -71,7 +71,8 @@ struct DevCache {
   uint32_t* scnt;   // mirrors of their counts, contiguous for enumeration
   unsigned long long* ctr;  // [0] nodes created (+ P roots), [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
-  float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima
+  float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima of
+                  // G64; [2049, 3073) bucket maxima of the single-word Gumbel g(r)
   // Hub child lists: for a node with more than HUB_MIN
   // children, its top HUB_K children by (count desc, token asc), valid while
   // the node's child count and csum are what they were when the list was
@@ -330,9 +331,17 @@ struct LmHeadArgs {
   const void* weight;   // bf16 [V, K]
   void* dump;           // nullable: [rows, V] logits in cfg.logits_dtype
 };
+// per-row lists of the blocks the GEMM epilogue defers to the exact tail
+struct LmHeadScratch {
+  void* cand_x;     // [rows][cap][64] logits (cache dtype)
+  int32_t* cand_b;  // [rows][cap]
+  int32_t* cand_n;  // [rows], zero between calls
+  int32_t cap;
+};
+constexpr int32_t LMHEAD_CAND_CAP = 256;
 cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const LmHeadArgs& h,
                                  const int2* rowinfo, unsigned long long* result,
-                                 cudaStream_t stream);
+                                 const LmHeadScratch& sc, cudaStream_t stream);
 cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
                                 unsigned long long* result, cudaStream_t stream);
 // reference = the unpruned kernel writing sampled[] directly; otherwise the
