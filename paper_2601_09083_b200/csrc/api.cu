@@ -23,7 +23,7 @@ struct srt_cache {
   int2* rowinfo = nullptr;      // verify: per-row (sequence, position)
   unsigned long long* result = nullptr;  // verify: per-row packed winner (pack_cand)
   int64_t row_cap = 0;          // rows the two buffers above can hold
-  LmHeadScratch lm{nullptr, nullptr, nullptr, 0};  // srt_verify_lmhead: deferred blocks
+  LmHeadScratch lm{nullptr, nullptr, nullptr, nullptr, 0};  // srt_verify_lmhead: deferred blocks
   int64_t lm_rows = 0;          // rows lm can hold
   void* path = nullptr;         // srt_verify_path: row lists and walk state
   size_t path_cap = 0;
@@ -198,6 +198,7 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   if (c->hubwork) cudaFreeAsync(c->hubwork, (cudaStream_t)stream);
   if (c->lm.cand_x) cudaFreeAsync(c->lm.cand_x, (cudaStream_t)stream);
   if (c->lm.cand_b) cudaFreeAsync(c->lm.cand_b, (cudaStream_t)stream);
+  if (c->lm.cand_X) cudaFreeAsync(c->lm.cand_X, (cudaStream_t)stream);
   if (c->lm.cand_n) cudaFreeAsync(c->lm.cand_n, (cudaStream_t)stream);
   delete c;
   return SRT_OK;
@@ -349,6 +350,7 @@ srt_status verify_lmhead_scan(srt_cache* c, const VerifyArgs& a, const LmHeadArg
     if (c->lm.cand_x) {
       SRT_CUDA(cudaFreeAsync(c->lm.cand_x, stream), "cudaFreeAsync(lm)");
       SRT_CUDA(cudaFreeAsync(c->lm.cand_b, stream), "cudaFreeAsync(lm)");
+      SRT_CUDA(cudaFreeAsync(c->lm.cand_X, stream), "cudaFreeAsync(lm)");
       SRT_CUDA(cudaFreeAsync(c->lm.cand_n, stream), "cudaFreeAsync(lm)");
     }
     const int64_t cap = std::max<int64_t>(rows_max, 4096);
@@ -357,6 +359,8 @@ srt_status verify_lmhead_scan(srt_cache* c, const VerifyArgs& a, const LmHeadArg
     SRT_CUDA(cudaMallocAsync(&c->lm.cand_x, (size_t)cap * LMHEAD_CAND_CAP * 64 * esz, stream),
              "cudaMallocAsync(lm candidates)");
     SRT_CUDA(cudaMallocAsync((void**)&c->lm.cand_b, (size_t)cap * LMHEAD_CAND_CAP * 4, stream),
+             "cudaMallocAsync(lm candidates)");
+    SRT_CUDA(cudaMallocAsync((void**)&c->lm.cand_X, (size_t)cap * LMHEAD_CAND_CAP * 4, stream),
              "cudaMallocAsync(lm candidates)");
     SRT_CUDA(cudaMallocAsync((void**)&c->lm.cand_n, (size_t)cap * 4, stream),
              "cudaMallocAsync(lm candidates)");

@@ -234,6 +234,7 @@ struct LmParams {
   void* dump;                  // nullable [rows, V] logits
   void* cand_x;                // [rows][cand_cap][64] deferred blocks' rounded logits
   int32_t* cand_b;             // [rows][cand_cap] their block indices
+  float* cand_X;               // [rows][cand_cap] their maxima (rounded)
   int32_t* cand_n;             // [rows] deferred blocks (may exceed cand_cap: overflow)
   int32_t cand_cap;
   uint32_t debug;              // development: 1 = epilogue skips its work, 2 = no MMAs,
@@ -481,6 +482,7 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           if (slot < p.cand_cap) {
             const int64_t e = r * (int64_t)p.cand_cap + slot;
             p.cand_b[e] = (int32_t)b;
+            p.cand_X[e] = X;
             if (DT == SRT_BF16) {
               uint4* o = reinterpret_cast<uint4*>((__nv_bfloat16*)p.cand_x + e * NOISE_BLK);
 #pragma unroll
@@ -541,6 +543,9 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 // over the deferred blocks and the epilogue's candidates is the row's.
 template <int DT>
 __global__ void __launch_bounds__(128) k_lmhead_tail(DevCache c, LmParams p) {
+  __shared__ float tab[NOISE_BUCKETS];
+  for (int i = threadIdx.x; i < NOISE_BUCKETS; i += blockDim.x) tab[i] = c.gbound[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t total = *p.total;
   const float T = p.temperature;
@@ -559,30 +564,53 @@ __global__ void __launch_bounds__(128) k_lmhead_tail(DevCache c, LmParams p) {
     const uint32_t pos = (uint32_t)ri.y, slo = (uint32_t)sid, shi = (uint32_t)(sid >> 32);
     float bz = -INFINITY;
     int32_t bv = INT_MAX;
-    for (int32_t i = 0; i < nc; ++i) {
+    for (int32_t i0 = 0; i0 < nc; i0 += 32) {
+      // lane i: deferred block i0 + i -- its bound against the row's final M
+      const int32_t i = i0 + lane;
       const int64_t e = r * (int64_t)p.cand_cap + i;
-      const int64_t b = p.cand_b[e];
-      const int n = block_len(p.V, b);
-      uint32_t wa, wb;
-      block_words((uint32_t)b, pos, slo, shi, k0, k1, wa, wb);
-      const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int k = 2 * lane + h;
-        if (k >= n) continue;
-        const float x = DT == SRT_BF16
-                            ? __bfloat162float(((const __nv_bfloat16*)p.cand_x)[e * NOISE_BLK + k])
-                            : ((const float*)p.cand_x)[e * NOISE_BLK + k];
-        const float xs = unit_t ? x : __fdiv_rn(x, T);
-        if (!(__fadd_rn(xs, bn.G) >= M)) continue;
-        const int64_t v = b * NOISE_BLK + k;
-        const float z = elem_z(xs, v, k, bn, pos, slo, shi, k0, k1, M, gstd);
-        if (cand_better(z, (int32_t)v, bz, bv)) {
-          bz = z;
-          bv = (int32_t)v;
-        }
+      int64_t b = 0;
+      float U = -INFINITY;
+      if (i < nc) {
+        b = p.cand_b[e];
+        const float X = p.cand_X[e];
+        const int n = block_len(p.V, b);
+        uint32_t wa, wb;
+        block_words((uint32_t)b, pos, slo, shi, k0, k1, wa, wb);
+        const float G = n == NOISE_BLK ? tab[wa >> 22] : block_noise(wa, wb, (uint32_t)n).G;
+        U = __fadd_rn(unit_t ? X : __fdiv_rn(X, T), G);
       }
-      M = fmaxf(M, bz);  // (lane-local: a tighter filter for this lane's next elements)
+      unsigned surv = __ballot_sync(0xffffffffu, U > -INFINITY && U >= M);
+      while (surv) {  // the surviving blocks, exactly, by the whole warp
+        const int j = __ffs(surv) - 1;
+        surv &= surv - 1;
+        const int64_t bj = __shfl_sync(0xffffffffu, b, j);
+        const int64_t ej = r * (int64_t)p.cand_cap + i0 + j;
+        const int n = block_len(p.V, bj);
+        uint32_t wa, wb;
+        block_words((uint32_t)bj, pos, slo, shi, k0, k1, wa, wb);
+        const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * lane + h;
+          if (k >= n) continue;
+          const float x = DT == SRT_BF16
+                              ? __bfloat162float(((const __nv_bfloat16*)p.cand_x)[ej * NOISE_BLK + k])
+                              : ((const float*)p.cand_x)[ej * NOISE_BLK + k];
+          const float xs = unit_t ? x : __fdiv_rn(x, T);
+          if (!(__fadd_rn(xs, bn.G) >= M)) continue;
+          const int64_t v = bj * NOISE_BLK + k;
+          const float z = elem_z(xs, v, k, bn, pos, slo, shi, k0, k1, M, gstd);
+          if (cand_better(z, (int32_t)v, bz, bv)) {
+            bz = z;
+            bv = (int32_t)v;
+          }
+        }
+        // the warp's best z tightens the bound for the remaining blocks
+        float wm = bz;
+        for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        M = fmaxf(M, wm);
+        surv &= __ballot_sync(0xffffffffu, U > -INFINITY && U >= M);
+      }
     }
     // the warp's best (larger z, then smaller v) -> the row's packed result
     const unsigned long long mine = bv == INT_MAX ? 0ull : pack_cand(bz, bv);
@@ -645,6 +673,7 @@ cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const L
   p.dump = h.dump;
   p.cand_x = sc.cand_x;
   p.cand_b = sc.cand_b;
+  p.cand_X = sc.cand_X;
   p.cand_n = sc.cand_n;
   p.cand_cap = sc.cap;
   static int dbg = -1;

@@ -335,6 +335,7 @@ struct LmHeadArgs {
 struct LmHeadScratch {
   void* cand_x;     // [rows][cap][64] logits (cache dtype)
   int32_t* cand_b;  // [rows][cap]
+  float* cand_X;    // [rows][cap]
   int32_t* cand_n;  // [rows], zero between calls
   int32_t cap;
 };
