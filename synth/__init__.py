@@ -27,7 +27,8 @@ import numpy as np
 
 __all__ = ["Workload", "zipf_tokens", "make_templates", "sibling_stream", "drift",
            "make_workload", "random_logits_np", "bf16_bits", "gap_profile", "FIG3_VOCAB",
-           "fig3_sentences", "splitmix64"]
+           "fig3_sentences", "splitmix64", "RolloutStreams", "policy_row_edits",
+           "SimPolicy"]
 
 
 def splitmix64(x: int) -> int:
@@ -187,3 +188,117 @@ def fig3_sentences():
     s += ["the cat sit on the sofa"] * 1
     s += ["the cat eat the fish"] * 2
     return [np.asarray([FIG3_VOCAB[w] for w in x.split()], np.int32) for x in s]
+
+
+# ---- rollout-loop inputs (the slot scheduler) ---------------
+# Streams are keyed, not drawn in sequence, so any subset of (prompt, epoch,
+# sample) can be generated in any order and every mode of a simulation sees
+# the same rollouts.
+
+_U64 = np.uint64
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser over a uint64 array (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        z = x + _U64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> _U64(30))) * _U64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> _U64(27))) * _U64(0x94D049BB133111EB)
+        return z ^ (z >> _U64(31))
+
+
+def _unit(x: np.ndarray) -> np.ndarray:
+    """uint64 -> float64 uniform in [0, 1) from the top 53 bits."""
+    return (x >> _U64(11)).astype(np.float64) * (1.0 / (1 << 53))
+
+
+class RolloutStreams:
+    """Ground-truth token streams of a dataset's rollouts: prompt p's template
+    at epoch e drifts from epoch e - 1 (5% edits), sample j of (p, e) is a
+    sibling stream of that template.  Epoch 0 is the history a warm cache
+    holds; run-ahead rollouts are further samples j >= K of the same
+    (p, e) (they are drawn from the current policy)."""
+
+    def __init__(self, seed: int, V: int, median: int, cap: int):
+        self.seed, self.V, self.median, self.cap = seed, V, median, cap
+        self.perm = np.random.default_rng([seed, 0]).permutation(V).astype(np.int32)
+        self._tmpl = {}
+
+    def template(self, p: int, e: int) -> np.ndarray:
+        if (p, e) not in self._tmpl:
+            if e == 0:
+                rng = np.random.default_rng([self.seed, 1, p])
+                self._tmpl[(p, e)] = make_templates(rng, 1, self.V, self.perm, self.median,
+                                                    self.cap)[0]
+            else:
+                rng = np.random.default_rng([self.seed, 2, p, e])
+                self._tmpl[(p, e)] = drift(rng, self.template(p, e - 1), self.V, self.perm)
+        return self._tmpl[(p, e)]
+
+    def stream(self, p: int, e: int, j: int) -> np.ndarray:
+        rng = np.random.default_rng([self.seed, 3, p, e, j])
+        return sibling_stream(rng, self.template(p, e), self.V, self.perm, self.cap)
+
+
+def policy_row_edits(seed: int, keys, pos, heads, V: int, profile: str = "rl-mix"):
+    """The policy stand-in of the rollout simulation, as sparse edits of an
+    all-zero logits row: the row of sequence `key` predicting position `pos`
+    puts its head token (the ground truth there) at +gap and 3 distractors
+    below it.  Every value is a function of (seed, key, pos) only, so the
+    committed stream does not depend on the drafts (losslessness makes the
+    modes' rollouts identical).  Returns (tokens [n, 4] int64, values [n, 4]
+    float32, already representable in bf16)."""
+    keys = np.asarray(keys, np.uint64)
+    pos = np.asarray(pos, np.int64).astype(np.uint64)
+    heads = np.asarray(heads, np.int64)
+    with np.errstate(over="ignore"):
+        base = _mix64(keys * _U64(0xD1B54A32D192ED03) ^ pos * _U64(0x8CB92BA72F3D8DD7)
+                      ^ _U64(seed & (2 ** 64 - 1)))
+        u = [_unit(_mix64(base + _U64(i))) for i in range(8)]
+    if profile == "rl-mix":
+        conf = u[0] < 0.7
+        gap = np.where(conf, 18 + 6 * u[1], 12 + 6 * u[1])
+        offs = [np.where(conf, 5 + 4 * u[2 + k], 0.5 + 3.5 * u[2 + k]) for k in range(3)]
+    else:
+        g = {"peaked": 26.0, "moderate": 18.0}[profile]
+        gap = np.full(len(keys), g)
+        offs = [0.5 + 3.5 * u[2 + k] for k in range(3)]
+    tok = np.empty((len(keys), 4), np.int64)
+    val = np.empty((len(keys), 4), np.float32)
+    tok[:, 0] = heads
+    val[:, 0] = gap
+    for k in range(3):
+        # offset 1 + k + 3m in [1, V - 1]: never the head, distinct per k (mod 3)
+        m = (u[5 + k] * ((V - 4) // 3)).astype(np.int64)
+        tok[:, k + 1] = (heads + 1 + k + 3 * m) % V
+        val[:, k + 1] = gap - offs[k]
+    # bf16-representable values: both engines see the same bits
+    val = (bf16_bits(val).astype(np.uint32) << 16).view(np.float32)
+    return tok, val
+
+
+class SimPolicy:
+    """The rollout simulation's policy stand-in for one tick's draft layout:
+    per logits row (sequence s = slots[i]; the root row predicts position
+    len[s], draft node j predicts len[s] + depth_j) the edits of
+    `policy_row_edits` with the head at the rollout's ground-truth token
+    (clamped to its last token).  truth: [S, W] padded table, truth_len: [S].
+    Returns (tokens [rows, 4], values [rows, 4]) in row order."""
+
+    def __init__(self, seed: int, V: int, profile: str = "rl-mix"):
+        self.seed, self.V, self.profile = seed, V, profile
+
+    def __call__(self, slots, row_offsets, draft_len, draft_depth, seq_len, seq_key, truth,
+                 truth_len):
+        slots = np.asarray(slots, np.int64)
+        n = len(slots)
+        B = draft_depth.shape[1]
+        dep = np.zeros((n, B + 1), np.int64)
+        dep[:, 1:] = draft_depth
+        valid = np.arange(B + 1)[None, :] <= np.asarray(draft_len, np.int64)[:, None]
+        si = np.broadcast_to(slots[:, None], (n, B + 1))[valid]   # row order
+        pos = np.asarray(seq_len, np.int64)[si] + dep[valid]
+        assert len(si) == int(row_offsets[n])
+        heads = truth[si, np.minimum(pos, np.asarray(truth_len, np.int64)[si] - 1)]
+        return policy_row_edits(self.seed, np.asarray(seq_key, np.uint64)[si], pos, heads,
+                                self.V, self.profile)

@@ -1,100 +1,82 @@
-"""Synthetic Fig. 5: mean accepted tokens per
-decoding step for three cache-maintenance strategies, driven through the
-libsrt kernels on a DAPO-shaped synthetic batch (1024 fresh rollouts of 64
-prompts x 16 samples, V = 151,936, Bmax = 32, D = 32):
+"""Synthetic Fig. 5 through the libsrt kernels,
+with the rollout loop's slot scheduler (paper_2601_09083_b200/rollout.py):
+a DAPO-shaped run of several training steps (B prompts x K samples per step,
+one slot per real sequence, long-tailed rollout lengths), each tick one SRT
+step (draft -> policy stand-in -> verify -> insert) over the occupied slots,
+for the paper's three cache-maintenance strategies:
 
-  history-only   the cache holds only completed responses of the previous
-                 epoch; nothing is inserted while the batch decodes
-                 (He et al. 2025, the paper's comparison);
-  online (SRT)   + every step's committed tokens are inserted (P:L151 first
-                 source: running rollouts);
-  online + run-ahead  + before the batch starts, run-ahead rollouts of the same
-                 prompts (generated in an earlier batch's bubbles, P:L151
-                 second source) were inserted.
+  history-only     the cache gets completed responses at the end of each
+                   training step only (the paper's comparison);
+  online (SRT)     every tick's committed tokens are inserted;
+  online+run-ahead + the slots freed by finished sequences (the bubbles of
+                   the long tail) decode rollouts of the next step's
+                   prompts (the look-ahead window), inserted online and
+                   discarded at step end.
 
-Only the ORDERING is comparable with the paper (its values are absent, O16);
-the logits are the bench stand-in (the ground-truth continuation is the
-policy's preferred token, rl-mix gaps), so acceptance measures how often the
-tree predicts the rollout.
+Plain decoding's step time is the longest rollout of the step (one token per
+tick; tests/test_rollout_sim.py pins this on the oracle engine), reported as
+the baseline.  Only the ORDERING of the strategies is comparable with the
+paper (its values are absent, O16).
 
-    python tools/fig5_sim.py [--steps 48] [--runahead 2] > profiles/r01_fig5_sim.json
+    python tools/fig5_sim.py [--steps 3] > profiles/r02_fig5_sim.json
 """
 import argparse
 import json
 import os
 import sys
+import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-import torch  # noqa: E402
-
-import bench  # noqa: E402
-
-CFG = dict(V=151936, prompts=64, samples=16, active=1024, Bmax=32, D=32, L=8, median=3000,
-           cap=8192, act_cap=8192, prior_epochs=1, node_capacity=1 << 27)
+import synth  # noqa: E402
+from paper_2601_09083_b200.rollout import GpuEngine, RolloutSim, SimConfig, summarize  # noqa: E402
 
 
-def run_mode(mode: str, steps: int, runahead: int, seed: int):
-    cfg = dict(CFG)
-    if mode == "online+runahead":
-        cfg["runahead"] = dict(first=0, prompts=cfg["prompts"], per=runahead, spans=0, lo=1, hi=1)
-    wl = bench.Workload(cfg, seed)
-    wl.t0[:] = 0  # fresh rollouts: nothing of this epoch is in the cache yet
-    run = bench.GpuRun(wl, "bf16", "rl-mix", seed)
-    gr = run.groups[0]
-    gr.ra = None  # run-ahead rollouts go in once, before the batch (below)
-    if mode == "online+runahead":
-        streams = wl.w.runahead
-        m = max(len(t) for _, t in streams)
-        tab = np.zeros((len(streams), m), np.int32)
-        for i, (_, t) in enumerate(streams):
-            tab[i, :len(t)] = t
-        dev = gr.dev
-        gr.cache.insert(torch.tensor([p for p, _ in streams], dtype=torch.int32, device=dev),
-                        torch.from_numpy(tab).to(dev),
-                        torch.zeros(len(streams), dtype=torch.int32, device=dev),
-                        torch.tensor([len(t) for _, t in streams], dtype=torch.int32, device=dev))
-    acc, com, match = [], [], []
-    seed_k = bench.step_seed(seed, 0)
-    for k in range(steps):
-        gr.draft()
-        gr.standin()
-        gr.cache.verify(gr.logits, gr.d, gr.seq_id, seed_k, gr.seq_tok, gr.seq_len, gr.max_new,
-                        out=gr.v, rows=gr.rows_max)
-        if mode != "history-only":
-            gr.cache.insert(gr.prompt_id, gr.seq_tok, gr.t_before, gr.seq_len, cursor=gr.cursor)
-        acc.append(float(gr.v.accept_len.float().mean().item()))
-        com.append(float(gr.v.n_commit.float().mean().item()))
-        match.append(float((gr.d.match_len > 0).float().mean().item()))
-    bits, st = run.status()
-    assert bits == 0, bits
-    del run, gr
-    torch.cuda.empty_cache()
-    return {"mean_accepted_per_step": float(np.mean(acc)),
-            "mean_committed_per_step": float(np.mean(com)),
-            "fraction_of_steps_with_a_match": float(np.mean(match)),
-            "accepted_per_step_curve": [round(a, 4) for a in acc]}
+def run_mode(mode, ra, a):
+    cfg = SimConfig(V=151936, D=a.depth, L=8, Bmax=32, prompts_per_step=a.prompts,
+                    samples=a.samples, steps=a.steps, mode=mode, run_ahead=ra, median=a.median,
+                    cap=a.cap, seed=a.seed, ra_per_prompt=a.ra_per_prompt,
+                    node_capacity=1 << 28)
+    t = time.time()
+    sim = RolloutSim(cfg, GpuEngine(cfg, synth.SimPolicy(cfg.seed, cfg.V)),
+                     synth.RolloutStreams(cfg.seed, cfg.V, cfg.median, cfg.cap))
+    sim.run()
+    out = summarize(sim.reports)
+    out["wall_s"] = round(time.time() - t, 1)
+    out["baseline_ticks_per_step"] = [
+        max(len(v) for k, v in sim.rollouts.items() if (k >> 44) & 0xFFFFF == s)
+        for s in range(cfg.steps)]
+    del sim
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=48)
-    ap.add_argument("--runahead", type=int, default=2, help="run-ahead rollouts per prompt")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--prompts", type=int, default=64)
+    ap.add_argument("--samples", type=int, default=16)
+    ap.add_argument("--median", type=int, default=1500)
+    ap.add_argument("--cap", type=int, default=6000)
+    ap.add_argument("--depth", type=int, default=16)
+    ap.add_argument("--ra-per-prompt", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
     a = ap.parse_args()
-    out = {"workload": "fig5-sim: 64 prompts x 16 samples (1024 fresh rollouts), V=151936, "
-                       f"Bmax=32, D=32, L=8, median 3000 tokens, {a.steps} decoding steps, "
-                       f"{a.runahead} run-ahead rollouts per prompt",
+    out = {"workload": f"fig5-sim: {a.steps} training steps x {a.prompts} prompts x {a.samples} "
+                       f"samples (one slot per real sequence), V=151936, Bmax=32, D={a.depth}, "
+                       f"L=8, rollout length LogNormal(median {a.median}, 0.9) <= {a.cap}, one "
+                       f"warm epoch; run-ahead: <= {a.ra_per_prompt} rollouts per look-ahead "
+                       f"prompt (the next step's batch)",
            "modes": {}}
-    for mode in ("history-only", "online", "online+runahead"):
-        out["modes"][mode] = run_mode(mode, a.steps, a.runahead, a.seed)
-        print(f"[fig5] {mode}: {out['modes'][mode]['mean_accepted_per_step']:.3f} accepted/step",
+    for mode, ra, name in (("history_only", False, "history-only"), ("srt", False, "online"),
+                           ("srt", True, "online+runahead")):
+        out["modes"][name] = run_mode(mode, ra, a)
+        print(f"[fig5] {name}: {out['modes'][name]['mean_accepted']:.3f} accepted/step, "
+              f"{out['modes'][name]['ticks']} ticks, {out['modes'][name]['wall_s']} s",
               file=sys.stderr, flush=True)
     m = out["modes"]
-    out["ordering_holds"] = (m["history-only"]["mean_accepted_per_step"]
-                             < m["online"]["mean_accepted_per_step"]
-                             < m["online+runahead"]["mean_accepted_per_step"])
+    acc = {k: v["mean_accepted"] for k, v in m.items()}
+    out["ordering_holds"] = acc["history-only"] < acc["online"] < acc["online+runahead"]
     print(json.dumps(out, indent=1))
 
 
