@@ -7,10 +7,14 @@ missing, the calls raise.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libsrt.so"
+# development A/B runs load another build of the same ABI (tools/*_probe*)
+if os.environ.get("SRT_LIB"):
+    LIB_PATH = Path(os.environ["SRT_LIB"]).resolve()
 
 SRT_OK, SRT_ERR_INVALID_CONFIG, SRT_ERR_INVALID_ARG, SRT_ERR_CUDA, SRT_ERR_DEVICE = range(5)
 STATUS_NAMES = {0: "SRT_OK", 1: "SRT_ERR_INVALID_CONFIG", 2: "SRT_ERR_INVALID_ARG",

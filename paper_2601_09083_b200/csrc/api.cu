@@ -122,6 +122,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_scnt = off;    off = align_up(off + W * 4);
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
   const size_t o_status = off;  off = align_up(off + 4);
+  const size_t o_sched = off;   off = align_up(off + 2 * 4);
   const size_t o_gb = off;      off = align_up(off + (3 * NOISE_BUCKETS + 1) * 4);
   // hub child lists: ~1 slot per 16 nodes' worth of hash, at least 2^12
   size_t HC = 4096;
@@ -159,6 +160,7 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.scnt = (uint32_t*)(b + o_scnt);
   d.ctr = (unsigned long long*)(b + o_ctr);
   d.status = (uint32_t*)(b + o_status);
+  d.sched = (uint32_t*)(b + o_sched);
   d.gbound = (float*)(b + o_gb);
   d.HC = (uint32_t)HC;
   {
@@ -176,7 +178,8 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.dirty_n = d.dirty + DIRTY_CAP;
   c->scratch = nullptr;
   c->scratch_cap = 0;
-  if ((e = launch_init_cache(d, stream)) != cudaSuccess ||
+  if ((e = cudaMemsetAsync(d.sched, 0, 2 * 4, stream)) != cudaSuccess ||
+      (e = launch_init_cache(d, stream)) != cudaSuccess ||
       (e = launch_noise_bounds(d, stream)) != cudaSuccess) {
     cudaFreeAsync(c->pool, stream);
     delete c;

@@ -33,6 +33,12 @@
 #include "noise.cuh"
 #include "srt_internal.cuh"
 
+#ifdef SRT_SCAN_PROF
+#define SRT_SCAN_PROF_ON 1
+#else
+#define SRT_SCAN_PROF_ON 0
+#endif
+
 namespace srt {
 
 namespace {
@@ -53,6 +59,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // (a suspend-time hint of ~10 ms was measured 0.5 % slower on the scan)
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -110,6 +117,12 @@ __device__ __forceinline__ uint32_t fkey(float x) {
 }
 __device__ __forceinline__ float key_value(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// block_len for V < 2^31 in 32-bit arithmetic (the hot loops)
+__device__ __forceinline__ int block_len32(int32_t V, int32_t b) {
+  const int32_t rem = V - b * NOISE_BLK;
+  return rem <= 0 ? 0 : (rem < NOISE_BLK ? rem : NOISE_BLK);
 }
 
 template <int DT>
@@ -171,9 +184,13 @@ struct ScanParams {
   int32_t V;
   int32_t nblk;                // ceil(V / 64)
   uint32_t sum_bytes;          // row summary bytes (nblk floats, 128-aligned)
-  uint32_t debug;              // development only (SRT_SCAN_DEBUG=8 prints the launch)
+  uint32_t debug;              // development only (SRT_SCAN_DEBUG: 8 prints the launch; 16 / 32
+                               // skip the tail / stream work, timing probes with wrong results;
+                               // 64: CTA 0 prints per-warp wait cycles)
   uint32_t l2_hint;            // 0 = default policy, 1 = evict_first on the streamed rows
   uint32_t spin;               // 1 = stream warps poll the ring with test_wait
+  uint32_t* sched;             // nullable: [0] next row to claim, [1] CTAs past the end (both 0
+                               // between launches); null = static rows blockIdx.x + k gridDim.x
 };
 
 // Warp roles: warp 0 = producer, warps 1..NSW = stream (NG groups taking
@@ -182,6 +199,7 @@ template <int DT, int NSW, int NT, int NST, int NS, uint32_t CHUNK, int NG>
 __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c, ScanParams a) {
   constexpr int GW = NSW / NG;  // warps per stream group
   static_assert(NSW % NG == 0, "stream groups must be equal");
+  static_assert(NT >= 2, "the tail needs the M warp and at least one worker");
   // each ring stage must always be consumed by the same group, in order: a
   // parity wait cannot tell use k from use k + 2
   static_assert(NST % NG == 0, "ring stages must map to one stream group each");
@@ -189,6 +207,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   constexpr int BLKB = NOISE_BLK * ESZ;  // bytes per block
   constexpr int PAIRB = 2 * BLKB;
   constexpr int PAIRS_PER_CHUNK = CHUNK / PAIRB;
+  constexpr int NR = NST + 2;  // row ids the producer may run ahead by (see the stream loop)
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;                                            // [NST][CHUNK]
   unsigned char* sums = ring + NST * CHUNK;                              // [NS][sum_bytes]
@@ -197,14 +216,41 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   uint64_t* ring_empty = ring_full + NST;                                // [NST]
   uint64_t* sum_ready = ring_empty + NST;                                // [NS]
   uint64_t* sum_free = sum_ready + NS;                                   // [NS]
-  unsigned long long* p1key = reinterpret_cast<unsigned long long*>(sum_free + NS);  // [NS]
+  uint64_t* m_ready = sum_free + NS;                                     // [NS]
+  unsigned long long* p1key = reinterpret_cast<unsigned long long*>(m_ready + NS);  // [NS]
   unsigned long long* rowhdr = p1key + NS;                               // [NS]
-  uint32_t* p1cnt = reinterpret_cast<uint32_t*>(rowhdr + NS);            // [NS]
+  int64_t* rowid = reinterpret_cast<int64_t*>(rowhdr + NS);              // [NS] row of a summary
+  int64_t* row_of = rowid + NS;                                          // [NR] row of the u-th row
+  uint32_t* p1cnt = reinterpret_cast<uint32_t*>(row_of + NR);            // [NS]
   uint32_t* rowM = p1cnt + ((NS + 3) & ~3);                              // [NS] shared M keys
   float* tab = reinterpret_cast<float*>(rowM + ((NS + 3) & ~3));         // [1024]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t total = *a.total;
+  // (built with -DSRT_SCAN_PROF and debug 64: CTA 0's warps print the cycles
+  // they spent in each wait; tools/build_ab.sh)
+#ifdef SRT_SCAN_PROF
+  const bool prof = (a.debug & 64) && blockIdx.x == 0;
+#else
+  constexpr bool prof = false;
+#endif
+  long long tw0 = 0, tw1 = 0, tw2 = 0, t_start = prof ? clock64() : 0;
+  unsigned long long g_start = 0;
+  if (SRT_SCAN_PROF_ON && (a.debug & 128)) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+#define SRT_TIMED(acc, stmt)                     \
+  do {                                           \
+    if (prof) {                                  \
+      const long long _t = clock64();            \
+      stmt;                                      \
+      acc += clock64() - _t;                     \
+    } else {                                     \
+      stmt;                                      \
+    }                                            \
+  } while (0)
+#define SRT_PROF_PRINT(role)                                                                 \
+  if (SRT_SCAN_PROF_ON && prof && lane == 0)                                                 \
+    printf("[scan prof] warp %2d %-8s total %lld  w0 %lld  w1 %lld  w2 %lld\n", wid, role,   \
+           clock64() - t_start, tw0, tw1, tw2)
   const int64_t row_bytes = (int64_t)a.V * ESZ;
   const uint32_t nch = (uint32_t)((row_bytes + CHUNK - 1) / CHUNK);
   const float T = a.temperature;
@@ -219,7 +265,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sum_ready[s], 1);
-      mbar_init(&sum_free[s], NT);
+      mbar_init(&sum_free[s], NT - 1);  // the workers
+      mbar_init(&m_ready[s], 1);
       p1key[s] = 0;
       p1cnt[s] = 0;
       rowM[s] = 0;
@@ -233,14 +280,47 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     if (lane == 0) {
       uint64_t pol = 0;
       if (a.l2_hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      // Rows are claimed one at a time from the launch's shared counter
+      // (a.sched; else the static sequence blockIdx.x, + gridDim.x, ...), so
+      // a CTA that met slow rows takes fewer of them.  The u-th row's id goes
+      // to row_of[u % NR] before its first chunk is issued (the stream warps
+      // read it after that chunk's full barrier); past the last row, one
+      // empty arrival per stream group carries the end (row id -1).
       uint64_t kc = 0;
-      for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+      int64_t si = blockIdx.x;
+      auto claim = [&]() -> int64_t {
+        if (a.sched) return (int64_t)atomicAdd(a.sched, 1u);
+        const int64_t r = si;
+        si += gridDim.x;
+        return r;
+      };
+      int64_t next = claim();  // claimed one row ahead: the atomic's round trip
+                               // overlaps the issue of the current row
+      for (int64_t u = 0;; ++u) {
+        const int64_t i = next;
+        if (i < total) next = claim();
+        if (i >= total) {
+          row_of[u % NR] = -1;
+          for (int g = 0; g < NG; ++g, ++kc) {
+            const int s = (int)(kc % NST);
+            const uint32_t use = (uint32_t)(kc / NST);
+            if (use > 0) mbar_wait(&ring_empty[s], (use - 1) & 1);
+            mbar_arrive(&ring_full[s]);
+          }
+          // the last CTA past the end resets the counter for the next launch
+          if (a.sched && atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+            atomicExch(a.sched, 0u);
+            atomicExch(a.sched + 1, 0u);
+          }
+          break;
+        }
         const int64_t row = a.row_list ? a.row_list[i] : i;
+        row_of[u % NR] = row;
         const char* base = (const char*)a.logits + row * row_bytes;
         for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
           const int s = (int)(kc % NST);
           const uint32_t use = (uint32_t)(kc / NST);
-          if (use > 0) mbar_wait(&ring_empty[s], (use - 1) & 1);
+          if (use > 0) SRT_TIMED(tw0, mbar_wait(&ring_empty[s], (use - 1) & 1));
           const int64_t left = row_bytes - (int64_t)ch * CHUNK;
           const uint32_t nb = (uint32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
           mbar_arrive_expect_tx(&ring_full[s], nb);
@@ -250,6 +330,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
             tma_load_1d(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s]);
         }
       }
+      SRT_PROF_PRINT("producer");
     }
     return;
   }
@@ -259,11 +340,24 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     const int grp = (wid - 1) / GW, w = (wid - 1) % GW;
     uint64_t kc = 0;
     int64_t u = 0;
-    for (int64_t i = blockIdx.x; i < total; i += gridDim.x, ++u) {
-      const int64_t row = a.row_list ? a.row_list[i] : i;
+    for (;; ++u) {
+      // the row id: read after this group's first chunk of the row has landed
+      // (the producer wrote it before issuing that chunk, and can be at most
+      // NR - 1 rows ahead: it reuses a stage only after both groups consumed
+      // a later chunk than their first one of row u)
+      const uint64_t kf = kc + (uint64_t)((grp - (int)(kc % NG) + NG) % NG);
+      mbar_wait(&ring_full[kf % NST], (uint32_t)((kf / NST) & 1));
+      const int64_t row = row_of[u % NR];
       const int sb = (int)(u % NS);
       const uint32_t suse = (uint32_t)(u / NS);
-      if (suse > 0) mbar_wait(&sum_free[sb], (suse - 1) & 1);
+      if (suse > 0) SRT_TIMED(tw1, mbar_wait(&sum_free[sb], (suse - 1) & 1));
+      if (row < 0) {  // past the last row: pass the end on to the tail
+        if (lane == 0 && atomicAdd(&p1cnt[sb], 1u) == NSW - 1) {
+          rowid[sb] = -1;
+          mbar_arrive(&sum_ready[sb]);
+        }
+        break;
+      }
       float* U = reinterpret_cast<float*>(sums + sb * a.sum_bytes);
       const int2 ri = a.rowinfo[row];
       const uint64_t sid = a.seq_id[ri.x];
@@ -275,17 +369,18 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         if (NG > 1 && (int)(kc % NG) != grp) continue;  // the other group's chunk
         const int s = (int)(kc % NST);
         if (a.spin) mbar_spin(&ring_full[s], (uint32_t)((kc / NST) & 1));
-        else mbar_wait(&ring_full[s], (uint32_t)((kc / NST) & 1));
-        const int64_t left = row_bytes - (int64_t)ch * CHUNK;
-        const int32_t nb = (int32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
-        const int32_t npairs = (nb + PAIRB - 1) / PAIRB;
+        else SRT_TIMED(tw0, mbar_wait(&ring_full[s], (uint32_t)((kc / NST) & 1)));
+        const int32_t left = (int32_t)(row_bytes - (int64_t)ch * CHUNK);
+        const int32_t nb = left < (int32_t)CHUNK ? left : (int32_t)CHUNK;
+        const int32_t npairs = (a.debug & 32) ? 0 : (nb + PAIRB - 1) / PAIRB;  // (32: timing probe)
         const unsigned char* st = ring + s * CHUNK;
+        // (the Philox call is issued next to the shared loads, so its ALU work
+        // hides their latency; measured faster than drawing it before the wait
+        // and releasing the stage before the bound arithmetic)
         for (int32_t pi = w * 32 + lane; pi < npairs; pi += GW * 32) {
           const uint32_t gp = ch * PAIRS_PER_CHUNK + (uint32_t)pi;  // pair index in the row
-          const int64_t e0 = (int64_t)gp * 2 * NOISE_BLK;             // first element
-          const int nA = block_len(a.V, 2 * (int64_t)gp);
-          const int nB = block_len(a.V, 2 * (int64_t)gp + 1);
-          (void)e0;
+          const int nA = block_len32(a.V, 2 * (int32_t)gp);
+          const int nB = block_len32(a.V, 2 * (int32_t)gp + 1);
           const unsigned char* pa = st + pi * PAIRB;
           float mA, mB;
           if (nA == NOISE_BLK && nB == NOISE_BLK) {
@@ -331,44 +426,47 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         __threadfence_block();
         if (atomicAdd(&p1cnt[sb], 1u) == NSW - 1) {  // the last stream warp publishes
           rowhdr[sb] = atomicExch(&p1key[sb], 0ull);
+          rowid[sb] = row;
           p1cnt[sb] = 0;
-          rowM[sb] = 0u;  // the tail's shared bound for this row starts empty
           mbar_arrive(&sum_ready[sb]);  // release: the summary is complete
         }
       }
     }
+    SRT_PROF_PRINT("stream");
     return;
   }
 
   // ======================= tail: M, then the surviving blocks ==============
-  const int t = wid - 1 - NSW;
-  int64_t u = 0;
-  for (int64_t i = blockIdx.x; i < total; i += gridDim.x, ++u) {
-    const int64_t row = a.row_list ? a.row_list[i] : i;
-    const int sb = (int)(u % NS);
-    mbar_wait(&sum_ready[sb], (uint32_t)((u / NS) & 1));
-    const unsigned long long hdr = rowhdr[sb];
-    const float* U = reinterpret_cast<const float*>(sums + sb * a.sum_bytes);
-    float bz = -INFINITY;
-    int32_t bv = INT_MAX;
-    if (hdr != 0) {  // else every logit of the row is NaN: no candidate
-      const int2 ri = a.rowinfo[row];
-      const uint64_t sid = a.seq_id[ri.x];
-      const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
-      const unsigned char* rowp = (const unsigned char*)a.logits + row * row_bytes;
-      const float X = key_value((uint32_t)(hdr >> 32));
-      const uint32_t bX = 0xFFFFFFFFu - (uint32_t)hdr;
-      // i* = the first element of block bX equal to X; M = z(i*), exactly
-      // (tail warp 0 only: the others pick their phase-1 block meanwhile)
-      float M = -INFINITY;
-      if (t == 0) {
-      const int nX = block_len(a.V, bX);
-      const int64_t vX = (int64_t)bX * NOISE_BLK;
-      uint32_t first = 0xFFFFFFFFu;
-      if (2 * lane < nX && load_x<DT>(rowp, vX + 2 * lane) == X) first = 2 * lane;
-      else if (2 * lane + 1 < nX && load_x<DT>(rowp, vX + 2 * lane + 1) == X) first = 2 * lane + 1;
-      const uint32_t jstar = __reduce_min_sync(0xffffffffu, first);
-      {
+  // Tail warp 0 (the M warp) runs ahead of the others: for each row it finds
+  // i* (the first element of the row's max-logit block equal to the row's
+  // max logit) and publishes M = z(i*) in rowM, then releases the row to the
+  // workers (m_ready).  Its global load and noise arithmetic are thus off the
+  // workers' per-row chain.
+  if (wid == 1 + NSW) {
+    for (int64_t u = 0;; ++u) {
+      const int sb = (int)(u % NS);
+      SRT_TIMED(tw0, mbar_wait(&sum_ready[sb], (uint32_t)((u / NS) & 1)));
+      const int64_t row = rowid[sb];
+      if (row < 0) {  // the end: pass it on to the workers
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&m_ready[sb]);
+        break;
+      }
+      const unsigned long long hdr = rowhdr[sb];
+      uint32_t mkey = 0u;  // (none: every logit of the row is NaN)
+      if (hdr != 0 && !(a.debug & 16)) {
+        const int2 ri = a.rowinfo[row];
+        const uint64_t sid = a.seq_id[ri.x];
+        const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+        const unsigned char* rowp = (const unsigned char*)a.logits + row * row_bytes;
+        const float X = key_value((uint32_t)(hdr >> 32));
+        const uint32_t bX = 0xFFFFFFFFu - (uint32_t)hdr;
+        const int nX = block_len32(a.V, (int32_t)bX);
+        const int64_t vX = (int64_t)bX * NOISE_BLK;
+        uint32_t first = 0xFFFFFFFFu;
+        if (2 * lane < nX && load_x<DT>(rowp, vX + 2 * lane) == X) first = 2 * lane;
+        else if (2 * lane + 1 < nX && load_x<DT>(rowp, vX + 2 * lane + 1) == X) first = 2 * lane + 1;
+        const uint32_t jstar = __reduce_min_sync(0xffffffffu, first);
         uint32_t wa, wb;
         block_words(bX, pos, s_lo, s_hi, k0, k1, wa, wb);
         const BlockNoise bn = block_noise(wa, wb, (uint32_t)nX);
@@ -379,13 +477,42 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
           const uint32_t k = (uint32_t)(vs & 3);
           g = element_noise_from_word(k == 0 ? pw.x : k == 1 ? pw.y : k == 2 ? pw.z : pw.w, bn);
         }
-        M = perturbed(X, g, T, unit_t);
+        mkey = fkey(perturbed(X, g, T, unit_t));  // M = z(i*) is never NaN
       }
+      __syncwarp();
+      if (lane == 0) {
+        rowM[sb] = mkey;
+        mbar_arrive(&m_ready[sb]);  // release: M and the row header
       }
+    }
+    SRT_PROF_PRINT("m-warp");
+    return;
+  }
+
+  // Workers (NT - 1 warps): every block whose bound U_b reaches an achieved z.
+  constexpr int NTW = NT - 1;
+  const int t = wid - 2 - NSW;
+  int64_t u = 0;
+  for (;; ++u) {
+    const int sb = (int)(u % NS);
+    SRT_TIMED(tw0, mbar_wait(&m_ready[sb], (uint32_t)((u / NS) & 1)));
+    const int64_t row = rowid[sb];
+    if (row < 0) break;
+    const unsigned long long hdr = rowhdr[sb];
+    const float* U = reinterpret_cast<const float*>(sums + sb * a.sum_bytes);
+    float bz = -INFINITY;
+    int32_t bv = INT_MAX;
+    if (hdr != 0 && !(a.debug & 16)) {  // else every logit NaN (debug 16: timing probe, no tail)
+      const int2 ri = a.rowinfo[row];
+      const uint64_t sid = a.seq_id[ri.x];
+      const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+      const unsigned char* rowp = (const unsigned char*)a.logits + row * row_bytes;
+      float M = key_value(*(volatile uint32_t*)&rowM[sb]);  // z(i*) from the M warp
+      bool raised = false;  // M raised since this warp last shared it (share_M)
       // Exact evaluation of block b by the whole warp (lane = 2 consecutive
       // tokens, coalesced); the best (z, v) and M are raised as it goes.
       auto eval_block = [&](int32_t b, float2 xx) {
-        const int n = block_len(a.V, b);
+        const int n = block_len32(a.V, b);
         uint32_t wa, wb;
         block_words((uint32_t)b, pos, s_lo, s_hi, k0, k1, wa, wb);
         const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
@@ -407,36 +534,41 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
           if (cand_better(z, (int32_t)(v + k), bz, bv)) {
             bz = z;
             bv = (int32_t)(v + k);
-            M = fmaxf(M, z);
+            if (z > M) { M = z; raised = true; }
           }
         }
       };
       auto load_block = [&](int32_t b) {
-        const int n = block_len(a.V, b);
+        const int n = block_len32(a.V, b);
         const int64_t v = (int64_t)b * NOISE_BLK + 2 * lane;
         float2 xx;
         xx.x = 2 * lane < n ? load_x<DT>(rowp, v) : NAN;
         xx.y = 2 * lane + 1 < n ? load_x<DT>(rowp, v + 1) : NAN;
         return xx;
       };
-      // the warp's M joins the row's shared bound; the row's best M comes back
+      // the warp's M joins the row's shared bound; the row's best M comes back.
+      // Only a warp whose lanes raised M since they last shared it publishes
+      // (warp max + one shared atomic); the others just read the pooled bound.
       auto share_M = [&]() {
-        const uint32_t wk = __reduce_max_sync(0xffffffffu, fkey(M));  // M is never NaN
-        if (lane == 0) atomicMax(&rowM[sb], wk);
-        __syncwarp();
+        if (__any_sync(0xffffffffu, raised)) {
+          const uint32_t wk = __reduce_max_sync(0xffffffffu, fkey(M));  // M is never NaN
+          if (lane == 0) atomicMax(&rowM[sb], wk);
+          __syncwarp();
+          raised = false;
+        }
         const uint32_t k = *(volatile uint32_t*)&rowM[sb];
         M = fmaxf(M, key_value(k));
       };
       const int32_t nchunk = (a.nblk + 31) / 32;
-      // Phase 1 (branch and bound): each tail warp first evaluates the block
-      // of its share with the largest bound U_b, which usually holds a z near
-      // the row's maximum; the tail warps pool their M before phase 2, so far
+      // Phase 1 (branch and bound): each worker first evaluates the block of
+      // its share with the largest bound U_b, which usually holds a z near
+      // the row's maximum; the workers pool their M before phase 2, so far
       // fewer blocks pass U_b >= M than against z(i*) alone.
       int32_t b1 = -1;
       {
         uint32_t bu = 0;
         int32_t bi = INT_MAX;
-        for (int32_t cb = t; cb < nchunk; cb += NT) {
+        for (int32_t cb = t; cb < nchunk; cb += NTW) {
           const int32_t b = cb * 32 + lane;
           if (b < a.nblk) {
             const uint32_t k = fkey(U[b]);
@@ -445,23 +577,18 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         }
         const uint32_t wbu = __reduce_max_sync(0xffffffffu, bu);
         const int32_t wbi = __reduce_min_sync(0xffffffffu, (wbu && bu == wbu) ? bi : INT_MAX);
-        float2 xx1 = make_float2(NAN, NAN);
-        if (wbu) {
+        if (wbu && U[wbi] >= M) {
           b1 = wbi;
-          xx1 = load_block(b1);  // in flight across the barrier
+          eval_block(b1, load_block(b1));
         }
-        share_M();  // z(i*) from warp 0
-        asm volatile("bar.sync 1, %0;" ::"r"(NT * 32) : "memory");
-        share_M();
-        if (b1 >= 0 && U[b1] >= M) eval_block(b1, xx1);
       }
       share_M();
-      asm volatile("bar.sync 1, %0;" ::"r"(NT * 32) : "memory");
+      SRT_TIMED(tw1, asm volatile("bar.sync 1, %0;" ::"r"(NTW * 32) : "memory"));
       share_M();
       // Phase 2: every other block whose bound reaches M, BATCH at a time so
       // their L2 loads overlap; M is re-pooled after each batch.
       constexpr int BATCH = 4;
-      for (int32_t cb = t; cb < nchunk; cb += NT) {
+      for (int32_t cb = t; cb < nchunk; cb += NTW) {
         const int32_t b = cb * 32 + lane;
         unsigned surv = __ballot_sync(0xffffffffu, b < a.nblk && b != b1 && U[b] >= M);
         while (surv) {
@@ -498,6 +625,14 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
       mbar_arrive(&sum_free[sb]);
     }
   }
+  SRT_PROF_PRINT("tail");
+  if (SRT_SCAN_PROF_ON && (a.debug & 128) && t == 0 && lane == 0) {  // per-CTA span (ns)
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    printf("[scan cta] %d %llu %llu %lld\n", blockIdx.x, g_start, g_end, u);
+  }
+#undef SRT_TIMED
+#undef SRT_PROF_PRINT
 }
 
 // per row: (sequence, position) — rows of sequence s are [row_offsets[s],
@@ -521,7 +656,8 @@ template <int DT, int NSW, int NT, int NST, int NS, uint32_t CHUNK, int NG>
 cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
   constexpr int THREADS = (1 + NSW + NT) * 32;
   const size_t smem = (size_t)NST * CHUNK + (size_t)NS * p.sum_bytes +
-                      (2 * NST + 2 * NS) * 8 + 2 * NS * 8 + 2 * ((NS + 3) & ~3) * 4 +
+                      (2 * NST + 3 * NS) * 8 + 2 * NS * 8 + (NS + NST + 2) * 8 +
+                      2 * ((NS + 3) & ~3) * 4 +
                       NOISE_BUCKETS * 4;
   auto kern = k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -605,6 +741,13 @@ cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2*
   }
   p.l2_hint = (uint32_t)cfg[5];
   p.spin = (uint32_t)cfg[7];
+  // rows claimed dynamically (SRT_SCAN_STATIC=1: the static interleave)
+  static int stat = -1;
+  if (stat < 0) {
+    const char* e = getenv("SRT_SCAN_STATIC");
+    stat = e ? atoi(e) : 0;
+  }
+  p.sched = stat ? nullptr : c.sched;
 #define SRT_ROWS_CASE(A, B, C, D, K, G)                                                            \
   if (cfg[0] == A && cfg[1] == B && cfg[2] == C && cfg[3] == D && cfg[4] == K && cfg[6] == G)     \
     return a.dtype == SRT_BF16 ? launch_rows<SRT_BF16, A, B, C, D, K * 1024u, G>(c, p, stream)    \
@@ -612,7 +755,9 @@ cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2*
   SRT_ROWS_CASE(4, 12, 4, 4, 32, 1)
   SRT_ROWS_CASE(8, 8, 4, 4, 32, 2)
   SRT_ROWS_CASE(8, 12, 4, 4, 32, 2)
+  SRT_ROWS_CASE(8, 11, 4, 4, 32, 2)
   SRT_ROWS_CASE(8, 10, 6, 2, 32, 2)
+  SRT_ROWS_CASE(8, 10, 6, 3, 32, 2)
   SRT_ROWS_CASE(12, 8, 6, 2, 32, 3)
   SRT_ROWS_CASE(12, 9, 6, 3, 32, 3)
 #undef SRT_ROWS_CASE

@@ -71,6 +71,7 @@ struct DevCache {
   uint32_t* scnt;   // mirrors of their counts, contiguous for enumeration
   unsigned long long* ctr;  // [0] nodes created (+ P roots), [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
+  uint32_t* sched;          // [2] the scan's row-claim counters (0 between launches)
   float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima of
                   // G64; [2049, 3073) bucket maxima of the single-word Gumbel g(r)
   // Hub child lists: for a node with more than HUB_MIN

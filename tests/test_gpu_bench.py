@@ -58,7 +58,7 @@ def test_fused_verify_insert_matches_separate_calls(D):
     import bench
     cfg = dict(bench.CONFIGS["grpo"])
     cfg.update(prompts=6, active=48, V=5000, cap=1024, act_cap=1024, median=300,
-               node_capacity=1 << 20 if D <= 32 else 1 << 22, D=D, L=8)
+               node_capacity={32: 1 << 20, 64: 1 << 23, 128: 1 << 24}[D], D=D, L=8)
     out = []
     for fused in (False, True):
         wl = bench.Workload(cfg, 2)

@@ -127,7 +127,8 @@ def test_insert_cursor_deep_siblings_midspan_flush(orc, D, V):
     block-wide).  Trees equal the oracle's; the call terminates."""
     rng = np.random.default_rng(D + V)
     P, n, T = 2, 64, 4 * D
-    pair = Pair(orc, V, P, D, 8, 8, node_capacity=1 << 20)
+    # nearly every window of length > log_V(n T) is a new node: up to n T D
+    pair = Pair(orc, V, P, D, 8, 8, node_capacity=1 << 20 if D <= 64 else 1 << 23)
     base = rng.integers(0, V, (P, T)).astype(np.int32)
     prompt = (np.arange(n) % P).astype(np.int32)
     # siblings share their prompt's template with 30% substitutions: nodes

@@ -49,7 +49,7 @@ def test_gpu_fig5_ordering():
     decoding step (deterministic, so a fixed property of this workload)."""
     from paper_2601_09083_b200.rollout import GpuEngine, summarize
     kw = dict(V=151936, D=32, L=8, Bmax=32, prompts_per_step=8, samples=8, steps=2, median=300,
-              cap=1024, seed=0, ra_per_prompt=8)
+              cap=1024, seed=0, ra_per_prompt=8, node_capacity=1 << 26)
     r = {}
     for mode, ra in (("history_only", False), ("srt", False), ("srt", True)):
         r[(mode, ra)] = summarize(sim(GpuEngine, mode, ra, **kw).reports)
