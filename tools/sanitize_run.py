@@ -37,7 +37,7 @@ torch.cuda.synchronize()
 print(f"[sanitize] lmhead 2 steps, error bits {run.status()[0]}", flush=True)
 # D = 128: one CTA of 4 warps per sequence, sibling spans of ~D positions
 D, V, n = 128, 8, 32
-c = srt.SrtCache(srt.config(V, 2, D, 8, 8, node_capacity=1 << 18))
+c = srt.SrtCache(srt.config(V, 2, D, 8, 8, node_capacity=1 << 22))
 rng = np.random.default_rng(0)
 toks = torch.from_numpy(rng.integers(0, V, (n, 4 * D)).astype(np.int32)).cuda()
 prompt = torch.from_numpy((np.arange(n) % 2).astype(np.int32)).cuda()
