@@ -342,6 +342,13 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       }
     }
   } else {
+#ifdef SRT_LMHEAD_PROF
+    long long tph[6] = {0, 0, 0, 0, 0, 0};
+    const long long tp0 = clock64();
+#define LMP(i, t) tph[i] += clock64() - (t)
+#else
+#define LMP(i, t) (void)0
+#endif
     // ============ epilogue: sample from the accumulator ===================
     // 16 warps: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its 32 rows) and
     // noise block jb = (w - 2) / 4 of the tile's four (columns 64 jb .. + 63).
@@ -360,6 +367,7 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       const int64_t b = (int64_t)nt * BLK_PER_TILE + jb;  // this warp's noise block
       const int n = block_len(p.V, b);
       // the row's key and best-so-far (global loads) before the accumulator wait
+      long long tq = clock64();
       int2 ri = make_int2(0, 0);
       if (rv && !(p.debug & 8)) ri = p.rowinfo[r];
       uint32_t pos = 0, slo = 0, shi = 0;
@@ -377,8 +385,12 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
         wa = (b & 1) ? w.z : w.x;
         wb = (b & 1) ? w.w : w.y;
       }
+      LMP(0, tq);
+      tq = clock64();
       bar_wait_sleep(&acc_full[a], (u >> 1) & 1);
       tc_fence_after();
+      LMP(1, tq);
+      tq = clock64();
       if (p.debug & 1) {  // development: the pipeline without the sampler
         __syncwarp();
         if (lane == 0) bar_arrive_leader(&acc_empty[a]);
@@ -392,6 +404,8 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive_leader(&acc_empty[a]);
+      LMP(2, tq);
+      tq = clock64();
       // ---- the block maximum X: rounding is monotone, so the max of the
       // rounded logits is the rounded max of the accumulators ----
       bool nan = false;
@@ -446,6 +460,8 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           atomicAdd(&g_lm_stats[3], 1ull); // warp-blocks
         }
       }
+      LMP(3, tq);
+      tq = clock64();
       if (U > -INFINITY && U >= M && !(p.debug & 16)) {
         // ---- the block can still hold the row's winner ----
         const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
@@ -520,12 +536,21 @@ k_lmhead_sample(const __grid_constant__ CUtensorMap map_a, const __grid_constant
           }
         }
       }
+      LMP(4, tq);
+      tq = clock64();
       if (__any_sync(0xffffffffu, nan) && lane == 0) set_error(c, SRT_DEV_NONFINITE_LOGIT);
       if (rv && bv != INT_MAX) {
         const unsigned long long pk = pack_cand(bz, bv);
         if (pk > cur) atomicMax(&p.result[r], pk);
       }
+      LMP(5, tq);
     }
+#ifdef SRT_LMHEAD_PROF
+    if (blockIdx.x < 2 && lane == 0)
+      printf("[lm prof] cta %d warp %2d total %lld loads %lld wait %lld tmem %lld bound %lld exact %lld out %lld tiles %u\n",
+             blockIdx.x, wid, clock64() - tp0, tph[0], tph[1], tph[2], tph[3], tph[4], tph[5], u);
+#endif
+#undef LMP
   }
   tc_fence_before();
   cluster_sync();  // both CTAs done with the tensor memory and the leader's barriers

@@ -320,7 +320,12 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
           const int s = (int)(kc % NST);
           const uint32_t use = (uint32_t)(kc / NST);
-          if (use > 0) SRT_TIMED(tw0, mbar_wait(&ring_empty[s], (use - 1) & 1));
+          if (use > 0) {
+            SRT_TIMED(tw0, mbar_wait(&ring_empty[s], (use - 1) & 1));
+            // the stream warps' generic-proxy reads of the stage are ordered
+            // before the async-proxy (TMA) overwrite
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          }
           const int64_t left = row_bytes - (int64_t)ch * CHUNK;
           const uint32_t nb = (uint32_t)(left < (int64_t)CHUNK ? left : (int64_t)CHUNK);
           mbar_arrive_expect_tx(&ring_full[s], nb);
