@@ -67,7 +67,7 @@ CONFIGS = {
 }
 
 KERNELS_PER_STEP = 9  # timed segments per group and step (an upper bound, for the profile buffer)
-SEGMENT_KERNELS = {"scan": 2, "hub_refresh": 2}  # segments that launch two kernels
+SEGMENT_KERNELS = {"scan": 2, "hub_refresh": 2, "tree_step": 2}  # segments of two kernels
                       # (+ insert_plan/walk of the run-ahead spans)
 
 
@@ -322,6 +322,11 @@ class Group:
         self.tree_stats = st
         self.path_rounds = None  # srt_verify_path rounds (bench --verify path)
         self.fused = True  # srt_verify_insert_cursor (accept + cursor insert in one kernel)
+        # srt_verify_insert_draft_cursor: commit + insert + hub refresh + the NEXT
+        # draft in one persistent kernel (GpuRun sets it; D <= 32, full verify)
+        self.fused_step = False
+        self.need_draft = True  # no draft of the current step in self.d yet
+        self.snap = None        # (row_offsets, draft_depth) of the last verified draft
         # ---- run-ahead spans (DAPO): a fixed schedule, uploaded once
         self.ra = None
         if wl.w.runahead and cfg.get("runahead"):
@@ -408,10 +413,35 @@ class Group:
     def draft(self):
         self.cache.draft(self.prompt_id, self.seq_tok, self.seq_len, self.seq_len, out=self.d,
                          cursor=self.cursor)
+        self.need_draft = False
+
+    def draft_if_needed(self):
+        """The fused step drafted this step already (inside the previous
+        verify); otherwise srt_draft_cursor."""
+        if not (self.fused_step and not self.need_draft):
+            self.draft()
+
+    def snapshot_layout(self):
+        """Keep the verified draft's row layout (the fused step overwrites
+        self.d with the next draft; the parity sample maps rows to positions)."""
+        self.snap = (self.d.row_offsets.clone(), self.d.draft_depth.clone())
 
     def verify_insert(self, seed: int, logits=None):
         c = self.cache
         lg = self.logits if logits is None else logits
+        if (self.fused_step and self.lm is None and self.path_rounds is None
+                and self.cache.cfg.max_depth <= 32):
+            # run-ahead spans target look-ahead prompts (no active sequence's
+            # tree); inserts commute (O14), so they go first and the next draft,
+            # inside the fused call, sees them as it would after the unfused step
+            if self.ra is not None:
+                self.runahead_insert()
+            c.verify_insert_draft(lg, self.d, self.seq_id, seed, self.seq_tok, self.seq_len,
+                                  self.max_new, self.prompt_id, self.cursor, pos_base=self.seq_len,
+                                  next_d=self.d, out=self.v, rows=self.rows_max)
+            self.need_draft = False
+            return
+        self.need_draft = True
         if self.lm is not None and logits is None:  # the LM head fused into the sampler
             c.verify_lmhead(self.lm["H"], self.lm["W"], self.d, self.seq_id, seed, self.seq_tok,
                             self.seq_len, self.max_new, prompt_id=self.prompt_id,
@@ -554,18 +584,25 @@ class GpuRun:
             return getattr(groups[0], name)
         raise AttributeError(name)
 
-    def step(self, seed: int, ev=None):
+    def step(self, seed: int, ev=None, rows_out=None):
         """Sequential step on the current stream: draft -> [stand-in] ->
-        verify -> insert for every group.  ev = 4 CUDA events bracketing the
-        draft segment and the verify+insert segment (stand-in excluded)."""
+        verify -> insert for every group (with --fused-step the draft of this
+        step was made by the previous step's fused call).  ev = 4 CUDA events
+        bracketing the draft segment and the verify+insert segment (stand-in
+        excluded); rows_out (1-element device tensor) <- this step's rows."""
         if ev:
             ev[0].record()
         for gr in self.groups:
-            gr.draft()
+            gr.draft_if_needed()
         if ev:
             ev[1].record()
         for gr in self.groups:
             gr.standin()
+        if rows_out is not None:
+            rows_out.copy_(sum(gr.d.row_offsets[-1:] for gr in self.groups))
+        for gr in self.groups:
+            if gr.fused_step:
+                gr.snapshot_layout()  # (the fused call overwrites self.d with the next draft)
         if ev:
             ev[2].record()
         for gr in self.groups:
@@ -863,6 +900,9 @@ def main():
                          "srt_verify_lmhead_insert_cursor (the LM-head GEMM fused with the "
                          "sampler, SURVEY f3a: the step then includes the LM head)")
     ap.add_argument("--path-rounds", type=int, default=3)
+    ap.add_argument("--fused-step", type=int, default=1,
+                    help="1: srt_verify_insert_draft_cursor (commit + insert + hub refresh + the "
+                         "next draft in one persistent kernel; D <= 32, --verify full, 1 group)")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: each step's draft segment and verify+insert segment replay as CUDA "
                          "graphs (no launch gaps); the per-kernel breakdown then comes from a "
@@ -940,6 +980,9 @@ def main():
         if args.verify == "lmhead":
             run.enable_lmhead(cfg.get("hidden", 1536), args.seed)
         G = run.G
+        if args.fused_step and args.verify == "full" and cfg["D"] <= 32 and G == 1:
+            for gr in run.groups:
+                gr.fused_step = True
     pipelined = G > 1
     K, W = args.steps, args.warmup
     seed = step_seed(args.seed, 0)
@@ -975,7 +1018,8 @@ def main():
             with torch.cuda.graph(g_vi):
                 gr0.verify_insert(seed)
             for _ in range(2):  # graph warm-up steps
-                g_draft.replay()
+                if not gr0.fused_step:
+                    g_draft.replay()
                 gr0.standin()
                 g_vi.replay()
             torch.cuda.synchronize()
@@ -1013,16 +1057,19 @@ def main():
                 if use_graph:
                     e = evs[k]
                     e[0].record()
-                    g_draft.replay()
+                    if not gr0.fused_step:  # (fused: the previous step drafted this one)
+                        g_draft.replay()
                     e[1].record()
                     gr0.standin()
+                    rows_log[k] = gr0.d.row_offsets[-1]  # (outside the timed segments)
+                    if k == K - 1:
+                        gr0.snapshot_layout()
                     e[2].record()
                     g_vi.replay()
                     e[3].record()
                 else:
-                    run.step(seed, evs[k])
+                    run.step(seed, evs[k], rows_out=rows_log[k:k + 1])
                 # bookkeeping outside the event-bracketed segments
-                rows_log[k] = run.d.row_offsets[-1]
                 if args.verify == "path":  # rows srt_verify_path actually sampled
                     nr = run.d.row_offsets[-1]
                     smp_log[k] = ((run.v.sampled[:run.rows_max] >= 0)
@@ -1049,8 +1096,7 @@ def main():
             gr.cache.profile_enable(KP * KERNELS_PER_STEP)
         prof_rows = torch.zeros(KP, dtype=torch.int64, device=run.dev)
         for k in range(KP):
-            run.step(seed)
-            prof_rows[k] = run.d.row_offsets[-1]
+            run.step(seed, rows_out=prof_rows[k:k + 1])
         torch.cuda.synchronize()
         prof_rows = prof_rows.cpu().numpy()
     prof = [x for gr in run.groups for x in gr.cache.profile_read()]
@@ -1144,7 +1190,8 @@ def main():
         "kernels": kern,
         "tree_stage_us_per_batch": {k: kern[k]["mean_us"] for k in
                                     ("draft", "row_offsets", "insert_plan", "insert_walk",
-                                     "insert_cursor", "accept", "accept_insert")
+                                     "insert_cursor", "accept", "accept_insert", "hub_refresh",
+                                     "tree_step")
                                     if k in kern},
         # kernels per timed segment: the scan segment launches k_rowinfo + k_scan_rows,
         # the hub refresh k_hub_pick + k_hub_refresh; every other segment one kernel
@@ -1215,15 +1262,16 @@ def capture_parity_sample(run, n_rows: int, seed_rows: int):
     tie-break divergence count."""
     torch = run.torch
     gr = run.groups[0]
-    total = int(gr.d.row_offsets[-1].item())
+    ro_t, dep_t = gr.snap if gr.snap is not None else (gr.d.row_offsets, gr.d.draft_depth)
+    total = int(ro_t[-1].item())
     if total <= 0 or n_rows <= 0:
         return None
     rng = np.random.default_rng(seed_rows)
     pick = np.sort(rng.choice(total, size=min(n_rows, total), replace=False))
-    row_off = gr.d.row_offsets.cpu().numpy()
+    row_off = ro_t.cpu().numpy()
     s_of = np.searchsorted(row_off, pick, side="right") - 1
     j = pick - row_off[s_of]  # 0 = root row, else draft node j - 1
-    depth = gr.d.draft_depth.cpu().numpy()
+    depth = dep_t.cpu().numpy()
     t_before = gr.t_before.cpu().numpy()
     pos = t_before[s_of] + np.where(j == 0, 0, depth[s_of, np.maximum(j - 1, 0)])
     idx = torch.from_numpy(pick).to(gr.logits.device)
@@ -1300,7 +1348,7 @@ def e2e_leg(run: GpuRun, args, steps: int):
             n = gr.n
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e[0].record()
-            gr.draft()
+            gr.draft_if_needed()
             rows_t = gr.d.row_offsets[-1:].to("cpu", non_blocking=True)
             e[1].record()
             torch.cuda.synchronize()

@@ -387,6 +387,38 @@ SRT_API srt_status srt_verify_lmhead_insert_cursor(
     uint8_t* finished, const int32_t* prompt_id, const int32_t* floor, uint32_t* cursor,
     srt_insert_stats* stats, void* stream);
 
+/*
+ * srt_verify_insert_draft_cursor — one call for everything after the policy
+ * forward of step k: srt_verify_insert_cursor (the scan of every drafted row,
+ * the commit, and the cursor insertion of the committed spans)
+ * followed by srt_draft_cursor of step k + 1 over the updated
+ * sequences, with the commit, insertion, hub-list refresh and next draft in
+ * ONE persistent kernel ordered per prompt:
+ * reading O14 orders draft(k+1) of prompt p after the inserts of p only, so
+ * a prompt drafts as soon as its own sequences are committed and inserted.
+ * Arguments: those of srt_verify_insert_cursor, then pos_base[n] (nullable;
+ * read after the commit, so it may alias seq_len: positions = the new length
+ * + depth) and the draft outputs of srt_draft (match_len ... row_offsets).
+ * The draft outputs MAY alias this call's draft inputs (the same buffers):
+ * sequence s's new draft is written only after its prompt's commits, and
+ * row_offsets[0 .. n] only after every commit.  Results are identical to
+ * srt_verify_insert_cursor then srt_draft_cursor(prompt_id, seq_tok,
+ * seq_len, pos_base, cursor).  Needs cfg.max_depth <= 32 (one warp per
+ * sequence; SRT_ERR_INVALID_ARG otherwise, before anything is enqueued).
+ * Device-side errors as both calls.
+ */
+SRT_API srt_status srt_verify_insert_draft_cursor(
+    srt_cache* cache, int32_t n, const void* logits, const int64_t* row_offsets,
+    const int32_t* draft_len, const int32_t* draft_tok, const int32_t* draft_parent,
+    const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed, float temperature,
+    int32_t eos_id, const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len,
+    int32_t* sampled, int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+    int32_t* accepted_nodes, uint8_t* finished, const int32_t* prompt_id, const int32_t* floor,
+    uint32_t* cursor, srt_insert_stats* stats, const int32_t* pos_base, int32_t* next_match_len,
+    int32_t* next_draft_len, int32_t* next_draft_tok, int32_t* next_draft_parent,
+    int32_t* next_draft_depth, int32_t* next_draft_pos, uint64_t* next_draft_mask,
+    int64_t* next_row_offsets, void* stream);
+
 /* records[s] <- the draft of sequence s < n (srt_draft's outputs). */
 SRT_API srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
                            const int32_t* draft_len, const int32_t* draft_tok,
@@ -538,7 +570,8 @@ typedef enum {
   SRT_K_INSERT_CURSOR = 6,
   SRT_K_HUB_REFRESH = 7, /* the hub child lists an insert call rebuilds */
   SRT_K_ACCEPT_INSERT = 8, /* srt_verify_insert_cursor's fused accept + cursor insert */
-  SRT_K_LMHEAD = 9         /* srt_verify_lmhead*: row info + the fused LM-head GEMM + sampler */
+  SRT_K_LMHEAD = 9,        /* srt_verify_lmhead*: row info + the fused LM-head GEMM + sampler */
+  SRT_K_TREE_STEP = 10     /* srt_verify_insert_draft_cursor: commit + insert + refresh + next draft */
 } srt_kernel_id;
 
 typedef struct {

@@ -25,14 +25,15 @@ SRT_BF16, SRT_F32 = 0, 1
 
 # Every symbol include/srt.h declares (tests check the export table).
 EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache_destroy",
-           "srt_insert", "srt_insert_cursor", "srt_draft", "srt_draft_cursor", "srt_verify", "srt_verify_path", "srt_verify_insert_cursor", "srt_verify_lmhead", "srt_verify_lmhead_insert_cursor", "srt_cache_dump",
+           "srt_insert", "srt_insert_cursor", "srt_draft", "srt_draft_cursor", "srt_verify", "srt_verify_path", "srt_verify_insert_cursor", "srt_verify_insert_draft_cursor", "srt_verify_lmhead", "srt_verify_lmhead_insert_cursor", "srt_cache_dump",
            "srt_cache_prune", "srt_cache_evict", "srt_cache_load", "srt_cache_status",
            "srt_cache_clear_errors", "srt_noise_table", "srt_log_det_range", "srt_row_noise", "srt_stream_read", "srt_sample_rows_reference",
            "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile", "srt_debug_insert_profile",
            "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
                 5: "accept", 6: "insert_cursor",
-                7: "hub_refresh", 8: "accept_insert", 9: "lmhead"}
+                7: "hub_refresh", 8: "accept_insert", 9: "lmhead",
+                10: "tree_step"}
 
 
 class SrtConfig(ctypes.Structure):
@@ -96,6 +97,8 @@ def load() -> ctypes.CDLL:
     L.srt_verify_insert_cursor.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, u64, f32, i32, vp,
                                            vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                            vp]
+    L.srt_verify_insert_draft_cursor.argtypes = (L.srt_verify_insert_cursor.argtypes[:-1] +
+                                                  [vp] * 9 + [vp])  # pos_base, 8 outputs, stream
     _lm = [vp, i32, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, u64, f32, i32, vp, vp, i64, vp,
            vp, vp, vp, vp, vp, vp]
     L.srt_verify_lmhead.argtypes = _lm + [vp]

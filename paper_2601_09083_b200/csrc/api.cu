@@ -123,12 +123,17 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   const size_t o_ctr = off;     off = align_up(off + 2 * 8);
   const size_t o_status = off;  off = align_up(off + 4);
   const size_t o_sched = off;   off = align_up(off + 2 * 4);
+  const size_t PP = (size_t)cfg->max_prompts;
+  const size_t o_step = off;    off = align_up(off + (6 * PP + 4 + PP * PDIRTY_WORDS) * 4);
   const size_t o_gb = off;      off = align_up(off + (3 * NOISE_BUCKETS + 1) * 4);
   // hub child lists: ~1 slot per 16 nodes' worth of hash, at least 2^12
   size_t HC = 4096;
   while (HC < H / 512 && HC < (1u << 18)) HC <<= 1;
+  size_t P2 = 1;  // prompts rounded up to a power of two: equal per-prompt partitions
+  while (P2 < (size_t)cfg->max_prompts) P2 <<= 1;
+  while (HC < 16 * P2) HC <<= 1;
   const size_t o_hub = off;     off = align_up(off + HC * (4 * 4 + 8 + (size_t)HUB_K * 12));
-  const size_t o_dirty = off;   off = align_up(off + ((size_t)DIRTY_CAP + 2) * 4);
+  const size_t o_dirty = off;   off = align_up(off + (size_t)DIRTY_CAP * 8 + 2 * 4);
   srt_cache* c = new srt_cache();
   c->cfg = *cfg;
   cudaGetDevice(&c->device);
@@ -161,8 +166,18 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
   d.ctr = (unsigned long long*)(b + o_ctr);
   d.status = (uint32_t*)(b + o_status);
   d.sched = (uint32_t*)(b + o_sched);
+  d.st_pcount = (uint32_t*)(b + o_step);
+  d.st_pdone = d.st_pcount + PP;
+  d.st_pready = d.st_pdone + PP;
+  d.st_pnd = d.st_pready + PP;
+  d.st_pnext = d.st_pnd + PP;
+  d.st_pfin = d.st_pnext + PP;
+  d.st_ndone = d.st_pfin + PP;
+  d.pdirty = d.st_ndone + 4;
   d.gbound = (float*)(b + o_gb);
   d.HC = (uint32_t)HC;
+  d.hub_shift = 0;
+  while (((size_t)1 << (d.hub_shift + 1)) * P2 <= HC) ++d.hub_shift;
   {
     char* hb = b + o_hub;
     d.hub_claim = (unsigned long long*)hb;  hb += HC * 8;
@@ -174,11 +189,13 @@ srt_status srt_cache_create(const srt_config* cfg, void* stream_, srt_cache** ou
     d.hub_tok = (int32_t*)hb;               hb += HC * HUB_K * 4;
     d.hub_cnt = (uint32_t*)hb;
   }
-  d.dirty = (uint32_t*)(b + o_dirty);
-  d.dirty_n = d.dirty + DIRTY_CAP;
+  d.dirty = (uint2*)(b + o_dirty);
+  d.dirty_n = (uint32_t*)(d.dirty + DIRTY_CAP);
   c->scratch = nullptr;
   c->scratch_cap = 0;
   if ((e = cudaMemsetAsync(d.sched, 0, 2 * 4, stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(d.st_pcount, 0, (6 * PP + 4 + PP * PDIRTY_WORDS) * 4, stream)) !=
+          cudaSuccess ||
       (e = launch_init_cache(d, stream)) != cudaSuccess ||
       (e = launch_noise_bounds(d, stream)) != cudaSuccess) {
     cudaFreeAsync(c->pool, stream);
@@ -219,7 +236,7 @@ srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const 
     c->scratch_cap = cap;
   }
   if (!c->hubwork)
-    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
+    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP * 2 + 1) * 4, stream),
              "cudaMallocAsync(hub work)");
   // cursor path: spans of <= D new positions; longer ones (run-ahead) walk
   const int32_t short_max = cursor ? c->cfg.max_depth : -1;
@@ -245,7 +262,7 @@ srt_status insert_impl(srt_cache* c, int32_t n, const int32_t* prompt_id, const 
              "insert cursor");
   SRT_CUDA(timed(c, SRT_K_HUB_REFRESH, stream,
                  [&] {
-                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + DIRTY_CAP,
+                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + 2 * DIRTY_CAP,
                                              stream);
                  }),
            "hub refresh");
@@ -451,7 +468,7 @@ srt_status srt_verify_lmhead_insert_cursor(
                accepted_nodes, finished};
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!c->hubwork)
-    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
+    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP * 2 + 1) * 4, stream),
              "cudaMallocAsync(hub work)");
   st = verify_lmhead_scan(c, a, h, stream);
   if (st != SRT_OK) return st;
@@ -463,7 +480,7 @@ srt_status srt_verify_lmhead_insert_cursor(
            "verify accept + insert");
   SRT_CUDA(timed(c, SRT_K_HUB_REFRESH, stream,
                  [&] {
-                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + DIRTY_CAP,
+                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + 2 * DIRTY_CAP,
                                              stream);
                  }),
            "hub refresh");
@@ -523,7 +540,7 @@ srt_status srt_verify_insert_cursor(
                accepted_nodes, finished};
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!c->hubwork)
-    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP + 1) * 4, stream),
+    SRT_CUDA(cudaMallocAsync(&c->hubwork, ((size_t)DIRTY_CAP * 2 + 1) * 4, stream),
              "cudaMallocAsync(hub work)");
   const srt_status st = verify_scan(c, a, stream);
   if (st != SRT_OK) return st;
@@ -535,10 +552,51 @@ srt_status srt_verify_insert_cursor(
            "verify accept + insert");
   SRT_CUDA(timed(c, SRT_K_HUB_REFRESH, stream,
                  [&] {
-                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + DIRTY_CAP,
+                   return launch_hub_refresh(c->dev, 0, c->hubwork, c->hubwork + 2 * DIRTY_CAP,
                                              stream);
                  }),
            "hub refresh");
+  return SRT_OK;
+}
+
+srt_status srt_verify_insert_draft_cursor(
+    srt_cache* c, int32_t n, const void* logits, const int64_t* row_offsets,
+    const int32_t* draft_len, const int32_t* draft_tok, const int32_t* draft_parent,
+    const int32_t* draft_depth, const uint64_t* seq_id, uint64_t seed, float temperature,
+    int32_t eos_id, const int32_t* max_new, int32_t* seq_tok, int64_t stride, int32_t* seq_len,
+    int32_t* sampled, int32_t* accept_len, int32_t* n_commit, int32_t* commit_tok,
+    int32_t* accepted_nodes, uint8_t* finished, const int32_t* prompt_id, const int32_t* floor_,
+    uint32_t* cursor, srt_insert_stats* stats_dev, const int32_t* pos_base, int32_t* next_match_len,
+    int32_t* next_draft_len, int32_t* next_draft_tok, int32_t* next_draft_parent,
+    int32_t* next_draft_depth, int32_t* next_draft_pos, uint64_t* next_draft_mask,
+    int64_t* next_row_offsets, void* stream_) {
+  SRT_NVTX("srt_verify_insert_draft_cursor");
+  if (!c || n < 0 || stride < 0) return SRT_ERR_INVALID_ARG;
+  if (!(temperature > 0.0f) || !(temperature < 3.4e38f)) return SRT_ERR_INVALID_ARG;
+  if (n == 0) return SRT_OK;
+  if (!logits || !row_offsets || !draft_len || !draft_tok || !draft_parent || !draft_depth ||
+      !seq_id || !max_new || !seq_tok || !seq_len || !sampled || !accept_len || !n_commit ||
+      !commit_tok || !accepted_nodes || !finished || !prompt_id || !cursor || !next_match_len ||
+      !next_draft_len || !next_draft_tok || !next_draft_parent || !next_draft_depth ||
+      !next_draft_pos || !next_draft_mask || !next_row_offsets)
+    return SRT_ERR_INVALID_ARG;
+  if (c->cfg.max_depth > 32) return SRT_ERR_INVALID_ARG;  // one warp per sequence
+  VerifyArgs a{n,       logits,     (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
+               draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
+               seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
+               accepted_nodes, finished};
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const srt_status st = verify_scan(c, a, stream);
+  if (st != SRT_OK) return st;
+  SRT_CUDA(timed(c, SRT_K_TREE_STEP, stream,
+                 [&] {
+                   return launch_tree_step(c->dev, a, c->result, prompt_id, floor_, cursor, c->tag,
+                                           stats_dev, pos_base, next_match_len, next_draft_len,
+                                           next_draft_tok, next_draft_parent, next_draft_depth,
+                                           next_draft_pos, next_draft_mask, next_row_offsets,
+                                           stream);
+                 }),
+           "fused tree step");
   return SRT_OK;
 }
 

@@ -15,6 +15,7 @@
 // threshold first (lane-wise top-2 counts), then every warp keeps a sorted
 // top-K of its share of the children at or above it, the lists are merged by rank.
 #include "srt_internal.cuh"
+#include "hub.cuh"
 
 namespace srt {
 
@@ -22,79 +23,31 @@ namespace {
 
 constexpr int REFRESH_WARPS = 8;
 
-__device__ __forceinline__ unsigned long long child_key(uint32_t cnt, int32_t tok) {
-  return ((unsigned long long)cnt << 32) | (0xFFFFFFFFu - (uint32_t)tok);  // larger = better
-}
-
-// A sorted (descending) warp list of up to 64 keys: lane i holds entries i and i + 32.
-struct KeyList {
-  unsigned long long k0, k1;
-  uint32_t v0, v1;
-  int size;
-  __device__ __forceinline__ unsigned long long key_at(int j) const {
-    return j < 32 ? __shfl_sync(0xffffffffu, k0, j) : __shfl_sync(0xffffffffu, k1, j - 32);
-  }
-  __device__ __forceinline__ void insert(unsigned long long k, uint32_t v, int lane, int K) {
-    const int pos = __popc(__ballot_sync(0xffffffffu, lane < size && k0 > k)) +
-                    __popc(__ballot_sync(0xffffffffu, lane + 32 < size && k1 > k));
-    if (pos >= K) return;
-    const unsigned long long uk0 = __shfl_up_sync(0xffffffffu, k0, 1);
-    const uint32_t uv0 = __shfl_up_sync(0xffffffffu, v0, 1);
-    const unsigned long long uk1 = __shfl_up_sync(0xffffffffu, k1, 1);
-    const uint32_t uv1 = __shfl_up_sync(0xffffffffu, v1, 1);
-    const unsigned long long lk = __shfl_sync(0xffffffffu, k0, 31);
-    const uint32_t lv = __shfl_sync(0xffffffffu, v0, 31);
-    if (lane + 32 >= pos) {
-      if (lane + 32 == pos) { k1 = k; v1 = v; }
-      else if (lane == 0) { k1 = lk; v1 = lv; }
-      else { k1 = uk1; v1 = uv1; }
-    }
-    if (lane >= pos) {
-      if (lane == pos) { k0 = k; v0 = v; }
-      else { k0 = uk0; v0 = uv0; }
-    }
-    size = min(size + 1, K);
-  }
-  // offer 32 candidates (one per lane): the ones that beat the current last entry enter
-  __device__ __forceinline__ void offer(bool valid, unsigned long long k, uint32_t v, int lane,
-                                       int K) {
-    const unsigned long long bar = size == K ? key_at(K - 1) : 0ull;
-    unsigned pending = __ballot_sync(0xffffffffu, valid && (size < K || k > bar));
-    while (pending) {
-      const int src = __ffs(pending) - 1;
-      pending &= pending - 1;
-      const unsigned long long kk = __shfl_sync(0xffffffffu, k, src);
-      const uint32_t vv = __shfl_sync(0xffffffffu, v, src);
-      if (size == K && kk <= key_at(K - 1)) continue;
-      insert(kk, vv, lane, K);
-    }
-  }
-};
-
 // Each dirty hub whose list is stale claims its cache slot for this refresh
 // generation with one CAS: the first claim of a slot wins (a node listed
 // several times refreshes once; of two hubs sharing a slot one refreshes, the
 // other keeps the full scan until a later refresh) and joins the work list.
-__global__ void k_hub_pick(DevCache c, uint32_t* work, uint32_t* work_n) {
+__global__ void k_hub_pick(DevCache c, uint2* work, uint32_t* work_n) {
   const uint32_t call = c.dirty_n[1] + 1;  // this refresh's generation
   const uint32_t n = min(*c.dirty_n, DIRTY_CAP);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t u = c.dirty[i];
-    if (u >= c.H) continue;  // roots are never expanded
+    const uint2 du = c.dirty[i];
+    const uint32_t u = du.x;
+    if (u >= c.H || du.y >= (uint32_t)c.P) continue;  // roots are never expanded
     const uint4 r = *rec_of(c, u);
     if (r.x <= HUB_MIN) continue;
-    const uint32_t slot = hub_slot(c, u);
+    const uint32_t slot = hub_slot(c, (int32_t)du.y, u);
     // (a list that is still valid needs no rebuild)
     if (c.hub_node[slot] == u && c.hub_nch[slot] == r.x && c.hub_csum[slot] == r.w) continue;
     const unsigned long long c0 = c.hub_claim[slot];
     if ((uint32_t)(c0 >> 32) == call) continue;  // claimed in this generation already
     if (atomicCAS(&c.hub_claim[slot], c0, ((unsigned long long)call << 32) | u) != c0) continue;
-    work[atomicAdd(work_n, 1u)] = u;
+    work[atomicAdd(work_n, 1u)] = du;
   }
 }
 
 __global__ void __launch_bounds__(REFRESH_WARPS * 32)
-k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* work_n) {
+k_hub_refresh(DevCache c, const uint2* __restrict__ work, const uint32_t* work_n) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     c.dirty_n[1] += 1;  // next refresh's generation
     c.dirty_n[0] = 0;   // k_hub_pick consumed the list
@@ -107,7 +60,8 @@ k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* wor
   const int K = min(HUB_K, c.Bmax);  // the draft never needs more than Bmax of them
   const uint32_t nw = *work_n;
   for (uint32_t it = blockIdx.x; it < nw; it += gridDim.x) {
-    const uint32_t u = work[it];
+    const uint2 wu = work[it];
+    const uint32_t u = wu.x;
     const uint4 r = *rec_of(c, u);
     const uint32_t nch = r.x;
     const uint32_t nb = blk_index(nch - 2) + 1;
@@ -129,7 +83,7 @@ k_hub_refresh(DevCache c, const uint32_t* __restrict__ work, const uint32_t* wor
     // The previous list of this node (if any) bounds the threshold from below:
     // counts only grow, so its K children still have counts >= its last
     // entry's, and no child below that count can enter the new list.
-    const uint32_t slot = hub_slot(c, u);
+    const uint32_t slot = hub_slot(c, (int32_t)wu.y, u);
     uint32_t thr = 0;
     if (c.hub_node[slot] == u && c.hub_len[slot] == (uint32_t)K) {
       thr = c.hub_cnt[(size_t)slot * HUB_K + K - 1];
@@ -233,8 +187,9 @@ cudaError_t launch_hub_refresh(const DevCache& c, uint32_t call, uint32_t* work,
   if (e != cudaSuccess) return e;
   const int g = num_sms() * 4;
   (void)call;
-  k_hub_pick<<<g, 256, 0, stream>>>(c, work, work_n);
-  k_hub_refresh<<<num_sms() * 8, REFRESH_WARPS * 32, 0, stream>>>(c, work, work_n);
+  k_hub_pick<<<g, 256, 0, stream>>>(c, reinterpret_cast<uint2*>(work), work_n);
+  k_hub_refresh<<<num_sms() * 8, REFRESH_WARPS * 32, 0, stream>>>(
+      c, reinterpret_cast<const uint2*>(work), work_n);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,209 @@
+// hub.cuh — the hub child lists' sorted warp list and the one-warp refresh
+// of a hub's list (hub.cu has the design; step.cu refreshes per prompt).
+#pragma once
+#include "srt_internal.cuh"
+
+namespace srt {
+namespace {
+
+__device__ __forceinline__ unsigned long long child_key(uint32_t cnt, int32_t tok) {
+  return ((unsigned long long)cnt << 32) | (0xFFFFFFFFu - (uint32_t)tok);  // larger = better
+}
+
+// A sorted (descending) warp list of up to 64 keys: lane i holds entries i and i + 32.
+struct KeyList {
+  unsigned long long k0, k1;
+  uint32_t v0, v1;
+  int size;
+  __device__ __forceinline__ unsigned long long key_at(int j) const {
+    return j < 32 ? __shfl_sync(0xffffffffu, k0, j) : __shfl_sync(0xffffffffu, k1, j - 32);
+  }
+  __device__ __forceinline__ void insert(unsigned long long k, uint32_t v, int lane, int K) {
+    const int pos = __popc(__ballot_sync(0xffffffffu, lane < size && k0 > k)) +
+                    __popc(__ballot_sync(0xffffffffu, lane + 32 < size && k1 > k));
+    if (pos >= K) return;
+    const unsigned long long uk0 = __shfl_up_sync(0xffffffffu, k0, 1);
+    const uint32_t uv0 = __shfl_up_sync(0xffffffffu, v0, 1);
+    const unsigned long long uk1 = __shfl_up_sync(0xffffffffu, k1, 1);
+    const uint32_t uv1 = __shfl_up_sync(0xffffffffu, v1, 1);
+    const unsigned long long lk = __shfl_sync(0xffffffffu, k0, 31);
+    const uint32_t lv = __shfl_sync(0xffffffffu, v0, 31);
+    if (lane + 32 >= pos) {
+      if (lane + 32 == pos) { k1 = k; v1 = v; }
+      else if (lane == 0) { k1 = lk; v1 = lv; }
+      else { k1 = uk1; v1 = uv1; }
+    }
+    if (lane >= pos) {
+      if (lane == pos) { k0 = k; v0 = v; }
+      else { k0 = uk0; v0 = uv0; }
+    }
+    size = min(size + 1, K);
+  }
+  // offer 32 candidates (one per lane): the ones that beat the current last entry enter
+  __device__ __forceinline__ void offer(bool valid, unsigned long long k, uint32_t v, int lane,
+                                       int K) {
+    const unsigned long long bar = size == K ? key_at(K - 1) : 0ull;
+    unsigned pending = __ballot_sync(0xffffffffu, valid && (size < K || k > bar));
+    while (pending) {
+      const int src = __ffs(pending) - 1;
+      pending &= pending - 1;
+      const unsigned long long kk = __shfl_sync(0xffffffffu, k, src);
+      const uint32_t vv = __shfl_sync(0xffffffffu, v, src);
+      if (size == K && kk <= key_at(K - 1)) continue;
+      insert(kk, vv, lane, K);
+    }
+  }
+};
+
+// One warp rebuilds hub u's list (prompt p's partition) if it is not valid:
+// the previous list's last count bounds the threshold from below (counts
+// only grow), else a lane-wise top-2 pass over the children picks one; then
+// every child at or above it is ranked into a sorted warp list of K entries.
+// Ordinary loads: the fused step orders them after the acquire of the
+// prompt's release (step.cu).
+// The caller orders it before any reader of p's lists.
+__device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int lane) {
+  if (u >= c.H) return;  // roots are never expanded
+  const uint4 r = *rec_of(c, u);
+  const uint32_t nch = r.x;
+  if (nch <= HUB_MIN) return;
+  const uint32_t slot = hub_slot(c, p, u);
+  const bool same = c.hub_node[slot] == u;
+  if (same && c.hub_nch[slot] == nch && c.hub_csum[slot] == r.w) return;  // still valid
+  const int K = min(HUB_K, c.Bmax);
+  const uint32_t nb = blk_index(nch - 2) + 1;
+  const uint32_t mybase = lane < (int)nb ? block_base(c, u, lane) : 0u;
+  auto pos_of = [&](uint32_t k) {
+    const uint32_t jj = k - 1;
+    const uint32_t bi = blk_index(jj);
+    const uint32_t base = __shfl_sync(0xffffffffu, mybase, (int)(bi & 31));
+    return base + (jj - blk_start(bi));
+  };
+  constexpr int U4 = 8;  // child loads in flight per lane
+  uint32_t thr = 0;
+  if (same && c.hub_len[slot] == (uint32_t)K) {
+    thr = c.hub_cnt[(size_t)slot * HUB_K + K - 1];
+  } else {
+    uint32_t t1 = 0, t2 = 0;
+    for (uint32_t kb = 0; kb < nch; kb += U4 * 32) {
+      uint32_t cv[U4];
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * 32 + lane;
+        const uint32_t pos = pos_of(k >= 1 ? k : 1);  // (a shuffle: every lane)
+        cv[q] = k == 0 ? c.cnt[r.y] : k < nch ? c.scnt[pos] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        if (cv[q] > t1) { t2 = t1; t1 = cv[q]; }
+        else if (cv[q] > t2) t2 = cv[q];
+      }
+    }
+    for (int i = 0; i < K; ++i) {  // the K-th largest of the lanes' top-2 counts
+      thr = __reduce_max_sync(0xffffffffu, t1);
+      const unsigned who = __ballot_sync(0xffffffffu, t1 == thr);
+      if (lane == __ffs(who) - 1) { t1 = t2; t2 = 0; }
+    }
+  }
+  KeyList L{0ull, 0ull, NONE, NONE, 0};
+  for (uint32_t kb = 0; kb < nch; kb += U4 * 32) {
+    uint32_t cv[U4], pv[U4];
+#pragma unroll
+    for (int q = 0; q < U4; ++q) {
+      const uint32_t k = kb + q * 32 + lane;
+      pv[q] = pos_of(k >= 1 ? k : 1);
+      cv[q] = k == 0 ? c.cnt[r.y] : k < nch ? c.scnt[pv[q]] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < U4; ++q) {
+      const uint32_t k = kb + q * 32 + lane;
+      const bool in = k < nch && cv[q] >= thr;
+      if (__any_sync(0xffffffffu, in)) {
+        uint32_t id = NONE;
+        int32_t tk = 0;
+        if (in) {
+          if (k == 0) { id = r.y; tk = (int32_t)r.z; }
+          else { id = c.slots[pv[q]]; tk = c.stok[pv[q]]; }
+        }
+        L.offer(in, child_key(cv[q], tk), id, lane, K);
+      }
+    }
+  }
+  const size_t e = (size_t)slot * HUB_K;
+  if (lane < L.size) {
+    c.hub_child[e + lane] = L.v0;
+    c.hub_tok[e + lane] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k0);
+    c.hub_cnt[e + lane] = (uint32_t)(L.k0 >> 32);
+  }
+  if (lane + 32 < L.size) {
+    c.hub_child[e + lane + 32] = L.v1;
+    c.hub_tok[e + lane + 32] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k1);
+    c.hub_cnt[e + lane + 32] = (uint32_t)(L.k1 >> 32);
+  }
+  if (lane == 0) {
+    c.hub_len[slot] = (uint32_t)L.size;
+    c.hub_nch[slot] = nch;
+    c.hub_csum[slot] = r.w;
+    c.hub_node[slot] = u;
+  }
+  __syncwarp();
+}
+
+// Hub u's list rebuilt from its previous list and the children counted since
+// it was built (kids[i * kstride], i < m, one count increment each): the new top K is
+// among those (a child neither listed nor counted kept its count, below the
+// old K-th entry's, which only grew).  Exact only when the touches account
+// for the whole csum change since the build; otherwise (no previous list, a
+// NONE touch = a hub a draft met without a list, lost touches) the full
+// scan of refresh_hub_warp.  sid: >= 96 words of this warp's shared memory.
+__device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const uint32_t* kids,
+                                 uint32_t m, uint32_t kstride, int lane, uint32_t* sid) {
+  if (u >= c.H) return;
+  const uint4 r = *rec_of(c, u);
+  const uint32_t nch = r.x;
+  if (nch <= HUB_MIN) return;
+  const uint32_t slot = hub_slot(c, p, u);
+  const bool same = c.hub_node[slot] == u;
+  if (same && c.hub_nch[slot] == nch && c.hub_csum[slot] == r.w) return;  // still valid
+  const int K = min(HUB_K, c.Bmax);
+  bool incr = same && K <= 32 && m <= 64 && c.hub_len[slot] == (uint32_t)K &&
+              r.w - c.hub_csum[slot] == m;
+  const uint32_t k0 = lane < (int)m ? kids[(size_t)lane * kstride] : 0u;
+  const uint32_t k1 = lane + 32 < (int)m ? kids[(size_t)(lane + 32) * kstride] : 0u;
+  incr = incr && !__any_sync(0xffffffffu, k0 == NONE || k1 == NONE);
+  if (!incr) {
+    refresh_hub_warp(c, p, u, lane);
+    return;
+  }
+  const size_t e = (size_t)slot * HUB_K;
+  const int ncand = K + (int)m;  // <= 96
+  if (lane < K) sid[lane] = c.hub_child[e + lane];
+  if (lane < (int)m) sid[K + lane] = k0;
+  if (lane + 32 < (int)m) sid[K + 32 + lane] = k1;
+  __syncwarp();
+  KeyList L{0ull, 0ull, NONE, NONE, 0};
+  for (int j0 = 0; j0 < ncand; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = j < ncand;
+    uint32_t id = keep ? sid[j] : NONE;
+    for (int i = 0; keep && i < j; ++i) keep = sid[i] != id;  // first occurrence only
+    unsigned long long key = 0;
+    if (keep) key = child_key(c.cnt[id], c.tok[id]);
+    L.offer(keep, key, id, lane, K);
+  }
+  if (lane < L.size) {
+    c.hub_child[e + lane] = L.v0;
+    c.hub_tok[e + lane] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k0);
+    c.hub_cnt[e + lane] = (uint32_t)(L.k0 >> 32);
+  }
+  if (lane == 0) {
+    c.hub_len[slot] = (uint32_t)L.size;
+    c.hub_nch[slot] = nch;
+    c.hub_csum[slot] = r.w;
+    c.hub_node[slot] = u;
+  }
+  __syncwarp();
+}
+
+}  // namespace
+}  // namespace srt

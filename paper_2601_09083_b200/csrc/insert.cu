@@ -195,7 +195,8 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
     S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
     S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
     S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
-    S.dbuf = reinterpret_cast<uint32_t*>(S.nlog + 4);
+    S.dbuf = reinterpret_cast<uint4*>(S.nlog + 4);
+    S.pdl = nullptr;
   }
   if (lane == 0) S.nlog[0] = S.nlog[1] = S.nlog[2] = 0;
   __syncwarp();
@@ -205,7 +206,7 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
   for (long long base = ((long long)blockIdx.x * CURSOR_WARPS + w) * 32; base < total;
        base += stride_w) {
     const long long idx = base + lane;
-    int32_t i = 0, j = 0, end = 0, f = 0;
+    int32_t i = 0, j = 0, end = 0, f = 0, pr = 0;
     uint32_t u = NONE;
     const int32_t* toks = nullptr;
     if (idx < total) {
@@ -218,7 +219,8 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
       f = from[s];
       i = span_lo(f, floor_ ? floor_[s] : 0, c.D) + (int32_t)(idx - offs[s]);
       toks = seq_tok + (int64_t)s * stride;
-      u = root_id(c, prompt_id[s]);
+      pr = prompt_id[s];
+      u = root_id(c, pr);
       end = min(i + c.D, to[s]);
       j = i;
       ++windows;
@@ -251,7 +253,7 @@ k_insert_walk(DevCache c, int32_t n, const int32_t* __restrict__ prompt_id,
           if (!cre[0] && is_slot_word(aux[0])) atomicAdd(&c.scnt[aux[0]], 1u);
         }
       }
-      dirty_push(c, S, counted && j - i >= 1 && j - i <= HUB_DIRTY_DEPTH, u, lane);
+      dirty_push(c, S, counted && j - i >= 1 && j - i <= HUB_DIRTY_DEPTH, u, pr, h, lane);
       const unsigned mc = __ballot_sync(0xffffffffu, a && cre[0]);
       const unsigned mp = __ballot_sync(0xffffffffu, counted && !cre[0] && aux[0] == NONE);
       if (mc | mp) {

@@ -415,14 +415,17 @@ struct CursorSmem {
   int32_t* log_tok;   // [LOGCAP] ... their tokens
   uint32_t* pend;     // [LOGCAP] nodes whose slot word was not published yet
   int* nlog;          // [4] created, pending, dirty
-  uint32_t* dbuf;     // [DBUF] shallow parents whose csum changed (hub refresh), flushed in batches
+  uint4* dbuf;        // [DBUF] (node, prompt, child, 0): shallow parents whose csum changed
+                      // (hub refresh) and the child counted, flushed in batches
+  uint32_t* pdl;      // null: flushed to the global dirty list; else the warp's prompt's own
+                      // list ([0] count, then (hub, child) pairs: the fused tree step)
 };
 constexpr int DBUF = 96;
 
 __host__ __device__ __forceinline__ size_t cursor_warp_bytes(int32_t D) {
   const size_t a = ((size_t)(D + 1) * 4 + 15) & ~size_t(15);
   const size_t f = ((size_t)(D + 1) + 15) & ~size_t(15);
-  return a + f + (size_t)LOGCAP * 16 + 16 + (size_t)DBUF * 4;
+  return a + f + (size_t)LOGCAP * 16 + 16 + (size_t)DBUF * 16;
 }
 
 // The dirty log (parents whose csum changed, for the hub refresh) is kept in
@@ -434,22 +437,31 @@ __device__ __forceinline__ void dirty_flush(const DevCache& c, const CursorSmem&
   const int nd = S.nlog[2];
   if (nd) {
     uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(c.dirty_n, (uint32_t)nd);
+    if (lane == 0) base = atomicAdd(S.pdl ? S.pdl : c.dirty_n, (uint32_t)nd);
     base = __shfl_sync(0xffffffffu, base, 0);
-    for (int i = lane; i < nd; i += 32)
-      if (base + i < DIRTY_CAP) c.dirty[base + i] = S.dbuf[i];
+    for (int i = lane; i < nd; i += 32) {
+      const uint4 e = S.dbuf[i];
+      if (S.pdl) {
+        if (base + i < PDIRTY_CAP) {
+          S.pdl[2 + 2 * (base + i)] = e.x;
+          S.pdl[3 + 2 * (base + i)] = e.z;
+        }
+      } else if (base + i < DIRTY_CAP) {
+        c.dirty[base + i] = make_uint2(e.x, e.y);
+      }
+    }
   }
   __syncwarp();
   if (lane == 0) S.nlog[2] = 0;
   __syncwarp();
 }
 __device__ __forceinline__ void dirty_push(const DevCache& c, const CursorSmem& S, bool want,
-                                           uint32_t u, int lane) {
+                                           uint32_t u, int32_t p, uint32_t child, int lane) {
   const unsigned m = __ballot_sync(0xffffffffu, want);
   if (!m) return;
   if (S.nlog[2] + __popc(m) > DBUF) dirty_flush(c, S, lane);
   const int nd = S.nlog[2];
-  if (want) S.dbuf[nd + __popc(m & lanemask_lt())] = u;
+  if (want) S.dbuf[nd + __popc(m & lanemask_lt())] = make_uint4(u, (uint32_t)p, child, 0u);
   __syncwarp();
   if (lane == 0) S.nlog[2] = nd + __popc(m);
   __syncwarp();
@@ -525,7 +537,8 @@ __device__ __forceinline__ CursorSmem carve_cursor_smem(unsigned char* base, int
   S.log_tok = reinterpret_cast<int32_t*>(S.log_par + LOGCAP);
   S.pend = reinterpret_cast<uint32_t*>(S.log_tok + LOGCAP);
   S.nlog = reinterpret_cast<int*>(S.pend + LOGCAP);
-  S.dbuf = reinterpret_cast<uint32_t*>(S.nlog + 4);
+  S.dbuf = reinterpret_cast<uint4*>(S.nlog + 4);
+  S.pdl = nullptr;
   return S;
 }
 
@@ -636,7 +649,7 @@ __device__ __forceinline__ void cursor_insert_seq(
       }
       if (gw + g == 0) {  // shallow parents whose csum changed: their hub lists are rebuilt after the call
         const int32_t l = lane + 1;
-        dirty_push(c, S, a && l >= 2 && l <= 1 + HUB_DIRTY_DEPTH, par[g], lane);
+        dirty_push(c, S, a && l >= 2 && l <= 1 + HUB_DIRTY_DEPTH, par[g], p, h, lane);
       }
       const unsigned mc = __ballot_sync(0xffffffffu, a && cre[g]);
       const unsigned mp = __ballot_sync(0xffffffffu, a && !cre[g] && aux[g] == NONE);

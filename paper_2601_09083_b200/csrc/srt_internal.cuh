@@ -31,6 +31,20 @@
 
 #include "../../include/srt.h"
 
+// Read-only loads of tree data.  A kernel that reads tree data other warps
+// wrote in the SAME launch (the fused tree step, step.cu, defines
+// SRT_COHERENT_LOADS before any include) must not use the non-coherent
+// read-only path (ld.global.nc is outside the memory model): it uses
+// ordinary loads, which the memory model orders after the acquire of the
+// release that published the data (step.cu's per-prompt ready flags).
+#ifdef SRT_COHERENT_LOADS
+#define SRT_LDG(p) (*(p))
+#define SRT_LD(x) (x)
+#else
+#define SRT_LDG(p) __ldg(p)
+#define SRT_LD(x) (x)
+#endif
+
 namespace srt {
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;  // "no block" / "value pending"
@@ -72,6 +86,18 @@ struct DevCache {
   unsigned long long* ctr;  // [0] nodes created (+ P roots), [1] next slot word
   uint32_t* status;         // sticky SRT_DEV_* bits
   uint32_t* sched;          // [2] the scan's row-claim counters (0 between launches)
+  // the fused tree step (step.cu): per prompt, sequences in the batch, sequences
+  // committed and inserted, list refresh done; drafts done; and each prompt's
+  // dirty hubs ([0] count, then PDIRTY_CAP nodes; consumed by its refresh)
+  uint32_t* st_pcount;      // [P]
+  uint32_t* st_pdone;       // [P]
+  uint32_t* st_pready;      // [P] 0 = inserting, 1 = hub refresh tasks published, 2 = ready
+  uint32_t* st_pnd;         // [P] refresh tasks (the prompt's dirty hubs)
+  uint32_t* st_pnext;       // [P] next task to claim
+  uint32_t* st_pfin;        // [P] tasks finished
+  uint32_t* st_ndone;       // [1]
+  uint32_t* pdirty;         // [P][PDIRTY_WORDS]: [0] touches, then (hub, child) pairs, then
+                            // the task starts (the pairs sorted by hub)
   float* gbound;  // [0, 1024) bucket maxima, [1024] global max, [1025, 2049) bucket minima of
                   // G64; [2049, 3073) bucket maxima of the single-word Gumbel g(r)
   // Hub child lists: for a node with more than HUB_MIN
@@ -89,13 +115,22 @@ struct DevCache {
   int32_t* hub_tok;     // [HC][HUB_K]
   uint32_t* hub_cnt;    // [HC][HUB_K]
   unsigned long long* hub_claim;  // [HC] (insert call << 32 | node) of the last refresh claim
-  uint32_t* dirty;      // [DIRTY_CAP] parents whose csum an insert changed (shallow ones) and hubs a draft found without a valid list
+  uint32_t hub_shift;   // log2 of the slots per prompt: prompt p's hubs live in slots
+                        // [p << hub_shift, (p + 1) << hub_shift) (a refresh of one prompt never
+                        // rewrites a list another prompt's draft may be reading)
+  uint2* dirty;         // [DIRTY_CAP] (node, prompt): parents whose csum an insert changed (shallow ones) and hubs a draft found without a valid list
   uint32_t* dirty_n;    // [0] entries, [1] refresh generation (a device counter: graph-safe)
 };
 
 constexpr uint32_t HUB_MIN = 64;  // listed above this fan-out (measured: 32 / 128 / 256 slower or equal)
 constexpr int HUB_K = 64;          // >= Bmax
 constexpr uint32_t DIRTY_CAP = 1u << 20;
+// fused tree step (step.cu): per prompt, the (hub, child) count increments of
+// the step's inserts at shallow parents (child NONE: a hub a draft met
+// without a valid list), then the refresh tasks (one per distinct hub)
+constexpr uint32_t PDIRTY_CAP = 255;
+// [0] count, [1] pad, pairs at 2 + 2i, task ranges (u32 pairs, 8-byte aligned) at 2 + 2 CAP
+constexpr size_t PDIRTY_WORDS = 2 + 4 * (size_t)PDIRTY_CAP;
 constexpr int HUB_DIRTY_DEPTH = 2;  // parents at depth 1..2 are logged as dirty
 
 // Candidate (z, v) packed so that a larger u64 is the better candidate under
@@ -186,8 +221,8 @@ __device__ __forceinline__ uint32_t hash_find(const DevCache& c, unsigned long l
   unsigned long long h = home_slot(c, key);
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
     const HashSlot* s = c.hash + h;
-    const unsigned long long k = __ldg(&s->key);
-    if (k == key) return __ldg(&s->val);
+    const unsigned long long k = SRT_LDG(&s->key);
+    if (k == key) return SRT_LDG(&s->val);
     if (k == EMPTY_KEY) return NONE;
     h = (h + 1) & mask;
   }
@@ -199,7 +234,7 @@ __device__ __forceinline__ uint32_t hash_slot(const DevCache& c, unsigned long l
   unsigned long long mask = c.H - 1;
   unsigned long long h = home_slot(c, key);
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
-    const unsigned long long k = __ldg(&c.hash[h].key);
+    const unsigned long long k = SRT_LDG(&c.hash[h].key);
     if (k == key) return (uint32_t)h;
     if (k == EMPTY_KEY) return NONE;
     h = (h + 1) & mask;
@@ -216,7 +251,7 @@ __device__ __forceinline__ uint32_t root_id(const DevCache& c, int32_t p) {
 }
 
 // record of node u: {nchild, child0, token of child0, csum}
-__device__ __forceinline__ uint4 ld_rec(const DevCache& c, uint32_t u) { return __ldg(&c.rec[2 * (size_t)u]); }
+__device__ __forceinline__ uint4 ld_rec(const DevCache& c, uint32_t u) { return SRT_LDG(&c.rec[2 * (size_t)u]); }
 __device__ __forceinline__ uint4* rec_of(const DevCache& c, uint32_t u) { return &c.rec[2 * (size_t)u]; }
 // the record's block words (base of child block i < 4, + 1; 0 = not created)
 __device__ __forceinline__ uint32_t* rec_bases(const DevCache& c, uint32_t u) {
@@ -225,7 +260,7 @@ __device__ __forceinline__ uint32_t* rec_bases(const DevCache& c, uint32_t u) {
 // First slot word of child block i of node u (read-only kernels).
 __device__ __forceinline__ uint32_t block_base(const DevCache& c, uint32_t u, uint32_t i) {
   if (i < 4) {
-    const uint32_t b = __ldg(rec_bases(c, u) + i);
+    const uint32_t b = SRT_LDG(rec_bases(c, u) + i);
     return b ? b - 1 : NONE;
   }
   return hash_find(c, block_key(u, i));
@@ -281,6 +316,7 @@ cudaError_t launch_insert_cursor(const DevCache& c, int32_t n, const int32_t* pr
                                  uint32_t* cursor, uint32_t tag, srt_insert_stats* stats,
                                  cudaStream_t stream);
 size_t insert_cursor_smem(int32_t D);
+
 cudaError_t launch_insert_walk(const DevCache& c, int32_t n, const int32_t* prompt_id,
                                const int32_t* seq_tok, int64_t stride, const int32_t* from,
                                const int32_t* to, const int32_t* floor_, srt_insert_stats* stats,
@@ -352,6 +388,13 @@ cudaError_t launch_scan(const DevCache& c, const VerifyArgs& a, bool reference, 
                         unsigned long long* result, cudaStream_t stream);
 cudaError_t launch_accept(const DevCache& c, const VerifyArgs& a, const unsigned long long* result,
                           cudaStream_t stream);
+cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
+                             const unsigned long long* result, const int32_t* prompt_id,
+                             const int32_t* floor_, uint32_t* cursor, uint32_t tag,
+                             srt_insert_stats* stats, const int32_t* pos_base, int32_t* match_len,
+                             int32_t* draft_len, int32_t* draft_tok, int32_t* draft_parent,
+                             int32_t* draft_depth, int32_t* draft_pos, uint64_t* draft_mask,
+                             int64_t* row_offsets, cudaStream_t stream);
 cudaError_t launch_accept_insert(const DevCache& c, const VerifyArgs& a,
                                  const unsigned long long* result, const int32_t* prompt_id,
                                  const int32_t* floor_, uint32_t* cursor, uint32_t tag,
@@ -390,19 +433,10 @@ cudaError_t launch_load_level(const DevCache& c, const uint32_t* parent_ids, con
                               uint32_t* out_ids, cudaStream_t stream);
 cudaError_t launch_hub_refresh(const DevCache& c, uint32_t call, uint32_t* work, uint32_t* work_n,
                                cudaStream_t stream);
-__device__ __forceinline__ uint32_t hub_slot(const DevCache& c, uint32_t u) {
-  return (uint32_t)(mix64(0x4855420000000000ull ^ u) & (c.HC - 1));
-}
-// Log a parent whose csum just changed (warp-collective: every lane calls it).
-__device__ __forceinline__ void log_dirty(const DevCache& c, bool want, uint32_t u) {
-  const unsigned m = __ballot_sync(0xffffffffu, want);
-  if (!m) return;
-  const int lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  if (lane == __ffs(m) - 1) base = atomicAdd(c.dirty_n, (uint32_t)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-  const uint32_t e = base + __popc(m & lanemask_lt());
-  if (want && e < DIRTY_CAP) c.dirty[e] = u;
+// the hub-list slot of node u of prompt p (direct-mapped inside p's partition)
+__device__ __forceinline__ uint32_t hub_slot(const DevCache& c, int32_t p, uint32_t u) {
+  return ((uint32_t)p << c.hub_shift) |
+         (uint32_t)(mix64(0x4855420000000000ull ^ u) & ((1ull << c.hub_shift) - 1));
 }
 cudaError_t launch_dump_level(const DevCache& c, const uint32_t* frontier, int32_t nf,
                               uint32_t* out_node, int32_t* out_parent, int32_t* out_tok,

@@ -223,6 +223,44 @@ class SrtCache:
             _ptr(stats, torch.int64, "stats"), _stream()), "srt_verify_insert_cursor")
         return out
 
+    def verify_insert_draft(self, logits, d: DraftOut, seq_id, seed: int, seq_tok, seq_len,
+                            max_new, prompt_id, cursor, pos_base=None, next_d: DraftOut | None = None,
+                            floor=None, stats=None, temperature: float = 1.0, eos_id: int = -1,
+                            out: VerifyOut | None = None, rows: int | None = None) -> VerifyOut:
+        """srt_verify_insert_draft_cursor: verify_insert() then the next step's
+        draft_cursor(prompt_id, seq_tok, seq_len, pos_base) in one persistent
+        kernel ordered per prompt.  next_d may be d itself (the draft buffers
+        are reused); pos_base may be seq_len (read after the commit)."""
+        n = seq_len.shape[0]
+        if logits.dtype != self.logits_dtype:
+            raise SrtError(f"logits dtype {logits.dtype} != cache's {self.logits_dtype}")
+        if logits.shape[-1] != self.V:
+            raise SrtError("logits row length != V")
+        if cursor.shape != (n, self.cfg.max_depth + 4):
+            raise ValueError(f"cursor must be ({n}, D + 4) int32")
+        if next_d is None:
+            next_d = d
+        if out is None:
+            out = VerifyOut.empty(n, logits.shape[0] if rows is None else rows, self.Bmax,
+                                  seq_tok.device)
+        i32 = torch.int32
+        check(self.L.srt_verify_insert_draft_cursor(
+            self._h, n, _ptr(logits, None, "logits"), _ptr(d.row_offsets, torch.int64),
+            _ptr(d.draft_len, i32), _ptr(d.draft_tok, i32), _ptr(d.draft_parent, i32),
+            _ptr(d.draft_depth, i32), _ptr(seq_id, torch.int64, "seq_id"),
+            ctypes.c_uint64(seed & (2 ** 64 - 1)), float(temperature), int(eos_id),
+            _ptr(max_new, i32, "max_new"), _ptr(seq_tok, i32, "seq_tok"), seq_tok.shape[1],
+            _ptr(seq_len, i32, "seq_len"), _ptr(out.sampled, i32), _ptr(out.accept_len, i32),
+            _ptr(out.n_commit, i32), _ptr(out.commit_tok, i32), _ptr(out.accepted_nodes, i32),
+            _ptr(out.finished, torch.uint8), _ptr(prompt_id, i32, "prompt_id"),
+            _ptr(floor, i32, "floor"), _ptr(cursor, i32, "cursor"),
+            _ptr(stats, torch.int64, "stats"), _ptr(pos_base, i32, "pos_base"),
+            _ptr(next_d.match_len, i32), _ptr(next_d.draft_len, i32), _ptr(next_d.draft_tok, i32),
+            _ptr(next_d.draft_parent, i32), _ptr(next_d.draft_depth, i32),
+            _ptr(next_d.draft_pos, i32), _ptr(next_d.draft_mask, torch.int64),
+            _ptr(next_d.row_offsets, torch.int64), _stream()), "srt_verify_insert_draft_cursor")
+        return out
+
     def verify_lmhead(self, hidden, weight, d: DraftOut, seq_id, seed: int, seq_tok, seq_len,
                       max_new, prompt_id=None, cursor=None, floor=None, stats=None,
                       temperature: float = 1.0, eos_id: int = -1, out: VerifyOut | None = None,

@@ -129,3 +129,46 @@ def test_graph_replay_matches_eager():
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("D", [16, 32])
+def test_fused_tree_step_matches_separate_calls(D):
+    """srt_verify_insert_draft_cursor (commit + cursor insert + per-prompt hub
+    refresh + the next draft in one persistent kernel) leaves exactly what
+    srt_verify_insert_cursor then srt_draft_cursor leave, step after step:
+    sampled rows, commits, sequence tables, trees, the next drafts and row
+    offsets (both from the same buffers the next step reads)."""
+    import torch
+    import bench
+    cfg = dict(bench.CONFIGS["grpo"])
+    cfg.update(prompts=12, active=96, V=5000, cap=1024, act_cap=1024, median=300,
+               node_capacity=1 << 21, D=D, L=8)
+    out = []
+    for fused_step in (False, True):
+        wl = bench.Workload(cfg, 3)
+        run = bench.GpuRun(wl, "bf16", "rl-mix", 3)
+        gr = run.groups[0]
+        gr.fused_step = fused_step
+        rec = []
+        for k in range(8):
+            run.step(bench.step_seed(3, k))
+            if not fused_step:
+                gr.draft()  # the next step's draft, as the fused call makes it
+            torch.cuda.synchronize()
+            rec.append(tuple(getattr(gr.d, k).cpu().numpy().copy() for k in
+                             ("match_len", "draft_len", "draft_tok", "draft_parent",
+                              "draft_depth", "draft_pos", "draft_mask", "row_offsets")) +
+                       (gr.v.n_commit.cpu().numpy().copy(), gr.v.commit_tok.cpu().numpy().copy(),
+                        gr.v.accept_len.cpu().numpy().copy()))
+        torch.cuda.synchronize()
+        assert run.status()[0] == 0
+        out.append((rec, gr.seq_tok.cpu().numpy(), gr.seq_len.cpu().numpy(),
+                    [gr.cache.dump(p) for p in range(cfg["prompts"])]))
+    (ra, ta, la, da), (rb, tb, lb, db) = out
+    for x, y in zip(ra, rb):
+        for u, v in zip(x, y):
+            np.testing.assert_array_equal(u, v)
+    np.testing.assert_array_equal(ta, tb)
+    np.testing.assert_array_equal(la, lb)
+    assert da == db
+    assert sum(int(r[1].sum()) for r in ra) > 0 and sum(int(r[8].sum()) for r in ra) > 96 * 8

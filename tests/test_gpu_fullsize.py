@@ -66,6 +66,9 @@ def test_fullsize_sampled_parity(orc, config, steps, n_prompts, n_rows):
     wl = bench.Workload(cfg, 0)
     run = bench.GpuRun(wl, "bf16", "rl-mix", 0)
     gr = run.groups[0]
+    # the launch configuration bench.py times: D <= 32 runs the fused tree step
+    # (srt_verify_insert_draft_cursor: commit + insert + refresh + next draft)
+    gr.fused_step = cfg["D"] <= 32
     for k in range(steps):
         run.step(bench.step_seed(0, k))
     torch.cuda.synchronize()
@@ -81,9 +84,10 @@ def test_fullsize_sampled_parity(orc, config, steps, n_prompts, n_rows):
     seq_len = gr.seq_len.cpu().numpy()
 
     # ---- the step under test: draft -> stand-in -> fused verify + insert -----
-    # (gr.verify_insert = srt_verify_insert_cursor, the kernel bench.py times,
-    # plus DAPO's run-ahead spans)
-    gr.draft()
+    # (gr.verify_insert = srt_verify_insert_draft_cursor for D <= 32, else
+    # srt_verify_insert_cursor -- the kernels bench.py times -- plus DAPO's
+    # run-ahead spans; with the fused step this draft is the previous call's)
+    gr.draft_if_needed()
     gr.standin()
     seed = bench.step_seed(0, steps)
     torch.cuda.synchronize()
@@ -155,6 +159,21 @@ def test_fullsize_sampled_parity(orc, config, steps, n_prompts, n_rows):
     # trees after the fused kernel's insert
     for p, o, _, _ in trees:
         _dump_equal(gr.cache, p, o)
+    if gr.fused_step:
+        # the NEXT drafts the fused call made from those trees, and the row offsets
+        torch.cuda.synchronize()
+        nd = {k: getattr(gr.d, k).cpu().numpy() for k in
+              ("match_len", "draft_len", "draft_tok", "draft_parent", "draft_depth", "draft_pos")}
+        nd["draft_mask"] = gr.d.draft_mask.cpu().numpy().view(np.uint64)
+        nro = gr.d.row_offsets.cpu().numpy()
+        assert nro[0] == 0 and np.array_equal(np.diff(nro), nd["draft_len"].astype(np.int64) + 1)
+        for p, o, seqs, _ in trees:
+            if not len(seqs):
+                continue
+            od2 = o.draft(np.zeros(len(seqs), np.int32), g_tok_after[seqs], g_len_after[seqs],
+                          g_len_after[seqs])
+            for k, v in nd.items():
+                assert np.array_equal(v[seqs], od2[k].astype(v.dtype)), (config, p, "next", k)
 
     # ---- random rows of the whole batch: full-V oracle Gumbel-max ------------
     total = int(row_off[-1])

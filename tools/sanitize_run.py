@@ -1,7 +1,8 @@
 """compute-sanitizer driver (SURVEY §5.2 race / memory evidence): a few eager
 steps of a small GRPO-shaped configuration (V = 151,936, 48 sequences, the
 same kernels bench.py times: cursor draft, scan, fused accept + cursor insert,
-hub refresh, walk insertion), the tiny configuration, the LM-head fused
+hub refresh, walk insertion; then the same with the fused tree step
+srt_verify_insert_draft_cursor), the tiny configuration, the LM-head fused
 sampler, and a D = 128 multi-warp cursor insert with sibling spans.
     compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_run.py"""
 import sys
@@ -14,20 +15,24 @@ import bench  # noqa: E402
 import paper_2601_09083_b200 as srt  # noqa: E402
 
 
-def small(name, **over):
+def small(name, fused_step=False, **over):
     cfg = dict(bench.CONFIGS[name])
     cfg.update(over)
     wl = bench.Workload(cfg, 1)
     run = bench.GpuRun(wl, "bf16", "rl-mix", 1)
+    run.groups[0].fused_step = fused_step
     for k in range(3):
         run.step(bench.step_seed(1, k))
     torch.cuda.synchronize()
     bits, _ = run.status()
-    print(f"[sanitize] {name} {cfg['active']} seqs: 3 steps, error bits {bits}", flush=True)
+    print(f"[sanitize] {name} {cfg['active']} seqs{' (fused tree step)' if fused_step else ''}: "
+          f"3 steps, error bits {bits}", flush=True)
     return run
 
 
 small("grpo", prompts=6, active=48, cap=1024, act_cap=1024, median=300, node_capacity=1 << 20)
+small("grpo", True, prompts=6, active=48, cap=1024, act_cap=1024, median=300,
+      node_capacity=1 << 20)
 small("tiny")
 run = small("grpo", prompts=4, active=32, cap=512, act_cap=512, median=200, node_capacity=1 << 20)
 run.enable_lmhead(256, 1)
