@@ -6,6 +6,8 @@
 namespace srt {
 namespace {
 
+__device__ unsigned long long g_refresh_stats[2];  // development: incremental, full-scan rebuilds
+
 __device__ __forceinline__ unsigned long long child_key(uint32_t cnt, int32_t tok) {
   return ((unsigned long long)cnt << 32) | (0xFFFFFFFFu - (uint32_t)tok);  // larger = better
 }
@@ -171,6 +173,7 @@ __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const
   const uint32_t k0 = lane < (int)m ? kids[(size_t)lane * kstride] : 0u;
   const uint32_t k1 = lane + 32 < (int)m ? kids[(size_t)(lane + 32) * kstride] : 0u;
   incr = incr && !__any_sync(0xffffffffu, k0 == NONE || k1 == NONE);
+  if (lane == 0) atomicAdd(&g_refresh_stats[incr ? 0 : 1], 1ull);
   if (!incr) {
     refresh_hub_warp(c, p, u, lane);
     return;

@@ -386,6 +386,10 @@ cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
       draft_max = std::max(draft_max, (double)(q[3] - q[2]));
       if (q[5]) { ++nref; rsum += q[4]; rmax = std::max(rmax, q[4]); hubs += q[5]; }
     }
+    unsigned long long rs[2] = {0, 0};
+    cudaMemcpyFromSymbol(rs, g_refresh_stats, sizeof rs);
+    fprintf(stderr, "[tree step] hub refreshes so far: %llu incremental, %llu full scans\n", rs[0],
+            rs[1]);
     fprintf(stderr, "[tree step] warps %d: phase1 end max %.1f mean %.1f us; wait max %.1f mean %.1f us; "
             "release max %.1f us; draft max %.1f mean %.1f us; end %.1f us; refreshes %d (%llu hubs) "
             "max %.1f mean %.1f kcycles\n",
