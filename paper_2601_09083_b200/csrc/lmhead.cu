@@ -650,6 +650,88 @@ __global__ void __launch_bounds__(128) k_lmhead_tail(DevCache c, LmParams p) {
   }
 }
 
+
+// A lower bound on each row's winning z before the GEMM (§8d): the row's
+// first drafted child token (the draft's most likely continuation; none for
+// a leaf row) gets its logit as a CUDA-core fp32 dot product, lowered by a
+// margin that covers both that sum's and the tensor cores' accumulation
+// error (2 K 2^-20 sum |h_k w_k|: 16x the fp32 bound), rounded like the
+// kernel's logit (monotone, so still below the logit the kernel will see),
+// and z = RN(RN(x/T) + g) with the element's exact noise (O11).  That is a
+// lower bound on an achieved z of the row, so every block whose bound is
+// below it can be skipped from the first tile on; it is stored as the row's
+// packed candidate (hint's exact z >= it replaces it when the hint's block is
+// evaluated, and any winner beats it), never returned as such unless exact.
+template <int DT>
+__global__ void __launch_bounds__(256) k_lmhead_seed(DevCache c, VerifyArgs a,
+                                                     const __nv_bfloat16* __restrict__ hidden,
+                                                     const __nv_bfloat16* __restrict__ W, int32_t K,
+                                                     const int2* __restrict__ rowinfo,
+                                                     unsigned long long* __restrict__ result) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = a.row_offsets[a.n];
+  const int32_t B = c.Bmax;
+  const float T = a.temperature;
+  const bool unit_t = T == 1.0f;
+  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < total;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int2 ri = rowinfo[r];
+    const int32_t s = ri.x;
+    const int32_t i = (int32_t)(r - a.row_offsets[s]);  // 0 = root row, else node i - 1
+    const int32_t nd = a.draft_len[s];
+    const int32_t* par = a.draft_parent + (int64_t)s * B;
+    // the node's first child in pop order (children follow their parent)
+    const bool ca = lane < nd && lane >= i && par[lane] == i - 1;
+    const bool cb = lane + 32 < nd && lane + 32 >= i && par[lane + 32] == i - 1;
+    const unsigned ma = __ballot_sync(0xffffffffu, ca), mb = __ballot_sync(0xffffffffu, cb);
+    if (!(ma | mb)) continue;
+    const int32_t j = ma ? __ffs(ma) - 1 : 31 + __ffs(mb);
+    const int32_t hint = a.draft_tok[(int64_t)s * B + j];
+    if (hint < 0 || hint >= c.V) continue;
+    const __nv_bfloat16* h = hidden + r * (int64_t)K;
+    const __nv_bfloat16* w = W + (int64_t)hint * K;
+    float d = 0.0f, sabs = 0.0f;
+    for (int32_t k = lane * 8; k < K; k += 256) {  // K % 8 == 0 (checked on the host)
+      const uint4 hv = *reinterpret_cast<const uint4*>(h + k);
+      const uint4 wv = *reinterpret_cast<const uint4*>(w + k);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv);
+      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 hf = __bfloat1622float2(h2[q]), wf = __bfloat1622float2(w2[q]);
+        d = fmaf(hf.x, wf.x, d);
+        d = fmaf(hf.y, wf.y, d);
+        sabs += fabsf(hf.x * wf.x) + fabsf(hf.y * wf.y);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+      sabs += __shfl_xor_sync(0xffffffffu, sabs, o);
+    }
+    const float margin = 2.0f * (float)K * 9.5367431640625e-07f * sabs * 1.0001f;  // 2^-20
+    const float x = as_logit<DT>(d - margin);
+    if (!(x > -INFINITY) || !(x < INFINITY)) continue;
+    // the hint element's noise (O11)
+    const int64_t b = hint / NOISE_BLK;
+    const int n = block_len(c.V, b);
+    uint32_t wa, wb;
+    block_words((uint32_t)b, (uint32_t)ri.y, (uint32_t)a.seq_id[s], (uint32_t)(a.seq_id[s] >> 32),
+                k0, k1, wa, wb);
+    const BlockNoise bn = block_noise(wa, wb, (uint32_t)n);
+    float g = bn.G;
+    const uint32_t jb = (uint32_t)(hint - b * NOISE_BLK);
+    if (jb != bn.p) {
+      const Philox4 pw = philox4x32_10((uint32_t)(hint >> 2), (uint32_t)ri.y,
+                                       (uint32_t)a.seq_id[s], (uint32_t)(a.seq_id[s] >> 32), k0, k1);
+      const uint32_t e = (uint32_t)(hint & 3);
+      g = element_noise_from_word(e == 0 ? pw.x : e == 1 ? pw.y : e == 2 ? pw.z : pw.w, bn);
+    }
+    const float z = perturbed(x, g, T, unit_t);
+    if (lane == 0 && z == z) atomicMax(&result[r], pack_cand(z, hint));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -710,6 +792,11 @@ cudaError_t launch_lmhead_sample(const DevCache& c, const VerifyArgs& a, const L
   const size_t smem = 1024 + (size_t)NST * STAGE_BYTES + 2 * NST * 8 + 4 * 8 + 16 +
                       2 * NOISE_BUCKETS * 4;
   auto kern = a.dtype == SRT_BF16 ? k_lmhead_sample<SRT_BF16> : k_lmhead_sample<SRT_F32>;
+  if (!(p.debug & 256)) {  // the rows' seeded bounds (debug 256: off)
+    auto sk = a.dtype == SRT_BF16 ? k_lmhead_seed<SRT_BF16> : k_lmhead_seed<SRT_F32>;
+    sk<<<num_sms() * 8, 256, 0, stream>>>(c, a, (const __nv_bfloat16*)h.hidden,
+                                          (const __nv_bfloat16*)h.weight, h.K, rowinfo, result);
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (p.debug & 64) {

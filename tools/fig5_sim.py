@@ -37,7 +37,7 @@ def run_mode(mode, ra, a):
     cfg = SimConfig(V=151936, D=a.depth, L=8, Bmax=32, prompts_per_step=a.prompts,
                     samples=a.samples, steps=a.steps, mode=mode, run_ahead=ra, median=a.median,
                     cap=a.cap, seed=a.seed, ra_per_prompt=a.ra_per_prompt,
-                    node_capacity=1 << 28)
+                    node_capacity=1 << 29)
     t = time.time()
     sim = RolloutSim(cfg, GpuEngine(cfg, synth.SimPolicy(cfg.seed, cfg.V)),
                      synth.RolloutStreams(cfg.seed, cfg.V, cfg.median, cfg.cap))
@@ -56,8 +56,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--prompts", type=int, default=64)
     ap.add_argument("--samples", type=int, default=16)
-    ap.add_argument("--median", type=int, default=1500)
-    ap.add_argument("--cap", type=int, default=6000)
+    ap.add_argument("--median", type=int, default=1000)
+    ap.add_argument("--cap", type=int, default=4000)
     ap.add_argument("--depth", type=int, default=16)
     ap.add_argument("--ra-per-prompt", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
