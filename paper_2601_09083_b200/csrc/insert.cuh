@@ -611,7 +611,6 @@ __device__ __forceinline__ void cursor_insert_seq(
   if (MW) __syncthreads(); else __syncwarp();
   tp_cur = clock64() - tp0;
   constexpr int ngroups = NGL;
-  const unsigned long long mask = c.H - 1;
   int32_t ybuf = 0;  // the span's tokens, 32 positions per load (lane i: position j + i)
   for (int32_t j = P; j < t_end; ++j) {
     const long long tj = clock64();
