@@ -7,7 +7,10 @@ T=${1:-v1}
 O=gpurun_out/$T
 mkdir -p $O
 B="timeout 600 python bench.py"
+timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 $B > $O/bench_grpo.log 2>&1
+$B --fused-step 0 --no-cpu-baseline --e2e-steps 0 > $O/bench_grpo_unfused_step.log 2>&1
 $B --dtype f32 --no-cpu-baseline > $O/bench_grpo_f32.log 2>&1
 for p in peaked moderate flat; do $B --profile $p --no-cpu-baseline --e2e-steps 0 > $O/bench_grpo_$p.log 2>&1; done
 $B --config ppo --no-cpu-baseline > $O/bench_ppo.log 2>&1
@@ -19,11 +22,13 @@ timeout 300 python tools/scan_probe.py --rows 33792 --profiles rl-mix,peaked,mod
 timeout 300 python tools/scan_probe.py --rows 16896 --profiles rl-mix,peaked,flat --iters 6 --dtype f32 > $O/scan_fulldraft_f32.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --no-cpu-baseline --e2e-steps 0 --steps 3 --warmup 3 > $O/launch_bench.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_scan_rows" -s 3 -c 1 -o $O/scan python bench.py --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 4 > $O/ncu_scan.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_draft|k_accept|k_hub_refresh" -s 12 -c 3 -o $O/tree python bench.py --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 4 > $O/ncu_tree.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_tree_step" -s 3 -c 1 -o $O/tree python bench.py --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 4 > $O/ncu_tree.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_draft|k_accept|k_hub_refresh" -s 12 -c 3 -o $O/tree_unfused python bench.py --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 4 --fused-step 0 > $O/ncu_tree_unfused.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_lmhead_sample" -s 3 -c 1 -o $O/lmhead python bench.py --verify lmhead --no-cpu-baseline --e2e-steps 0 --steps 1 --warmup 4 > $O/ncu_lmhead.log 2>&1
 timeout 600 compute-sanitizer --tool racecheck python -c "
 import sys, torch; sys.path.insert(0, '.')
 import paper_2601_09083_b200 as srt
 b = torch.zeros(1 << 24, dtype=torch.bfloat16, device='cuda'); s = torch.zeros(1, dtype=torch.int64, device='cuda')
 srt.stream_read(b, 32768, 4, 1, s); torch.cuda.synchronize(); print('stream_read done')" > $O/racecheck_stream_read.log 2>&1
+for t in memcheck synccheck racecheck; do timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > $O/sanitize_$t.log 2>&1; tail -1 $O/sanitize_$t.log; done
 ls -la $O
