@@ -63,7 +63,10 @@ CONFIGS = {
                  slot_capacity=1 << 29,
                  # run-ahead generation: rollouts of the next 64 prompts (the
                  # look-ahead window) are inserted as spans of 512-2048 tokens, 8 per step
-                 runahead=dict(first=64, prompts=64, per=4, spans=8, lo=512, hi=2048)),
+                 runahead=dict(first=64, prompts=64, per=4, spans=8, lo=512, hi=2048),
+                 # measured: the fused tree step is slower here (16 sequences per prompt,
+                 # deeper hubs: 316-326 us vs 270 us for the separate kernels)
+                 fused_step=False),
 }
 
 KERNELS_PER_STEP = 9  # timed segments per group and step (an upper bound, for the profile buffer)
@@ -763,15 +766,27 @@ class ShardedRun:
                           self.seq_tok, self.seq_len, self.max_new, out=self.v, rows=self.rows_max)
         self.ex.commit()
 
-    def step(self, seed: int, ev=None):
+    fused_step = False  # (the fused tree step needs verify and insert on one cache)
+    snap = None
+
+    def draft_if_needed(self):
+        self.draft()
+
+    def snapshot_layout(self):
+        self.snap = (self.d.row_offsets.clone(), self.d.draft_depth.clone())
+
+    def step(self, seed: int, ev=None, rows_out=None):
         """draft (owner) -> draft return -> [stand-in] -> verify -> span
-        all-gather -> owner insert.  ev = 4 events (stand-in excluded)."""
+        all-gather -> owner insert.  ev = 4 events (stand-in excluded);
+        rows_out (1-element device tensor) <- this step's rows."""
         if ev:
             ev[0].record()
         self.draft()
         if ev:
             ev[1].record()
         self.standin()
+        if rows_out is not None:
+            rows_out.copy_(self.d.row_offsets[-1:])
         if ev:
             ev[2].record()
         self.verify_insert(seed)
@@ -900,9 +915,10 @@ def main():
                          "srt_verify_lmhead_insert_cursor (the LM-head GEMM fused with the "
                          "sampler, SURVEY f3a: the step then includes the LM head)")
     ap.add_argument("--path-rounds", type=int, default=3)
-    ap.add_argument("--fused-step", type=int, default=1,
+    ap.add_argument("--fused-step", type=int, default=-1,
                     help="1: srt_verify_insert_draft_cursor (commit + insert + hub refresh + the "
-                         "next draft in one persistent kernel; D <= 32, --verify full, 1 group)")
+                         "next draft in one persistent kernel; D <= 32, --verify full, 1 group); "
+                         "0: the separate kernels; -1: the configuration's measured choice")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: each step's draft segment and verify+insert segment replay as CUDA "
                          "graphs (no launch gaps); the per-kernel breakdown then comes from a "
@@ -980,7 +996,8 @@ def main():
         if args.verify == "lmhead":
             run.enable_lmhead(cfg.get("hidden", 1536), args.seed)
         G = run.G
-        if args.fused_step and args.verify == "full" and cfg["D"] <= 32 and G == 1:
+        fused = cfg.get("fused_step", True) if args.fused_step < 0 else bool(args.fused_step)
+        if fused and args.verify == "full" and cfg["D"] <= 32 and G == 1:
             for gr in run.groups:
                 gr.fused_step = True
     pipelined = G > 1

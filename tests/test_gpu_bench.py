@@ -172,3 +172,25 @@ def test_fused_tree_step_matches_separate_calls(D):
     np.testing.assert_array_equal(la, lb)
     assert da == db
     assert sum(int(r[1].sum()) for r in ra) > 0 and sum(int(r[8].sum()) for r in ra) > 96 * 8
+
+
+@pytest.mark.parametrize("extra", [[], ["--sharded"], ["--fused-step", "0"], ["--verify", "path"],
+                                   ["--graph", "0"]])
+def test_bench_cli_runs(extra):
+    """bench.py's control flow end to end on the tiny configuration (the
+    driver runs it; the single-rank, sharded, unfused, path-only and eager
+    variants): one parseable JSON line with the contract's keys."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "tiny",
+                        "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1",
+                        *extra], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "roofline", "e2e", "gpu_launches", "config"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] > 0
