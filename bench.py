@@ -768,6 +768,7 @@ class ShardedRun:
 
     fused_step = False  # (the fused tree step needs verify and insert on one cache)
     snap = None
+    ra = None  # (no run-ahead spans in the sharded configuration)
 
     def draft_if_needed(self):
         self.draft()

@@ -289,3 +289,66 @@ class _OracleView:
 
     def dump(self, _):
         return self.o.dump(self.p)
+
+
+def test_fullsize_b200x8_sharded_rank(orc):
+    """BJ:configs[4] per rank at full size through the hash-sharded path
+    bench.py times (bench.ShardedRun at N = 1: owner drafts over the mirror
+    tables, the draft-return all-to-all, verify, the span all-gather, the
+    owner's cursor insert; 4096 sequences of 256 prompts x 16): after 2 steps
+    the trees of sampled prompts, the next drafts of their sequences and their
+    verify / commit on the bench's own logits equal the oracle's."""
+    import torch
+    import bench
+
+    cfg = dict(bench.CONFIGS["b200x8"])
+    run = bench.ShardedRun(cfg, 0, 0, 1, "bf16", "rl-mix", gather=lambda t: t)
+    for k in range(2):
+        run.step(bench.step_seed(0, k))
+    torch.cuda.synchronize()
+    assert run.status()[0] == 0
+    wl = bench.Workload(cfg, 0, prompt_ids=range(0, cfg["prompts"]))  # block 0 = every prompt
+    rng = np.random.default_rng(23)
+    prompts = [int(p) for p in rng.choice(np.unique(wl.seq_prompt), size=2, replace=False)]
+    # the owner's mirror tables (at N = 1: mirror j = local sequence j)
+    seq_tok = run.m_tok.cpu().numpy()
+    seq_len = run.m_len.cpu().numpy()
+    assert np.array_equal(seq_len, run.seq_len.cpu().numpy())
+    trees = []
+    for p in prompts:
+        o, seqs = _history_tree(orc, wl, cfg, p, seq_tok, seq_len, run)
+        _dump_equal(run.cache, p, o)
+        trees.append((p, o, seqs))
+    # the step under test
+    run.draft()
+    run.standin()
+    seed = bench.step_seed(0, 2)
+    torch.cuda.synchronize()
+    d = run.d
+    g_draft = {k: getattr(d, k).cpu().numpy() for k in
+               ("match_len", "draft_len", "draft_tok", "draft_parent", "draft_depth", "draft_pos")}
+    row_off = d.row_offsets.cpu().numpy()
+    run.verify_insert(seed)
+    torch.cuda.synchronize()
+    sampled = run.v.sampled.cpu().numpy()
+    n_commit = run.v.n_commit.cpu().numpy()
+    drafted = 0
+    for p, o, seqs in trees:
+        od = o.draft(np.zeros(len(seqs), np.int32), seq_tok[seqs], seq_len[seqs], seq_len[seqs])
+        for k, v in g_draft.items():
+            assert np.array_equal(v[seqs], od[k].astype(v.dtype)), (p, k)
+        drafted += int(od["draft_len"].sum())
+        rows = np.concatenate([np.arange(row_off[s], row_off[s + 1]) for s in seqs])
+        bits = run.logits[torch.from_numpy(rows).to(run.logits.device)].view(torch.int16)
+        bits = bits.cpu().numpy().view(np.uint16)
+        o_tok = np.ascontiguousarray(seq_tok[seqs])
+        o_len = np.ascontiguousarray(seq_len[seqs])
+        ov = o.verify(bits, od["row_offsets"], od["draft_len"], od["draft_tok"], od["draft_parent"],
+                      od["draft_depth"], wl.seq_id[seqs], seed, o_tok, o_len, wl.max_new[seqs])
+        assert np.array_equal(sampled[rows], ov["sampled"]), (p, "sampled")
+        assert np.array_equal(n_commit[seqs], ov["n_commit"]), (p, "n_commit")
+        # the owner inserted the spans: its tree equals the oracle's after the commit
+        o.insert(np.zeros(len(seqs), np.int32), o_tok, seq_len[seqs], o_len)
+        _dump_equal(run.cache, p, o)
+    assert drafted > 0
+    assert run.status()[0] == 0
