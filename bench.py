@@ -433,7 +433,7 @@ class Group:
         c = self.cache
         lg = self.logits if logits is None else logits
         if (self.fused_step and self.lm is None and self.path_rounds is None
-                and self.cache.cfg.max_depth <= 32):
+                and self.cache.cfg.max_depth <= 128):
             # run-ahead spans target look-ahead prompts (no active sequence's
             # tree); inserts commute (O14), so they go first and the next draft,
             # inside the fused call, sees them as it would after the unfused step
@@ -918,7 +918,7 @@ def main():
     ap.add_argument("--path-rounds", type=int, default=3)
     ap.add_argument("--fused-step", type=int, default=-1,
                     help="1: srt_verify_insert_draft_cursor (commit + insert + hub refresh + the "
-                         "next draft in one persistent kernel; D <= 32, --verify full, 1 group); "
+                         "next draft in one persistent kernel; D <= 128, --verify full, 1 group); "
                          "0: the separate kernels; -1: the configuration's measured choice")
     ap.add_argument("--graph", type=int, default=1,
                     help="1: each step's draft segment and verify+insert segment replay as CUDA "
@@ -998,7 +998,7 @@ def main():
             run.enable_lmhead(cfg.get("hidden", 1536), args.seed)
         G = run.G
         fused = cfg.get("fused_step", True) if args.fused_step < 0 else bool(args.fused_step)
-        if fused and args.verify == "full" and cfg["D"] <= 32 and G == 1:
+        if fused and args.verify == "full" and cfg["D"] <= 128 and G == 1:
             for gr in run.groups:
                 gr.fused_step = True
     pipelined = G > 1

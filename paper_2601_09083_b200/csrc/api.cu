@@ -580,7 +580,8 @@ srt_status srt_verify_insert_draft_cursor(
       !next_draft_len || !next_draft_tok || !next_draft_parent || !next_draft_depth ||
       !next_draft_pos || !next_draft_mask || !next_row_offsets)
     return SRT_ERR_INVALID_ARG;
-  if (c->cfg.max_depth > 32) return SRT_ERR_INVALID_ARG;  // one warp per sequence
+  if (c->cfg.max_depth > SRT_CURSOR_MAX_DEPTH) return SRT_ERR_INVALID_ARG;
+  if (insert_cursor_smem(c->cfg.max_depth) > 200 * 1024) return SRT_ERR_INVALID_ARG;
   VerifyArgs a{n,       logits,     (int)c->cfg.logits_dtype, row_offsets, draft_len, draft_tok,
                draft_parent, draft_depth, seq_id, seed,    temperature, eos_id,    max_new,
                seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,

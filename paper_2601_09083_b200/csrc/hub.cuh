@@ -157,7 +157,7 @@ __device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int l
 // old K-th entry's, which only grew).  Exact only when the touches account
 // for the whole csum change since the build; otherwise (no previous list, a
 // NONE touch = a hub a draft met without a list, lost touches) the full
-// scan of refresh_hub_warp.  sid: >= 96 words of this warp's shared memory.
+// scan of refresh_hub_warp.  sid: >= 128 words of this warp's shared memory.
 __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const uint32_t* kids,
                                  uint32_t m, uint32_t kstride, int lane, uint32_t* sid) {
   if (u >= c.H) return;
@@ -168,8 +168,7 @@ __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const
   const bool same = c.hub_node[slot] == u;
   if (same && c.hub_nch[slot] == nch && c.hub_csum[slot] == r.w) return;  // still valid
   const int K = min(HUB_K, c.Bmax);
-  bool incr = same && K <= 32 && m <= 64 && c.hub_len[slot] == (uint32_t)K &&
-              r.w - c.hub_csum[slot] == m;
+  bool incr = same && m <= 64 && c.hub_len[slot] == (uint32_t)K && r.w - c.hub_csum[slot] == m;
   const uint32_t k0 = lane < (int)m ? kids[(size_t)lane * kstride] : 0u;
   const uint32_t k1 = lane + 32 < (int)m ? kids[(size_t)(lane + 32) * kstride] : 0u;
   incr = incr && !__any_sync(0xffffffffu, k0 == NONE || k1 == NONE);
@@ -179,8 +178,9 @@ __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const
     return;
   }
   const size_t e = (size_t)slot * HUB_K;
-  const int ncand = K + (int)m;  // <= 96
+  const int ncand = K + (int)m;  // <= 128
   if (lane < K) sid[lane] = c.hub_child[e + lane];
+  if (lane + 32 < K) sid[lane + 32] = c.hub_child[e + lane + 32];
   if (lane < (int)m) sid[K + lane] = k0;
   if (lane + 32 < (int)m) sid[K + 32 + lane] = k1;
   __syncwarp();
@@ -198,6 +198,11 @@ __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const
     c.hub_child[e + lane] = L.v0;
     c.hub_tok[e + lane] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k0);
     c.hub_cnt[e + lane] = (uint32_t)(L.k0 >> 32);
+  }
+  if (lane + 32 < L.size) {
+    c.hub_child[e + lane + 32] = L.v1;
+    c.hub_tok[e + lane + 32] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k1);
+    c.hub_cnt[e + lane + 32] = (uint32_t)(L.k1 >> 32);
   }
   if (lane == 0) {
     c.hub_len[slot] = (uint32_t)L.size;

@@ -207,26 +207,49 @@ __device__ long long refresh_tasks(const DevCache& c, int32_t p, int lane,
   return clock64() - t0;
 }
 
-__global__ void __launch_bounds__(STEP_WARPS * 32)
+// NG = 1 (D <= 32): 4 warps per CTA, one warp per sequence in both phases.
+// NG > 1 (D <= 32 NG): NG warps per CTA; phase 1 inserts one sequence per CTA
+// (one warp per depth group, insert.cuh's multi-warp cursor insert), phase
+// 2 drafts one sequence per warp as before.
+template <int NG>
+__global__ void __launch_bounds__((NG == 1 ? STEP_WARPS : NG) * 32)
 k_tree_step(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result,
             const int32_t* __restrict__ prompt_id, const int32_t* __restrict__ floor_,
             uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats,
             StepDraftArgs d) {
+  constexpr int WPC = NG == 1 ? STEP_WARPS : NG;  // warps per CTA
   extern __shared__ __align__(16) unsigned char step_smem[];
+  __shared__ uint32_t sh_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const size_t cw = cursor_warp_bytes(c.D);
   const size_t per_warp = (cw + 2 * 65 * 4 + 15) & ~size_t(15);
   unsigned char* mine = step_smem + (size_t)w * (per_warp > 64 * 8 + 64 * sizeof(Ent)
                                                      ? per_warp
                                                      : 64 * 8 + 64 * sizeof(Ent));
-  const int32_t gw = blockIdx.x * STEP_WARPS + w;
-  const int32_t W = gridDim.x * STEP_WARPS;
+  const int32_t gw = blockIdx.x * WPC + w;
+  const int32_t W = gridDim.x * WPC;
   const int32_t n = a.n;
   unsigned long long* const prof = g_step_prof;
   unsigned long long pf[8] = {prof ? gtime() : 0ull, 0, 0, 0, 0, 0, 0, 0};
 
   // ---- phase 1: commit + insert; the last of a prompt rebuilds its hub lists
-  {
+  // (the warp that completes a prompt's count groups its touches and
+  // publishes them as refresh tasks; it and the prompt's waiting draft warps
+  // share the tasks)
+  auto publish_tasks = [&](int32_t p, uint32_t* pdl) {
+    __threadfence();  // every sibling's updates (they fenced before counting)
+    const uint32_t n_t = min(*(volatile uint32_t*)pdl, PDIRTY_CAP);
+    const uint32_t nd = group_touches(c, p, pdl, n_t,
+                                      reinterpret_cast<unsigned long long*>(mine), lane);
+    if (lane == 0) {
+      c.st_pnd[p] = nd;
+      if (!nd) pdl[0] = 0;
+      __threadfence();
+      atomicExch(&c.st_pready[p], nd ? 1u : 2u);
+    }
+    __syncwarp();
+  };
+  if (NG == 1) {
     CursorSmem S = carve_cursor_smem(mine, 0, c.D);
     int32_t* ctok = reinterpret_cast<int32_t*>(mine + cw);
     int32_t* acc = ctok + 65;
@@ -250,21 +273,46 @@ k_tree_step(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ res
         last = atomicAdd(&c.st_pdone[p], 1u) + 1 == c.st_pcount[p];
       }
       if (__shfl_sync(0xffffffffu, last, 0)) {
-        // publish the prompt's dirty hubs as refresh tasks; this warp and
-        // the prompt's draft warps (idle until it is ready) share them
-        __threadfence();  // every sibling's updates (they fenced before counting)
-        const uint32_t n_t = min(*(volatile uint32_t*)pdl, PDIRTY_CAP);
-        const uint32_t nd = group_touches(c, p, pdl, n_t,
-                                          reinterpret_cast<unsigned long long*>(mine), lane);
-        if (lane == 0) {
-          c.st_pnd[p] = nd;
-          if (!nd) pdl[0] = 0;
-          __threadfence();
-          atomicExch(&c.st_pready[p], nd ? 1u : 2u);
-        }
-        __syncwarp();
+        publish_tasks(p, pdl);
         pf[4] += refresh_tasks(c, p, lane, pf[5], reinterpret_cast<uint32_t*>(mine));
       }
+    }
+  } else {
+    // one sequence per CTA: warp 0 commits it, every warp inserts its depth
+    // group (S.A shared: warp 0's slice), warp 0 counts it toward the prompt
+    CursorSmem S = carve_cursor_smem(step_smem, 0, c.D);  // (stride set below)
+    for (int32_t s = blockIdx.x; s < n; s += gridDim.x) {
+      const int32_t t = a.seq_len[s];
+      __syncthreads();
+      if (w == 0) {
+        int32_t* ctok = reinterpret_cast<int32_t*>(mine + cw);
+        accept_seq(c, a, result, s, ctok, ctok + 65, lane);
+      }
+      __syncthreads();
+      const int32_t t_end = a.seq_len[s];
+      const int32_t p = prompt_id[s];
+      if (p < 0 || p >= c.P) {
+        if (threadIdx.x == 0) set_error(c, SRT_DEV_BAD_PROMPT);
+        continue;
+      }
+      uint32_t* const pdl = c.pdirty + (size_t)p * PDIRTY_WORDS;
+      S = carve_cursor_smem(mine, 0, c.D);
+      S.A = carve_cursor_smem(step_smem, 0, c.D).A;
+      S.pdl = pdl;
+      cursor_insert_seq<NG, true>(c, S, s, p, t, t_end, a.seq_tok, a.stride, floor_, INT_MAX,
+                                  cursor, tag, stats);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        sh_last = atomicAdd(&c.st_pdone[p], 1u) + 1 == c.st_pcount[p];
+      }
+      __syncthreads();
+      if (sh_last) {
+        if (w == 0) publish_tasks(p, pdl);
+        __syncthreads();
+        pf[4] += refresh_tasks(c, p, lane, pf[5], reinterpret_cast<uint32_t*>(mine));
+      }
+      __syncthreads();
     }
   }
   __syncwarp();
@@ -310,6 +358,7 @@ k_tree_step(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ res
     pf[3] = gtime();
     for (int i = 0; i < 8; ++i) prof[(size_t)gw * 8 + i] = pf[i];
   }
+  (void)sh_last;
 }
 
 }  // namespace
@@ -327,27 +376,31 @@ cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
                              int32_t* draft_len, int32_t* draft_tok, int32_t* draft_parent,
                              int32_t* draft_depth, int32_t* draft_pos, uint64_t* draft_mask,
                              int64_t* row_offsets, cudaStream_t stream) {
-  if (c.D > 32) return cudaErrorInvalidValue;  // one warp per sequence
+  const int ng = (c.D + 31) >> 5;
+  if (ng > 4) return cudaErrorInvalidValue;  // D <= SRT_CURSOR_MAX_DEPTH
   if (a.n <= 0) return cudaSuccess;
   k_step_prep<<<1, 1024, 0, stream>>>(c, a.n, prompt_id);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t)STEP_WARPS * tree_step_smem_per_warp(c.D);
-  auto kern = k_tree_step;
+  const int wpc = ng == 1 ? STEP_WARPS : ng;  // warps per CTA
+  const size_t smem = (size_t)wpc * tree_step_smem_per_warp(c.D);
+  auto kern = ng == 1 ? k_tree_step<1> : ng == 2 ? k_tree_step<2> : ng == 3 ? k_tree_step<3>
+                                                                            : k_tree_step<4>;
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   // every CTA resident: a draft waits on other warps' inserts
-  static int per_sm = 0;
-  static size_t per_sm_smem = 0;
-  if (!per_sm || per_sm_smem != smem) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, STEP_WARPS * 32, smem);
-    if (e != cudaSuccess || per_sm <= 0) return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;
-    per_sm_smem = smem;
+  static int per_sm[5] = {0, 0, 0, 0, 0};
+  static size_t per_sm_smem[5] = {0, 0, 0, 0, 0};
+  if (!per_sm[ng] || per_sm_smem[ng] != smem) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ng], kern, wpc * 32, smem);
+    if (e != cudaSuccess || per_sm[ng] <= 0)
+      return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;
+    per_sm_smem[ng] = smem;
   }
-  const int need = (a.n + STEP_WARPS - 1) / STEP_WARPS;
-  const int grid = need < per_sm * num_sms() ? need : per_sm * num_sms();
+  const int need = ng == 1 ? (a.n + STEP_WARPS - 1) / STEP_WARPS : a.n;
+  const int grid = need < per_sm[ng] * num_sms() ? need : per_sm[ng] * num_sms();
   StepDraftArgs d{pos_base, match_len, draft_len, draft_tok, draft_parent, draft_depth,
                   draft_pos, draft_mask, row_offsets};
   static int dbg = -1;
@@ -360,11 +413,10 @@ cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
       cudaMemcpyToSymbol(g_step_prof, &pbuf, sizeof(pbuf));
     }
   }
-  kern<<<grid, STEP_WARPS * 32, smem, stream>>>(c, a, result, prompt_id, floor_, cursor, tag,
-                                                 stats, d);
+  kern<<<grid, wpc * 32, smem, stream>>>(c, a, result, prompt_id, floor_, cursor, tag, stats, d);
   e = cudaGetLastError();
-  if (dbg && e == cudaSuccess && grid * STEP_WARPS <= 65536) {
-    const int nw = grid * STEP_WARPS;
+  if (dbg && e == cudaSuccess && grid * wpc <= 65536) {
+    const int nw = grid * wpc;
     std::vector<unsigned long long> h((size_t)nw * 8);
     cudaStreamSynchronize(stream);
     cudaMemcpy(h.data(), pbuf, h.size() * 8, cudaMemcpyDeviceToHost);

@@ -131,7 +131,7 @@ def test_graph_replay_matches_eager():
     assert out[0][2] == out[1][2]
 
 
-@pytest.mark.parametrize("D", [16, 32])
+@pytest.mark.parametrize("D", [16, 32, 64, 128])
 def test_fused_tree_step_matches_separate_calls(D):
     """srt_verify_insert_draft_cursor (commit + cursor insert + per-prompt hub
     refresh + the next draft in one persistent kernel) leaves exactly what
@@ -142,7 +142,7 @@ def test_fused_tree_step_matches_separate_calls(D):
     import bench
     cfg = dict(bench.CONFIGS["grpo"])
     cfg.update(prompts=12, active=96, V=5000, cap=1024, act_cap=1024, median=300,
-               node_capacity=1 << 21, D=D, L=8)
+               node_capacity={16: 1 << 21, 32: 1 << 21, 64: 1 << 23, 128: 1 << 24}[D], D=D, L=8)
     out = []
     for fused_step in (False, True):
         wl = bench.Workload(cfg, 3)

@@ -66,9 +66,9 @@ def test_fullsize_sampled_parity(orc, config, steps, n_prompts, n_rows):
     wl = bench.Workload(cfg, 0)
     run = bench.GpuRun(wl, "bf16", "rl-mix", 0)
     gr = run.groups[0]
-    # the launch configuration bench.py times: D <= 32 runs the fused tree step
+    # the launch configuration: every D <= 128 here runs the fused tree step
     # (srt_verify_insert_draft_cursor: commit + insert + refresh + next draft)
-    gr.fused_step = cfg["D"] <= 32
+    gr.fused_step = cfg["D"] <= 128
     for k in range(steps):
         run.step(bench.step_seed(0, k))
     torch.cuda.synchronize()
