@@ -1025,14 +1025,16 @@ def main():
     com_log = torch.zeros(K, dtype=torch.int64, device=run.dev)
     logs = [torch.zeros(3, K, dtype=torch.int64, device=run.dev) for _ in range(G)]
     use_graph = bool(args.graph) and not pipelined and G == 1
+    step_prof = []
     if use_graph:
         # capture one step's two segments (the stand-in stays eager between
         # them); the sharded path's segments include its NCCL collectives
         gr0 = run.groups[0]
         try:
             g_draft, g_vi = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_draft):
-                gr0.draft()
+            if not gr0.fused_step:  # (fused: the previous step's call drafts this one)
+                with torch.cuda.graph(g_draft):
+                    gr0.draft()
             with torch.cuda.graph(g_vi):
                 gr0.verify_insert(seed)
             for _ in range(2):  # graph warm-up steps
@@ -1108,16 +1110,34 @@ def main():
         my_ms = float(sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in evs))
     KP = K
     prof_rows = None
-    if use_graph:  # per-kernel breakdown: a profiled eager pass after the timed region
+    if use_graph:
+        # per-kernel breakdown: the same two segments captured again with the
+        # library's event pairs inside (every replay re-records them; read after
+        # each step with srt_profile_peek), KP more graph-replayed steps with
+        # their rows logged -- the timed graphs carry no profiling nodes
         KP = min(K, 20)
-        for gr in run.groups:
-            gr.cache.profile_enable(KP * KERNELS_PER_STEP)
+        gr0.cache.profile_enable(4 * KERNELS_PER_STEP)
+        gp_draft, gp_vi = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        if not gr0.fused_step:
+            with torch.cuda.graph(gp_draft):
+                gr0.draft()
+        with torch.cuda.graph(gp_vi):
+            gr0.verify_insert(seed)
         prof_rows = torch.zeros(KP, dtype=torch.int64, device=run.dev)
         for k in range(KP):
-            run.step(seed, rows_out=prof_rows[k:k + 1])
+            if not gr0.fused_step:
+                gp_draft.replay()
+            gr0.standin()
+            prof_rows[k] = gr0.d.row_offsets[-1]
+            gp_vi.replay()
+            step_prof.append(gr0.cache.profile_peek())
         torch.cuda.synchronize()
+        prof = [x for sp in step_prof for x in sp]
         prof_rows = prof_rows.cpu().numpy()
-    prof = [x for gr in run.groups for x in gr.cache.profile_read()]
+        del gp_draft, gp_vi
+        gr0.cache.profile_enable(0)
+    else:
+        prof = [x for gr in run.groups for x in gr.cache.profile_read()]
     bits, st = run.status()
     if bits:
         raise RuntimeError(f"device error bits {bits} in the timed region")
@@ -1179,8 +1199,9 @@ def main():
                              f"pipelined on {G} streams); forward stand-in and bookkeeping "
                              f"INCLUDED" if pipelined else
                              ("draft + verify + insert device time (CUDA events around the two "
-                              "CUDA-graph replays per step; per-kernel breakdown from a profiled "
-                              "eager pass of the same steps); forward stand-in excluded"
+                              "CUDA-graph replays per step; per-kernel breakdown from the same "
+                              "segments re-captured with the library's event pairs and replayed "
+                              "after the timed region, rows logged); forward stand-in excluded"
                               if use_graph else
                               "draft + verify + insert device time (CUDA events); forward "
                               "stand-in excluded")),

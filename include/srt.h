@@ -582,6 +582,11 @@ typedef struct {
 SRT_API srt_status srt_profile_enable(srt_cache* cache, int64_t capacity);
 SRT_API srt_status srt_profile_read(srt_cache* cache, srt_profile_record* host_buf, int64_t cap,
                                     int64_t* n_records, void* stream);
+/* As srt_profile_read but keeps the records: for launches captured in a CUDA
+ * graph, each replay re-records the same event pairs, so peeking after a
+ * replay (BLOCKING) returns that replay's per-kernel times. */
+SRT_API srt_status srt_profile_peek(srt_cache* cache, srt_profile_record* host_buf, int64_t cap,
+                                    int64_t* n_records, void* stream);
 
 /*
  * srt_debug_draft_profile — development support: when dev_buf (DEVICE,

@@ -28,7 +28,7 @@ EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache
            "srt_insert", "srt_insert_cursor", "srt_draft", "srt_draft_cursor", "srt_verify", "srt_verify_path", "srt_verify_insert_cursor", "srt_verify_insert_draft_cursor", "srt_verify_lmhead", "srt_verify_lmhead_insert_cursor", "srt_cache_dump",
            "srt_cache_prune", "srt_cache_evict", "srt_cache_load", "srt_cache_status",
            "srt_cache_clear_errors", "srt_noise_table", "srt_log_det_range", "srt_row_noise", "srt_stream_read", "srt_sample_rows_reference",
-           "srt_profile_enable", "srt_profile_read", "srt_debug_draft_profile", "srt_debug_insert_profile",
+           "srt_profile_enable", "srt_profile_read", "srt_profile_peek", "srt_debug_draft_profile", "srt_debug_insert_profile",
            "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
                 5: "accept", 6: "insert_cursor",
@@ -124,6 +124,7 @@ def load() -> ctypes.CDLL:
     L.srt_debug_insert_profile.argtypes = [vp]
     L.srt_profile_read.argtypes = [vp, ctypes.POINTER(SrtProfileRecord), i64,
                                    ctypes.POINTER(ctypes.c_int64), vp]
+    L.srt_profile_peek.argtypes = L.srt_profile_read.argtypes
     for name in EXPORTS:
         if name not in ("srt_abi_version", "srt_error_string"):
             getattr(L, name).restype = ctypes.c_int

@@ -89,9 +89,14 @@ template <class F>
 cudaError_t timed(srt_cache* c, int32_t kernel, cudaStream_t stream, F fn) {
   if (c->prof_n >= c->prof_cap) return fn();
   const int64_t i = c->prof_n++;
-  cudaEventRecord(c->ev[2 * i], stream);
+  // under stream capture the records become event nodes of the graph
+  // (External), re-recorded by every replay -- srt_profile_peek
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cs);
+  const unsigned fl = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  cudaEventRecordWithFlags(c->ev[2 * i], stream, fl);
   cudaError_t e = fn();
-  cudaEventRecord(c->ev[2 * i + 1], stream);
+  cudaEventRecordWithFlags(c->ev[2 * i + 1], stream, fl);
   c->kid[i] = kernel;
   return e;
 }
@@ -881,6 +886,20 @@ srt_status srt_profile_read(srt_cache* c, srt_profile_record* host_buf, int64_t 
   }
   *n_records = n;
   c->prof_n = 0;
+  return SRT_OK;
+}
+
+srt_status srt_profile_peek(srt_cache* c, srt_profile_record* host_buf, int64_t cap,
+                            int64_t* n_records, void* stream) {
+  if (!c || !n_records || cap < 0) return SRT_ERR_INVALID_ARG;
+  SRT_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "profile sync");
+  const int64_t n = c->prof_n;
+  for (int64_t i = 0; i < n && i < cap && host_buf; ++i) {
+    float ms = 0.f;
+    SRT_CUDA(cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]), "cudaEventElapsedTime");
+    host_buf[i] = srt_profile_record{c->kid[i], ms};
+  }
+  *n_records = n;
   return SRT_OK;
 }
 

@@ -339,6 +339,17 @@ class SrtCache:
         return [(_lib.KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms))
                 for i in range(min(n.value, cap))]
 
+    def profile_peek(self):
+        """profile_read without clearing (blocking): after a CUDA-graph replay,
+        the replay's per-kernel times of the captured launches."""
+        n = ctypes.c_int64(0)
+        cap = 256
+        buf = (_lib.SrtProfileRecord * cap)()
+        check(self.L.srt_profile_peek(self._h, buf, cap, ctypes.byref(n), _stream()),
+              "srt_profile_peek")
+        return [(_lib.KERNEL_NAMES.get(buf[i].kernel, str(buf[i].kernel)), float(buf[i].ms))
+                for i in range(min(n.value, cap))]
+
     def clear_errors(self):
         check(self.L.srt_cache_clear_errors(self._h, _stream()), "srt_cache_clear_errors")
 

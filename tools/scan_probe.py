@@ -29,10 +29,17 @@ def make_rows(R, V, profile, dtype, gen):
         gap = torch.full((R,), 18.0, device="cuda")
     elif profile == "gap15":
         gap = torch.full((R,), 15.0, device="cuda")
-    else:  # rl-mix
+    else:  # rl-mix (rl-mix-d: with the bench stand-in's 3 distractors below the head)
         u = torch.rand(R, device="cuda", generator=gen)
         hi = torch.rand(R, device="cuda", generator=gen) < 0.7
         gap = torch.where(hi, 18 + 6 * u, 12 + 6 * u)
+        if profile == "rl-mix-d":
+            ar = torch.arange(R, device="cuda")
+            for k in range(3):
+                off = torch.where(hi, 5 + 4 * torch.rand(R, device="cuda", generator=gen),
+                                  0.5 + 3.5 * torch.rand(R, device="cuda", generator=gen))
+                dk = torch.randint(0, V, (R,), device="cuda", generator=gen)
+                x[ar, dk] = (gap - off).to(dtype)
     x[torch.arange(R, device="cuda"), heads] = gap.to(dtype)
     return x
 
