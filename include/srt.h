@@ -403,9 +403,12 @@ SRT_API srt_status srt_verify_lmhead_insert_cursor(
  * sequence s's new draft is written only after its prompt's commits, and
  * row_offsets[0 .. n] only after every commit.  Results are identical to
  * srt_verify_insert_cursor then srt_draft_cursor(prompt_id, seq_tok,
- * seq_len, pos_base, cursor).  Needs cfg.max_depth <= 32 (one warp per
- * sequence; SRT_ERR_INVALID_ARG otherwise, before anything is enqueued).
- * Device-side errors as both calls.
+ * seq_len, pos_base, cursor).  cfg.max_depth <= SRT_CURSOR_MAX_DEPTH (one
+ * warp per sequence's insert for D <= 32, one CTA of ceil(D/32) warps above;
+ * SRT_ERR_INVALID_ARG otherwise, before anything is enqueued).  The kernel
+ * keeps every CTA resident (cross-warp waits): do not run another kernel
+ * that could hold SMs indefinitely concurrently.  Device-side errors as both
+ * calls.
  */
 SRT_API srt_status srt_verify_insert_draft_cursor(
     srt_cache* cache, int32_t n, const void* logits, const int64_t* row_offsets,
