@@ -51,9 +51,13 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--profiles", default="peaked,rl-mix,gap15,flat")
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--prealloc-gb", type=float, default=0.0,
+                    help="allocate this much device memory first (placement experiments)")
+    ap.add_argument("--padrows", type=int, default=0, help="extra rows after the scanned ones")
     a = ap.parse_args()
     dt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
     R, V = a.rows, a.V
+    hold = torch.empty(int(a.prealloc_gb * 2**30), dtype=torch.uint8, device="cuda") if a.prealloc_gb else None
     cache = srt.SrtCache(srt.config(V, 1, 4, 2, 4, node_capacity=1024, logits_dtype=dt))
     n = R
     d = srt.DraftOut.empty(n, 4, "cuda")
