@@ -673,6 +673,10 @@ cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
     if (e != cudaSuccess || per_sm <= 0) per_sm = 1;
     blocks = per_sm * num_sms();
+    if (const char* g = getenv("SRT_SCAN_GRID")) {  // development knob: fewer CTAs
+      const int x = atoi(g);
+      if (x > 0 && x < blocks) blocks = x;
+    }
     if (p.debug & 8)
       fprintf(stderr, "[srt scan] rows: NSW=%d NT=%d NST=%d NS=%d CHUNK=%u NG=%d hint=%u spin=%u smem=%zu -> %d CTAs\n",
               NSW, NT, NST, NS, CHUNK, NG, p.l2_hint, p.spin, smem, blocks);

@@ -211,13 +211,13 @@ __device__ long long refresh_tasks(const DevCache& c, int32_t p, int lane,
 // NG > 1 (D <= 32 NG): NG warps per CTA; phase 1 inserts one sequence per CTA
 // (one warp per depth group, insert.cuh's multi-warp cursor insert), phase
 // 2 drafts one sequence per warp as before.
-template <int NG>
-__global__ void __launch_bounds__((NG == 1 ? STEP_WARPS : NG) * 32)
+template <int NG, int WPC_ = (NG == 1 ? STEP_WARPS : NG)>
+__global__ void __launch_bounds__(WPC_ * 32)
 k_tree_step(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result,
             const int32_t* __restrict__ prompt_id, const int32_t* __restrict__ floor_,
             uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats,
             StepDraftArgs d) {
-  constexpr int WPC = NG == 1 ? STEP_WARPS : NG;  // warps per CTA
+  constexpr int WPC = WPC_;  // warps per CTA
   extern __shared__ __align__(16) unsigned char step_smem[];
   __shared__ uint32_t sh_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -382,10 +382,19 @@ cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
   k_step_prep<<<1, 1024, 0, stream>>>(c, a.n, prompt_id);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int wpc = ng == 1 ? STEP_WARPS : ng;  // warps per CTA
+  // SRT_TREE_GRID=<CTAs> (development knob): D <= 32 only, 12 warps per CTA
+  // (one CTA fills an SM's registers), at most that many CTAs
+  static int tree_grid = -1;
+  if (tree_grid < 0) {
+    const char* ev = getenv("SRT_TREE_GRID");
+    tree_grid = ev ? atoi(ev) : 0;
+  }
+  const bool wide = ng == 1 && tree_grid > 0;
+  const int wpc = wide ? 12 : ng == 1 ? STEP_WARPS : ng;  // warps per CTA
   const size_t smem = (size_t)wpc * tree_step_smem_per_warp(c.D);
-  auto kern = ng == 1 ? k_tree_step<1> : ng == 2 ? k_tree_step<2> : ng == 3 ? k_tree_step<3>
-                                                                            : k_tree_step<4>;
+  auto kern = wide ? k_tree_step<1, 12> : ng == 1 ? k_tree_step<1> : ng == 2 ? k_tree_step<2>
+            : ng == 3 ? k_tree_step<3> : k_tree_step<4>;
+  const int kslot = wide ? 0 : ng;
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -393,14 +402,15 @@ cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
   // every CTA resident: a draft waits on other warps' inserts
   static int per_sm[5] = {0, 0, 0, 0, 0};
   static size_t per_sm_smem[5] = {0, 0, 0, 0, 0};
-  if (!per_sm[ng] || per_sm_smem[ng] != smem) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ng], kern, wpc * 32, smem);
-    if (e != cudaSuccess || per_sm[ng] <= 0)
+  if (!per_sm[kslot] || per_sm_smem[kslot] != smem) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[kslot], kern, wpc * 32, smem);
+    if (e != cudaSuccess || per_sm[kslot] <= 0)
       return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;
-    per_sm_smem[ng] = smem;
+    per_sm_smem[kslot] = smem;
   }
-  const int need = ng == 1 ? (a.n + STEP_WARPS - 1) / STEP_WARPS : a.n;
-  const int grid = need < per_sm[ng] * num_sms() ? need : per_sm[ng] * num_sms();
+  const int need = ng == 1 ? (a.n + wpc - 1) / wpc : a.n;
+  int grid = need < per_sm[kslot] * num_sms() ? need : per_sm[kslot] * num_sms();
+  if (wide && grid > tree_grid) grid = tree_grid;
   StepDraftArgs d{pos_base, match_len, draft_len, draft_tok, draft_parent, draft_depth,
                   draft_pos, draft_mask, row_offsets};
   static int dbg = -1;
