@@ -924,6 +924,9 @@ def main():
                     help="1: each step's draft segment and verify+insert segment replay as CUDA "
                          "graphs (no launch gaps); the per-kernel breakdown then comes from a "
                          "separate profiled eager pass")
+    ap.add_argument("--step-overlap", type=int, default=-1,
+                    help="SMs the fused tree step runs on BESIDE the scan (srt_cache_set_step_overlap; "
+                         "0 = after the scan on every SM, -1 = the library's default)")
     ap.add_argument("--groups", type=int, default=1,
                     help="prompt groups pipelined on separate streams (1 = sequential; >1 measured slower: the latency-bound tree kernels stall behind the scan's HBM traffic)")
     args = ap.parse_args()
@@ -1001,6 +1004,8 @@ def main():
         if fused and args.verify == "full" and cfg["D"] <= 128 and G == 1:
             for gr in run.groups:
                 gr.fused_step = True
+                if args.step_overlap >= 0:
+                    gr.cache.set_step_overlap(args.step_overlap)
     pipelined = G > 1
     K, W = args.steps, args.warmup
     seed = step_seed(args.seed, 0)

@@ -422,6 +422,23 @@ SRT_API srt_status srt_verify_insert_draft_cursor(
     int32_t* next_draft_depth, int32_t* next_draft_pos, uint64_t* next_draft_mask,
     int64_t* next_row_offsets, void* stream);
 
+/*
+ * srt_cache_set_step_overlap — where srt_verify_insert_draft_cursor runs its
+ * fused tree step.  sms > 0: on `sms` SMs BESIDE the scan,
+ * which then runs on the other SMs: the step kernel is a programmatic
+ * dependent launch on the caller's stream (it starts while the scan runs)
+ * and commits and inserts each sequence as soon as the scan has finished
+ * that sequence's rows, so the latency-bound tree work hides under the
+ * HBM-bound scan.  If the two kernels do not overlap (a tool or another
+ * context holding the SMs) the step kernel simply runs after the scan: the
+ * scan never waits on it.  0: after the scan, on every SM.  -1: the library
+ * default (SRT_STEP_OVERLAP in the environment overrides it).  Applies to
+ * cfg.max_depth <= 32 and 16-byte aligned logits rows; other calls run the
+ * step after the scan.  Results are identical in every mode.
+ * SRT_ERR_INVALID_ARG unless -1 <= sms < the SM count.
+ */
+SRT_API srt_status srt_cache_set_step_overlap(srt_cache* cache, int32_t sms);
+
 /* records[s] <- the draft of sequence s < n (srt_draft's outputs). */
 SRT_API srt_status srt_pack_drafts(int32_t n, int32_t Bmax, const int32_t* match_len,
                            const int32_t* draft_len, const int32_t* draft_tok,

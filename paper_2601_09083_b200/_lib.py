@@ -29,7 +29,8 @@ EXPORTS = ["srt_abi_version", "srt_error_string", "srt_cache_create", "srt_cache
            "srt_cache_prune", "srt_cache_evict", "srt_cache_load", "srt_cache_status",
            "srt_cache_clear_errors", "srt_noise_table", "srt_log_det_range", "srt_row_noise", "srt_stream_read", "srt_sample_rows_reference",
            "srt_profile_enable", "srt_profile_read", "srt_profile_peek", "srt_debug_draft_profile", "srt_debug_insert_profile",
-           "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans"]
+           "srt_pack_drafts", "srt_unpack_drafts", "srt_pack_spans", "srt_apply_spans",
+           "srt_cache_set_step_overlap"]
 KERNEL_NAMES = {0: "insert_plan", 1: "insert_walk", 2: "draft", 3: "row_offsets", 4: "scan",
                 5: "accept", 6: "insert_cursor",
                 7: "hub_refresh", 8: "accept_insert", 9: "lmhead",
@@ -120,6 +121,7 @@ def load() -> ctypes.CDLL:
     L.srt_stream_read.argtypes = [vp, i64, i32, i32, i32, vp, vp]
     L.srt_sample_rows_reference.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, f32, vp, vp]
     L.srt_profile_enable.argtypes = [vp, i64]
+    L.srt_cache_set_step_overlap.argtypes = [vp, i32]
     L.srt_debug_draft_profile.argtypes = [vp]
     L.srt_debug_insert_profile.argtypes = [vp]
     L.srt_profile_read.argtypes = [vp, ctypes.POINTER(SrtProfileRecord), i64,

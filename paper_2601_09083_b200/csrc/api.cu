@@ -14,6 +14,11 @@
 
 using namespace srt;
 
+// SMs the fused tree step takes beside the scan by default
+#ifndef SRT_STEP_OVERLAP_DEFAULT
+#define SRT_STEP_OVERLAP_DEFAULT 0
+#endif
+
 struct srt_cache {
   srt_config cfg;
   DevCache dev;
@@ -30,6 +35,10 @@ struct srt_cache {
   uint32_t* hubwork = nullptr;  // hub refresh work list [DIRTY_CAP + 1]
   int device;
   uint32_t tag;  // identifies this cache in insert cursors (never 0)
+  // the tree step beside the scan (srt_verify_insert_draft_cursor, overlap mode)
+  uint32_t* ov = nullptr;       // its state words (tree_step_ov_words)
+  size_t ov_cap = 0;
+  int32_t ov_sms = -1;          // srt_cache_set_step_overlap (-1: the default)
   // per-kernel timing (srt_profile_enable)
   std::vector<cudaEvent_t> ev;
   std::vector<int32_t> kid;
@@ -225,6 +234,7 @@ srt_status srt_cache_destroy(srt_cache* c, void* stream) {
   if (c->lm.cand_b) cudaFreeAsync(c->lm.cand_b, (cudaStream_t)stream);
   if (c->lm.cand_X) cudaFreeAsync(c->lm.cand_X, (cudaStream_t)stream);
   if (c->lm.cand_n) cudaFreeAsync(c->lm.cand_n, (cudaStream_t)stream);
+  if (c->ov) cudaFreeAsync(c->ov, (cudaStream_t)stream);
   delete c;
   return SRT_OK;
 }
@@ -361,6 +371,64 @@ srt_status verify_scan(srt_cache* c, const VerifyArgs& a, cudaStream_t stream) {
   SRT_CUDA(timed(c, SRT_K_SCAN, stream,
                  [&] { return launch_scan(c->dev, a, false, c->rowinfo, c->result, stream); }),
            "verify scan");
+  return SRT_OK;
+}
+
+// SMs the fused tree step runs on beside the scan (0: after it, on every SM).
+// SRT_STEP_OVERLAP=<SMs> sets it; 0 turns the overlap off.  D <= 32 and the
+// rows scan (16-byte aligned rows) only.
+int tree_step_overlap_sms(const srt_cache* c, const VerifyArgs& a) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("SRT_STEP_OVERLAP");
+    env = e ? atoi(e) : -1;
+  }
+  const int g = c->ov_sms >= 0 ? c->ov_sms : env >= 0 ? env : SRT_STEP_OVERLAP_DEFAULT;
+  if (g <= 0 || c->cfg.max_depth > 32 || !scan_cluster_size(c->cfg.vocab_size, a.dtype) ||
+      ((uintptr_t)a.logits % 16) != 0 || g >= num_sms())
+    return 0;
+  return g;
+}
+
+srt_status tree_step_overlapped(srt_cache* c, const VerifyArgs& a, int ov_sms,
+                                const int32_t* prompt_id, const int32_t* floor_, uint32_t* cursor,
+                                srt_insert_stats* stats_dev, const int32_t* pos_base,
+                                int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
+                                int32_t* draft_parent, int32_t* draft_depth, int32_t* draft_pos,
+                                uint64_t* draft_mask, int64_t* row_offsets, cudaStream_t stream) {
+  const srt_status bs = row_buffers(c, a, stream);
+  if (bs != SRT_OK) return bs;
+  const size_t words = tree_step_ov_words(a.n, c->cfg.max_prompts);
+  if (c->ov_cap < words) {
+    if (c->ov) SRT_CUDA(cudaFreeAsync(c->ov, stream), "cudaFreeAsync(ov)");
+    SRT_CUDA(cudaMallocAsync(&c->ov, words * 4, stream), "cudaMallocAsync(ov)");
+    c->ov_cap = words;
+  }
+  uint32_t* seq_done = tree_step_ov_seq_done(c->ov, a.n, c->cfg.max_prompts);
+  // prep -> rowinfo -> scan (all SMs but ov_sms; each CTA triggers its
+  // dependents as it starts) -> the step kernel, a programmatic dependent
+  // launch: it starts on the free SMs while the scan runs and waits per
+  // sequence on the scan's row counters (never on the scan's completion).
+  // If the launch is not overlapped it runs after the scan, with the same
+  // results: the scan never waits on it.
+  SRT_CUDA(launch_step_prep_ov(c->dev, a.n, prompt_id, a.row_offsets, c->ov, stream), "step prep");
+  SRT_CUDA(timed(c, SRT_K_SCAN, stream,
+                 [&] {
+                   cudaError_t e = launch_rowinfo(c->dev, a, c->rowinfo, c->result, stream);
+                   if (e != cudaSuccess) return e;
+                   return launch_scan_list(c->dev, a, c->rowinfo, nullptr,
+                                           tree_step_ov_total(c->ov, a.n, c->cfg.max_prompts),
+                                           c->result, stream, seq_done, num_sms() - ov_sms);
+                 }),
+           "verify scan beside the fused tree step");
+  SRT_CUDA(timed(c, SRT_K_TREE_STEP, stream,
+                 [&] {
+                   return launch_tree_step_ov(c->dev, a, c->result, prompt_id, floor_, cursor,
+                                              c->tag, stats_dev, pos_base, match_len, draft_len,
+                                              draft_tok, draft_parent, draft_depth, draft_pos,
+                                              draft_mask, row_offsets, c->ov, ov_sms, stream);
+                 }),
+           "fused tree step beside the scan");
   return SRT_OK;
 }
 
@@ -592,6 +660,12 @@ srt_status srt_verify_insert_draft_cursor(
                seq_tok, stride,     seq_len,  sampled,     accept_len,  n_commit,  commit_tok,
                accepted_nodes, finished};
   cudaStream_t stream = (cudaStream_t)stream_;
+  const int ov_sms = tree_step_overlap_sms(c, a);
+  if (ov_sms > 0)
+    return tree_step_overlapped(c, a, ov_sms, prompt_id, floor_, cursor, stats_dev, pos_base,
+                                next_match_len, next_draft_len, next_draft_tok, next_draft_parent,
+                                next_draft_depth, next_draft_pos, next_draft_mask,
+                                next_row_offsets, stream);
   const srt_status st = verify_scan(c, a, stream);
   if (st != SRT_OK) return st;
   SRT_CUDA(timed(c, SRT_K_TREE_STEP, stream,
@@ -603,6 +677,12 @@ srt_status srt_verify_insert_draft_cursor(
                                            stream);
                  }),
            "fused tree step");
+  return SRT_OK;
+}
+
+srt_status srt_cache_set_step_overlap(srt_cache* c, int32_t sms) {
+  if (!c || sms < -1 || sms >= num_sms()) return SRT_ERR_INVALID_ARG;
+  c->ov_sms = sms;
   return SRT_OK;
 }
 

@@ -191,6 +191,10 @@ struct ScanParams {
   uint32_t spin;               // 1 = stream warps poll the ring with test_wait
   uint32_t* sched;             // nullable: [0] next row to claim, [1] CTAs past the end (both 0
                                // between launches); null = static rows blockIdx.x + k gridDim.x
+  uint32_t* seq_done;          // nullable: per sequence, rows whose result is final (the last
+                               // worker of a row counts it, after its fence: the fused tree
+                               // step beside the scan waits on these)
+  int grid_cap;                // host side: at most this many CTAs (0 = one per SM)
 };
 
 // Warp roles: warp 0 = producer, warps 1..NSW = stream (NG groups taking
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   uint32_t* p1cnt = reinterpret_cast<uint32_t*>(row_of + NR);            // [NS]
   uint32_t* rowM = p1cnt + ((NS + 3) & ~3);                              // [NS] shared M keys
   float* tab = reinterpret_cast<float*>(rowM + ((NS + 3) & ~3));         // [1024]
+  uint32_t* wdone = reinterpret_cast<uint32_t*>(tab + NOISE_BUCKETS);    // [NS] workers done
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t total = *a.total;
@@ -258,6 +263,9 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
 
   for (int i = tid; i < NOISE_BUCKETS; i += blockDim.x) tab[i] = c.gbound[i];
+  // the fused tree step beside the scan is this launch's programmatic
+  // dependent: let it start now (it syncs on seq_done, not on completion)
+  if (a.seq_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&ring_full[s], 1);
@@ -270,6 +278,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
       p1key[s] = 0;
       p1cnt[s] = 0;
       rowM[s] = 0;
+      wdone[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -627,6 +636,14 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     __syncwarp();
     if (lane == 0) {
       if (wbest) atomicMax(&a.result[row], wbest);
+      if (a.seq_done) {  // the row's last worker: its result is final
+        __threadfence();
+        if (atomicAdd(&wdone[sb], 1u) == NTW - 1) {
+          wdone[sb] = 0;  // (before the arrival that frees the slot)
+          __threadfence();
+          atomicAdd(&a.seq_done[a.rowinfo[row].x], 1u);
+        }
+      }
       mbar_arrive(&sum_free[sb]);
     }
   }
@@ -663,7 +680,7 @@ cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
   const size_t smem = (size_t)NST * CHUNK + (size_t)NS * p.sum_bytes +
                       (2 * NST + 3 * NS) * 8 + 2 * NS * 8 + (NS + NST + 2) * 8 +
                       2 * ((NS + 3) & ~3) * 4 +
-                      NOISE_BUCKETS * 4;
+                      NOISE_BUCKETS * 4 + ((NS + 3) & ~3) * 4;
   auto kern = k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -681,7 +698,8 @@ cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
       fprintf(stderr, "[srt scan] rows: NSW=%d NT=%d NST=%d NS=%d CHUNK=%u NG=%d hint=%u spin=%u smem=%zu -> %d CTAs\n",
               NSW, NT, NST, NS, CHUNK, NG, p.l2_hint, p.spin, smem, blocks);
   }
-  k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG><<<blocks, THREADS, smem, stream>>>(c, p);
+  const int grid = p.grid_cap > 0 && p.grid_cap < blocks ? p.grid_cap : blocks;
+  k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG><<<grid, THREADS, smem, stream>>>(c, p);
   return cudaGetLastError();
 }
 
@@ -715,9 +733,12 @@ cudaError_t launch_scan_cluster(const DevCache& c, const VerifyArgs& a, int2* ro
 // be 0 for every listed row.
 cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2* rowinfo,
                              const int32_t* row_list, const int64_t* count,
-                             unsigned long long* result, cudaStream_t stream) {
+                             unsigned long long* result, cudaStream_t stream,
+                             uint32_t* seq_done, int grid_cap) {
   if (!scan_cluster_size(c.V, a.dtype)) return cudaErrorInvalidValue;
   ScanParams p;
+  p.seq_done = seq_done;
+  p.grid_cap = grid_cap;
   p.logits = a.logits;
   p.rowinfo = rowinfo;
   p.row_list = row_list;

@@ -399,9 +399,28 @@ cudaError_t launch_accept_insert(const DevCache& c, const VerifyArgs& a,
                                  const unsigned long long* result, const int32_t* prompt_id,
                                  const int32_t* floor_, uint32_t* cursor, uint32_t tag,
                                  srt_insert_stats* stats, cudaStream_t stream);
+// seq_done (nullable): per-sequence count of rows whose result is final;
+// grid_cap > 0: at most that many CTAs (the rest of the SMs run another kernel)
 cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2* rowinfo,
                              const int32_t* row_list, const int64_t* count,
-                             unsigned long long* result, cudaStream_t stream);
+                             unsigned long long* result, cudaStream_t stream,
+                             uint32_t* seq_done = nullptr, int grid_cap = 0);
+// the fused tree step beside the scan (step.cu): state words for n sequences
+// of P prompts, its prep (before the scan), the per-sequence row counters the
+// scan must count into, and the kernel (grid CTAs, each filling an SM)
+size_t tree_step_ov_words(int32_t n, int32_t P);
+cudaError_t launch_step_prep_ov(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                                const int64_t* row_offsets, uint32_t* ovbuf, cudaStream_t stream);
+uint32_t* tree_step_ov_seq_done(uint32_t* ovbuf, int32_t n, int32_t P);
+const int64_t* tree_step_ov_total(uint32_t* ovbuf, int32_t n, int32_t P);
+cudaError_t launch_tree_step_ov(const DevCache& c, const VerifyArgs& a,
+                                const unsigned long long* result, const int32_t* prompt_id,
+                                const int32_t* floor_, uint32_t* cursor, uint32_t tag,
+                                srt_insert_stats* stats, const int32_t* pos_base,
+                                int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
+                                int32_t* draft_parent, int32_t* draft_depth, int32_t* draft_pos,
+                                uint64_t* draft_mask, int64_t* row_offsets, uint32_t* ovbuf,
+                                int grid, cudaStream_t stream);
 // path-only verification (srt_verify_path): scratch = 2 row lists + per-seq state
 cudaError_t launch_path_verify(const DevCache& c, const VerifyArgs& a, int2* rowinfo,
                                unsigned long long* result, void* scratch, int rounds,

@@ -107,6 +107,12 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+__host__ __device__ __forceinline__ size_t tree_step_smem_per_warp_dev(int32_t D) {
+  const size_t per_warp = (cursor_warp_bytes(D) + 2 * 65 * 4 + 15) & ~size_t(15);
+  const size_t dr = 64 * 8 + 64 * sizeof(Ent);
+  return per_warp > dr ? per_warp : dr;
+}
+
 // Sort prompt p's n touch pairs (hub, child) by hub in shared memory (sk:
 // >= 256 u64 of this warp's) and write them back with the refresh tasks:
 // task t = the pairs [lo, hi) of one hub that needs a list (more than HUB_MIN
@@ -175,7 +181,8 @@ __device__ uint32_t group_touches(const DevCache& c, int32_t p, uint32_t* pdl, u
 // finishing the last one resets p's touch list and marks p ready (2).
 // Returns the cycles spent; hubs counts the tasks run.
 __device__ long long refresh_tasks(const DevCache& c, int32_t p, int lane,
-                                   unsigned long long& hubs, uint32_t* sid) {
+                                   unsigned long long& hubs, uint32_t* sid,
+                                   bool* finisher = nullptr) {
   const long long t0 = clock64();
   uint32_t* const pdl = c.pdirty + (size_t)p * PDIRTY_WORDS;
   const uint2* const task = reinterpret_cast<const uint2*>(pdl + 2 + 2 * PDIRTY_CAP);
@@ -201,6 +208,7 @@ __device__ long long refresh_tasks(const DevCache& c, int32_t p, int lane,
         atomicExch(&c.st_pready[p], 2u);  // release prompt p to its drafts
       }
       __syncwarp();
+      if (finisher) *finisher = true;
       break;
     }
   }
@@ -361,6 +369,299 @@ k_tree_step(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ res
   (void)sh_last;
 }
 
+
+// ---- the tree step beside the scan (srt_cache_set_step_overlap, D <= 32;
+// measured slower than the step after the scan on B200, so off by default:
+// DESIGN.md §5).  The scan runs on all SMs but G; this kernel, a
+// programmatic dependent launch of the scan, runs G CTAs of OV_WARPS warps
+// (each fills an SM's register file) on the SMs the scan leaves, and commits
+// and inserts each sequence as soon as the scan has finished that sequence's
+// rows (ov.seq_done, counted by the scan's last worker of each row).  Work
+// items, claimed dynamically by every warp:
+//   * phase 1 of sequence s (the sequences in order, as the scan finishes
+//     them): accept + cursor insert; the last of a prompt publishes its hub
+//     refresh tasks (ov.rf) and starts on them;
+//   * a prompt's hub refresh tasks (any warp, while it waits);
+//   * the draft of one sequence whose prompt is ready (ov.dq, appended by the
+//     warp that finishes the prompt's refresh).
+// A warp waiting for the scan runs the other two kinds.  No wait depends on
+// a warp that is not running or on the scan's completion (the scan never
+// waits on this kernel), so neither co-residency nor actual overlap is
+// needed for progress: run after the scan, the kernel gives the same result.
+constexpr int OV_WARPS = 12;
+
+struct OvState {
+  int64_t* total;      // row_offsets[n] as of the call (the scan's row count: the caller's
+                       // row_offsets may be overwritten by the next drafts meanwhile)
+  uint32_t* seq_done;  // [n] rows of sequence s the scan has finished
+  uint32_t* plist;     // [n] the batch's sequences grouped by prompt
+  uint32_t* pstart;    // [P + 1] prompt p's sequences: plist[pstart[p] .. pstart[p + 1])
+  uint32_t* pfill;     // [P] (prep scratch)
+  uint32_t* dq;        // [n] draft queue (NONE until written)
+  uint32_t* rf;        // [P] prompts with published refresh tasks (NONE until written)
+  uint32_t* ctr;       // [0] next phase-1 sequence, [1] draft entries reserved,
+                       // [2] draft entries claimed, [3] rf entries reserved
+};
+
+size_t ov_words(int32_t n, int32_t P) { return 2 + 3 * (size_t)n + 3 * (size_t)P + 1 + 8; }
+OvState ov_carve(uint32_t* b, int32_t n, int32_t P) {
+  OvState o;
+  o.total = reinterpret_cast<int64_t*>(b);  // (the buffer is 256-byte aligned)
+  o.seq_done = b + 2;
+  o.plist = o.seq_done + n;
+  o.dq = o.plist + n;
+  o.pstart = o.dq + n;
+  o.pfill = o.pstart + P + 1;
+  o.rf = o.pfill + P;
+  o.ctr = o.rf + P;
+  return o;
+}
+
+// k_step_prep plus the overlap state: per-prompt sequence lists (a counting
+// sort by prompt), cleared row counters and queues.  One CTA.
+__global__ void __launch_bounds__(1024) k_step_prep_ov(DevCache c, int32_t n,
+                                                       const int32_t* __restrict__ prompt_id,
+                                                       const int64_t* __restrict__ row_offsets,
+                                                       OvState o) {
+  __shared__ uint32_t carry_sh;
+  __shared__ uint32_t wsum[32];
+  for (int32_t i = threadIdx.x; i < c.P; i += blockDim.x) {
+    c.st_pcount[i] = 0;
+    c.st_pdone[i] = 0;
+    c.st_pready[i] = 0;
+    c.st_pnd[i] = 0;
+    c.st_pnext[i] = 0;
+    c.st_pfin[i] = 0;
+    o.pfill[i] = 0;
+    o.rf[i] = NONE;
+  }
+  for (int32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    o.seq_done[s] = 0;
+    o.dq[s] = NONE;
+  }
+  if (threadIdx.x < 8) o.ctr[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    *c.st_ndone = 0;
+    carry_sh = 0;
+    *o.total = row_offsets[n];
+  }
+  __syncthreads();
+  for (int32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    const int32_t p = prompt_id[s];
+    if (p >= 0 && p < c.P) atomicAdd(&c.st_pcount[p], 1u);
+  }
+  __syncthreads();
+  // pstart = exclusive prefix sum of pcount (block scan, 1024 prompts a pass)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int32_t b = 0; b < c.P; b += blockDim.x) {
+    const int32_t i = b + threadIdx.x;
+    const uint32_t v = i < c.P ? c.st_pcount[i] : 0u;
+    uint32_t x = v;
+    for (int k = 1; k < 32; k <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, k);
+      if (lane >= k) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t z = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0u;
+      for (int k = 1; k < 32; k <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, z, k);
+        if (lane >= k) z += y;
+      }
+      wsum[lane] = z;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t carry = carry_sh;
+    const uint32_t excl = carry + (w ? wsum[w - 1] : 0u) + x - v;
+    if (i < c.P) o.pstart[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_sh = carry + wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) o.pstart[c.P] = carry_sh;
+  __syncthreads();
+  for (int32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    const int32_t p = prompt_id[s];
+    if (p >= 0 && p < c.P) o.plist[o.pstart[p] + atomicAdd(&o.pfill[p], 1u)] = (uint32_t)s;
+  }
+}
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  return *(const volatile uint32_t*)p;
+}
+
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32, 1)
+k_tree_step_ov(DevCache c, VerifyArgs a, const unsigned long long* __restrict__ result,
+               const int32_t* __restrict__ prompt_id, const int32_t* __restrict__ floor_,
+               uint32_t* __restrict__ cursor, uint32_t tag, srt_insert_stats* stats,
+               StepDraftArgs d, OvState o) {
+  extern __shared__ __align__(16) unsigned char step_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char* mine = step_smem + (size_t)w * tree_step_smem_per_warp_dev(c.D);
+  const int32_t n = a.n;
+  const int32_t gw = blockIdx.x * WPC + w;
+  unsigned long long* const prof = g_step_prof;
+  unsigned long long pf[8] = {prof ? gtime() : 0ull, 0, 0, 0, 0, 0, 0, 0};
+
+  // append sequences [b, e) of plist (or the single sequence `one`) to the
+  // draft queue; the caller has fenced after everything the drafts read
+  auto push_drafts = [&](const uint32_t* src, uint32_t cnt) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&o.ctr[1], cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t i = lane; i < cnt; i += 32)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(o.dq + base + i), "r"(src[i])
+                   : "memory");
+    __syncwarp();
+  };
+  auto push_prompt = [&](int32_t p) {
+    const uint32_t b = o.pstart[p], e = o.pstart[p + 1];
+    push_drafts(o.plist + b, e - b);
+  };
+  // one draft whose prompt is ready, if any entry is reserved and unclaimed
+  auto try_draft = [&]() -> bool {
+    uint32_t idx = NONE;
+    if (lane == 0) {
+      uint32_t h = ld_volatile_u32(&o.ctr[2]);
+      while (h < ld_volatile_u32(&o.ctr[1])) {
+        const uint32_t old = atomicCAS(&o.ctr[2], h, h + 1);
+        if (old == h) {
+          idx = h;
+          break;
+        }
+        h = old;
+      }
+    }
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx == NONE) return false;
+    uint32_t s = NONE;
+    if (lane == 0)
+      do s = ld_acquire_u32(&o.dq[idx]); while (s == NONE);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    __threadfence();
+    ++pf[6];
+    draft_seq(c, (int32_t)s, prompt_id, a.seq_tok, a.stride, a.seq_len, d.pos_base, cursor, tag,
+              d.match_len, d.draft_len, d.draft_tok, d.draft_parent, d.draft_depth, d.draft_pos,
+              d.draft_mask, reinterpret_cast<unsigned long long*>(mine),
+              reinterpret_cast<Ent*>(mine + 64 * 8), lane, c.pdirty);
+    __syncwarp();
+    uint32_t last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(c.st_ndone, 1u) + 1 == (uint32_t)n;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __threadfence();
+      row_offsets_warp(n, d.draft_len, d.row_offsets, lane);
+    }
+    return true;
+  };
+  // run refresh tasks of a recently published prompt, if one has any left
+  auto run_refresh = [&](int32_t p) {
+    bool fin = false;
+    pf[4] += refresh_tasks(c, p, lane, pf[5], reinterpret_cast<uint32_t*>(mine), &fin);
+    if (fin) push_prompt(p);
+  };
+  auto try_refresh = [&]() -> bool {
+    int32_t pick = -1;
+    if (lane == 0) {
+      const uint32_t t = ld_volatile_u32(&o.ctr[3]);
+      for (uint32_t i = t; i > 0 && i + 8 > t; --i) {
+        const uint32_t p = ld_volatile_u32(&o.rf[i - 1]);
+        if (p == NONE) continue;
+        if (ld_acquire_u32(&c.st_pready[p]) == 1u &&
+            ld_volatile_u32(&c.st_pnext[p]) < ld_volatile_u32(&c.st_pnd[p])) {
+          pick = (int32_t)p;
+          break;
+        }
+      }
+    }
+    pick = __shfl_sync(0xffffffffu, pick, 0);
+    if (pick < 0) return false;
+    __threadfence();
+    run_refresh(pick);
+    return true;
+  };
+
+  bool p1_left = true;
+  while (true) {
+    if (try_draft()) continue;
+    if (p1_left) {
+      uint32_t s = 0;
+      if (lane == 0) s = atomicAdd(&o.ctr[0], 1u);
+      s = __shfl_sync(0xffffffffu, s, 0);
+      if (s >= (uint32_t)n) {
+        p1_left = false;
+        continue;
+      }
+      // wait for the scan to finish the sequence's rows, helping meanwhile
+      const uint32_t rows = (uint32_t)(a.row_offsets[s + 1] - a.row_offsets[s]);
+      while (true) {
+        uint32_t done = 0;
+        if (lane == 0) done = ld_acquire_u32(&o.seq_done[s]);
+        done = __shfl_sync(0xffffffffu, done, 0);
+        if (done >= rows) break;
+        if (!try_draft() && !try_refresh() && lane == 0) __nanosleep(64);
+        __syncwarp();
+      }
+      __threadfence();
+      CursorSmem S = carve_cursor_smem(mine, 0, c.D);
+      int32_t* ctok = reinterpret_cast<int32_t*>(mine + cursor_warp_bytes(c.D));
+      const int32_t t = accept_seq(c, a, result, (int32_t)s, ctok, ctok + 65, lane);
+      __syncwarp();
+      const int32_t t_end = a.seq_len[s];
+      const int32_t p = prompt_id[s];
+      if (p < 0 || p >= c.P) {
+        if (lane == 0) set_error(c, SRT_DEV_BAD_PROMPT);
+        __threadfence();
+        push_drafts(&s, 1);  // (an empty draft; s is read by lane 0 .. 0 only)
+        continue;
+      }
+      uint32_t* const pdl = c.pdirty + (size_t)p * PDIRTY_WORDS;
+      S.pdl = pdl;
+      cursor_insert_seq<1>(c, S, (int32_t)s, p, t, t_end, a.seq_tok, a.stride, floor_, INT_MAX,
+                           cursor, tag, stats);
+      __syncwarp();
+      uint32_t last = 0;
+      if (lane == 0) {
+        __threadfence();  // this sequence's tree updates before the prompt's count
+        last = atomicAdd(&c.st_pdone[p], 1u) + 1 == c.st_pcount[p];
+      }
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        __threadfence();  // every sibling's updates (they fenced before counting)
+        const uint32_t n_t = min(*(volatile uint32_t*)pdl, PDIRTY_CAP);
+        const uint32_t nd = group_touches(c, p, pdl, n_t,
+                                          reinterpret_cast<unsigned long long*>(mine), lane);
+        if (lane == 0) {
+          c.st_pnd[p] = nd;
+          if (!nd) pdl[0] = 0;
+          __threadfence();
+          atomicExch(&c.st_pready[p], nd ? 1u : 2u);
+          if (nd) {
+            const uint32_t e = atomicAdd(&o.ctr[3], 1u);
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(o.rf + e), "r"((uint32_t)p)
+                         : "memory");
+          }
+        }
+        __syncwarp();
+        if (nd) run_refresh(p);
+        else push_prompt(p);
+      }
+      continue;
+    }
+    // no phase-1 work left: the remaining drafts wait on other warps' refreshes
+    if (ld_volatile_u32(&o.ctr[2]) >= (uint32_t)n) break;
+    if (!try_refresh() && lane == 0) __nanosleep(128);
+    __syncwarp();
+  }
+  if (prof && lane == 0) {
+    pf[3] = gtime();
+    pf[1] = pf[2] = pf[3];
+    for (int i = 0; i < 8; ++i) prof[(size_t)gw * 8 + i] = pf[i];
+  }
+}
 }  // namespace
 
 size_t tree_step_smem_per_warp(int32_t D) {
@@ -460,6 +761,59 @@ cudaError_t launch_tree_step(const DevCache& c, const VerifyArgs& a,
             nref ? rsum / 1e3 / nref : 0.0);
   }
   return e;
+}
+
+size_t tree_step_ov_words(int32_t n, int32_t P) { return ov_words(n, P); }
+
+cudaError_t launch_step_prep_ov(const DevCache& c, int32_t n, const int32_t* prompt_id,
+                                const int64_t* row_offsets, uint32_t* ovbuf, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  k_step_prep_ov<<<1, 1024, 0, stream>>>(c, n, prompt_id, row_offsets, ov_carve(ovbuf, n, c.P));
+  return cudaGetLastError();
+}
+
+uint32_t* tree_step_ov_seq_done(uint32_t* ovbuf, int32_t n, int32_t P) {
+  return ov_carve(ovbuf, n, P).seq_done;
+}
+
+const int64_t* tree_step_ov_total(uint32_t* ovbuf, int32_t n, int32_t P) {
+  return ov_carve(ovbuf, n, P).total;
+}
+
+cudaError_t launch_tree_step_ov(const DevCache& c, const VerifyArgs& a,
+                                const unsigned long long* result, const int32_t* prompt_id,
+                                const int32_t* floor_, uint32_t* cursor, uint32_t tag,
+                                srt_insert_stats* stats, const int32_t* pos_base,
+                                int32_t* match_len, int32_t* draft_len, int32_t* draft_tok,
+                                int32_t* draft_parent, int32_t* draft_depth, int32_t* draft_pos,
+                                uint64_t* draft_mask, int64_t* row_offsets, uint32_t* ovbuf,
+                                int grid, cudaStream_t stream) {
+  if (c.D > 32 || grid <= 0) return cudaErrorInvalidValue;
+  if (a.n <= 0) return cudaSuccess;
+  const size_t smem = (size_t)OV_WARPS * tree_step_smem_per_warp(c.D);
+  auto kern = k_tree_step_ov<OV_WARPS>;
+  static size_t set_smem = 0;
+  if (set_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set_smem = smem;
+  }
+  StepDraftArgs d{pos_base, match_len, draft_len, draft_tok, draft_parent, draft_depth,
+                  draft_pos, draft_mask, row_offsets};
+  // a programmatic dependent launch: it may start once every CTA of the scan
+  // before it has triggered (they do as they start), on the SMs the scan left
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(OV_WARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, c, a, result, prompt_id, floor_, cursor, tag, stats, d,
+                            ov_carve(ovbuf, a.n, c.P));
 }
 
 }  // namespace srt

@@ -326,6 +326,11 @@ class SrtCache:
             check(r, "srt_cache_status")
         return int(bits.value), {k: int(getattr(st, k)) for k, _ in SrtCacheStats._fields_}
 
+    def set_step_overlap(self, sms: int) -> None:
+        """srt_cache_set_step_overlap: the fused tree step of verify_insert_draft
+        on `sms` SMs beside the scan (0: after it on every SM, -1: default)."""
+        check(self.L.srt_cache_set_step_overlap(self._h, int(sms)), "srt_cache_set_step_overlap")
+
     def profile_enable(self, capacity: int) -> None:
         check(self.L.srt_profile_enable(self._h, int(capacity)), "srt_profile_enable")
 

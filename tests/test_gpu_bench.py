@@ -174,6 +174,52 @@ def test_fused_tree_step_matches_separate_calls(D):
     assert sum(int(r[1].sum()) for r in ra) > 0 and sum(int(r[8].sum()) for r in ra) > 96 * 8
 
 
+@pytest.mark.parametrize("D", [16, 32])
+def test_fused_tree_step_beside_scan_matches(D):
+    """The fused tree step run BESIDE the scan (srt_cache_set_step_overlap:
+    the step kernel on a few SMs, committing each sequence as the scan
+    finishes its rows) leaves exactly what the step after the scan leaves,
+    step after step: sampled rows, commits, sequence tables, trees, the next
+    drafts and row offsets -- for several SM splits, including one SM (every
+    sequence's work serialised behind the scan's progress)."""
+    import torch
+    import bench
+    cfg = dict(bench.CONFIGS["grpo"])
+    cfg.update(prompts=12, active=96, V=5000, cap=1024, act_cap=1024, median=300,
+               node_capacity=1 << 21, D=D, L=8)
+    out = []
+    for sms in (0, 1, 8, 40):
+        wl = bench.Workload(cfg, 5)
+        run = bench.GpuRun(wl, "bf16", "rl-mix", 5)
+        gr = run.groups[0]
+        gr.fused_step = True
+        gr.cache.set_step_overlap(sms)
+        rec = []
+        for k in range(8):
+            rows = int(gr.d.row_offsets[gr.n].item()) if k else None  # (the rows this step verifies)
+            run.step(bench.step_seed(5, k))
+            torch.cuda.synchronize()
+            rec.append(tuple(getattr(gr.d, k).cpu().numpy().copy() for k in
+                             ("match_len", "draft_len", "draft_tok", "draft_parent",
+                              "draft_depth", "draft_pos", "draft_mask", "row_offsets")) +
+                       (gr.v.n_commit.cpu().numpy().copy(), gr.v.commit_tok.cpu().numpy().copy(),
+                        gr.v.accept_len.cpu().numpy().copy(),
+                        gr.v.sampled[:rows].cpu().numpy().copy() if rows else np.zeros(0)))
+        torch.cuda.synchronize()
+        assert run.status()[0] == 0
+        out.append((rec, gr.seq_tok.cpu().numpy(), gr.seq_len.cpu().numpy(),
+                    [gr.cache.dump(p) for p in range(cfg["prompts"])]))
+    ra, ta, la, da = out[0]
+    for rb, tb, lb, db in out[1:]:
+        for x, y in zip(ra, rb):
+            for u, v in zip(x, y):
+                np.testing.assert_array_equal(u, v)
+        np.testing.assert_array_equal(ta, tb)
+        np.testing.assert_array_equal(la, lb)
+        assert da == db
+    assert sum(int(r[1].sum()) for r in ra) > 0 and sum(int(r[8].sum()) for r in ra) > 96 * 8
+
+
 @pytest.mark.parametrize("extra", [[], ["--sharded"], ["--fused-step", "0"], ["--verify", "path"],
                                    ["--graph", "0"]])
 def test_bench_cli_runs(extra):

@@ -8,5 +8,4 @@ timeout 400 python bench.py --verify lmhead --no-cpu-baseline > gpurun_out/bench
 timeout 400 python bench.py --config ppo --no-cpu-baseline > gpurun_out/bench_ppo.log 2>&1
 timeout 600 python bench.py --config dapo --no-cpu-baseline > gpurun_out/bench_dapo.log 2>&1
 timeout 400 python bench.py --sharded --no-cpu-baseline > gpurun_out/bench_sharded.log 2>&1
-for t in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > gpurun_out/sanitize_$t.log 2>&1; tail -2 gpurun_out/sanitize_$t.log; done
 ls gpurun_out
