@@ -229,6 +229,12 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
   uint32_t* rowM = p1cnt + ((NS + 3) & ~3);                              // [NS] shared M keys
   float* tab = reinterpret_cast<float*>(rowM + ((NS + 3) & ~3));         // [1024]
   uint32_t* wdone = reinterpret_cast<uint32_t*>(tab + NOISE_BUCKETS);    // [NS] workers done
+  // per row: (position, sequence id lo, hi, sequence), fetched by the
+  // producer one row ahead (meta_p, like row_of) and handed to the tail with
+  // the summary (meta_s): no warp on the stream's path waits on the two
+  // dependent global loads (rowinfo, then seq_id) at a row's start
+  uint4* meta_p = reinterpret_cast<uint4*>(wdone + ((NS + 3) & ~3));   // [NR]
+  uint4* meta_s = meta_p + NR;                                           // [NS]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t total = *a.total;
@@ -303,10 +309,23 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         si += gridDim.x;
         return r;
       };
-      int64_t next = claim();  // claimed one row ahead: the atomic's round trip
-                               // overlaps the issue of the current row
+      // the row after the current one: claimed, and its meta fetched, while
+      // the current row's first chunk is in flight (the ring's other stages
+      // hide the round trips)
+      auto fetch = [&](int64_t i, int64_t& row, uint4& m) {
+        row = a.row_list ? a.row_list[i] : i;
+        const int2 ri = a.rowinfo[row];
+        const uint64_t sid = a.seq_id[ri.x];
+        m = make_uint4((uint32_t)ri.y, (uint32_t)sid, (uint32_t)(sid >> 32), (uint32_t)ri.x);
+      };
+      int64_t next = claim();
+      int64_t nrow = -1;
+      uint4 nmeta = make_uint4(0, 0, 0, 0);
+      if (next < total) fetch(next, nrow, nmeta);
       for (int64_t u = 0;; ++u) {
         const int64_t i = next;
+        const int64_t row = nrow;
+        const uint4 meta = nmeta;
         if (i < total) next = claim();
         if (i >= total) {
           row_of[u % NR] = -1;
@@ -323,8 +342,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
           }
           break;
         }
-        const int64_t row = a.row_list ? a.row_list[i] : i;
         row_of[u % NR] = row;
+        meta_p[u % NR] = meta;
         const char* base = (const char*)a.logits + row * row_bytes;
         for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
           const int s = (int)(kc % NST);
@@ -342,6 +361,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
             tma_load_1d_hint(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s], pol);
           else
             tma_load_1d(ring + s * CHUNK, base + (int64_t)ch * CHUNK, nb, &ring_full[s]);
+          if (ch == 0 && next < total) fetch(next, nrow, nmeta);
         }
       }
       SRT_PROF_PRINT("producer");
@@ -373,9 +393,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         break;
       }
       float* U = reinterpret_cast<float*>(sums + sb * a.sum_bytes);
-      const int2 ri = a.rowinfo[row];
-      const uint64_t sid = a.seq_id[ri.x];
-      const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+      const uint4 meta = meta_p[u % NR];
+      const uint32_t pos = meta.x, s_lo = meta.y, s_hi = meta.z;
       float tmax = -INFINITY;
       uint32_t tblk = 0xFFFFFFFFu;
       bool nan = false;
@@ -441,6 +460,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         if (atomicAdd(&p1cnt[sb], 1u) == NSW - 1) {  // the last stream warp publishes
           rowhdr[sb] = atomicExch(&p1key[sb], 0ull);
           rowid[sb] = row;
+          meta_s[sb] = meta;
           p1cnt[sb] = 0;
           mbar_arrive(&sum_ready[sb]);  // release: the summary is complete
         }
@@ -469,9 +489,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
       const unsigned long long hdr = rowhdr[sb];
       uint32_t mkey = 0u;  // (none: every logit of the row is NaN)
       if (hdr != 0 && !(a.debug & 16)) {
-        const int2 ri = a.rowinfo[row];
-        const uint64_t sid = a.seq_id[ri.x];
-        const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+        const uint4 meta = meta_s[sb];
+        const uint32_t pos = meta.x, s_lo = meta.y, s_hi = meta.z;
         const unsigned char* rowp = (const unsigned char*)a.logits + row * row_bytes;
         const float X = key_value((uint32_t)(hdr >> 32));
         const uint32_t bX = 0xFFFFFFFFu - (uint32_t)hdr;
@@ -517,9 +536,8 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     float bz = -INFINITY;
     int32_t bv = INT_MAX;
     if (hdr != 0 && !(a.debug & 16)) {  // else every logit NaN (debug 16: timing probe, no tail)
-      const int2 ri = a.rowinfo[row];
-      const uint64_t sid = a.seq_id[ri.x];
-      const uint32_t pos = (uint32_t)ri.y, s_lo = (uint32_t)sid, s_hi = (uint32_t)(sid >> 32);
+      const uint4 meta = meta_s[sb];
+      const uint32_t pos = meta.x, s_lo = meta.y, s_hi = meta.z;
       const unsigned char* rowp = (const unsigned char*)a.logits + row * row_bytes;
       float M = key_value(*(volatile uint32_t*)&rowM[sb]);  // z(i*) from the M warp
       bool raised = false;  // M raised since this warp last shared it (share_M)
@@ -641,7 +659,7 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
         if (atomicAdd(&wdone[sb], 1u) == NTW - 1) {
           wdone[sb] = 0;  // (before the arrival that frees the slot)
           __threadfence();
-          atomicAdd(&a.seq_done[a.rowinfo[row].x], 1u);
+          atomicAdd(&a.seq_done[meta_s[sb].w], 1u);
         }
       }
       mbar_arrive(&sum_free[sb]);
@@ -680,7 +698,7 @@ cudaError_t launch_rows(const DevCache& c, ScanParams p, cudaStream_t stream) {
   const size_t smem = (size_t)NST * CHUNK + (size_t)NS * p.sum_bytes +
                       (2 * NST + 3 * NS) * 8 + 2 * NS * 8 + (NS + NST + 2) * 8 +
                       2 * ((NS + 3) & ~3) * 4 +
-                      NOISE_BUCKETS * 4 + ((NS + 3) & ~3) * 4;
+                      NOISE_BUCKETS * 4 + ((NS + 3) & ~3) * 4 + (size_t)(NST + 2 + NS) * 16;
   auto kern = k_scan_rows<DT, NSW, NT, NST, NS, CHUNK, NG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
