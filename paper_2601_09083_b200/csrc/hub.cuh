@@ -157,7 +157,7 @@ __device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int l
 // old K-th entry's, which only grew).  Exact only when the touches account
 // for the whole csum change since the build; otherwise (no previous list, a
 // NONE touch = a hub a draft met without a list, lost touches) the full
-// scan of refresh_hub_warp.  sid: >= 128 words of this warp's shared memory.
+// scan of refresh_hub_warp.  sid: >= 384 words (1.5 KB) of this warp's shared memory.
 __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const uint32_t* kids,
                                  uint32_t m, uint32_t kstride, int lane, uint32_t* sid) {
   if (u >= c.H) return;
@@ -184,28 +184,44 @@ __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const
   if (lane < (int)m) sid[K + lane] = k0;
   if (lane + 32 < (int)m) sid[K + 32 + lane] = k1;
   __syncwarp();
-  KeyList L{0ull, 0ull, NONE, NONE, 0};
-  for (int j0 = 0; j0 < ncand; j0 += 32) {
-    const int j = j0 + lane;
+  // every candidate's key (0 for a repeat of an earlier one), then its rank
+  // among all of them: the entries of rank < K are the new list, written in
+  // place -- no serial inserts (keys of distinct children are distinct: the
+  // token breaks count ties)
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(sid + 128);
+  unsigned long long key[4];
+  uint32_t cid[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = q * 32 + lane;
+    cid[q] = j < ncand ? sid[j] : NONE;
     bool keep = j < ncand;
-    uint32_t id = keep ? sid[j] : NONE;
-    for (int i = 0; keep && i < j; ++i) keep = sid[i] != id;  // first occurrence only
-    unsigned long long key = 0;
-    if (keep) key = child_key(c.cnt[id], c.tok[id]);
-    L.offer(keep, key, id, lane, K);
+    for (int i = 0; keep && i < j; ++i) keep = sid[i] != cid[q];  // first occurrence only
+    key[q] = keep ? child_key(c.cnt[cid[q]], c.tok[cid[q]]) : 0ull;
   }
-  if (lane < L.size) {
-    c.hub_child[e + lane] = L.v0;
-    c.hub_tok[e + lane] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k0);
-    c.hub_cnt[e + lane] = (uint32_t)(L.k0 >> 32);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q * 32 < ncand) skey[q * 32 + lane] = key[q];
+  __syncwarp();
+  uint32_t rank[4] = {0, 0, 0, 0};
+  for (int i = 0; i < ncand; ++i) {
+    const unsigned long long ki = skey[i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rank[q] += ki > key[q];
   }
-  if (lane + 32 < L.size) {
-    c.hub_child[e + lane + 32] = L.v1;
-    c.hub_tok[e + lane + 32] = (int32_t)(0xFFFFFFFFu - (uint32_t)L.k1);
-    c.hub_cnt[e + lane + 32] = (uint32_t)(L.k1 >> 32);
+  int nvalid = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    nvalid += __popc(__ballot_sync(0xffffffffu, key[q] != 0ull));
+    if (key[q] != 0ull && rank[q] < (uint32_t)K) {
+      c.hub_child[e + rank[q]] = cid[q];
+      c.hub_tok[e + rank[q]] = (int32_t)(0xFFFFFFFFu - (uint32_t)key[q]);
+      c.hub_cnt[e + rank[q]] = (uint32_t)(key[q] >> 32);
+    }
   }
+  __syncwarp();
   if (lane == 0) {
-    c.hub_len[slot] = (uint32_t)L.size;
+    c.hub_len[slot] = (uint32_t)min(nvalid, K);
     c.hub_nch[slot] = nch;
     c.hub_csum[slot] = r.w;
     c.hub_node[slot] = u;
