@@ -56,6 +56,9 @@ k_hub_refresh(DevCache c, const uint2* __restrict__ work, const uint32_t* work_n
   __shared__ uint32_t sv[REFRESH_WARPS][HUB_K];
   __shared__ int sn[REFRESH_WARPS];
   __shared__ uint32_t sthr[REFRESH_WARPS];
+  constexpr int WCAP = 128;  // a warp's candidates ranked in shared memory (else serial inserts)
+  __shared__ unsigned long long ck[REFRESH_WARPS][WCAP];
+  __shared__ uint32_t cv_id[REFRESH_WARPS][WCAP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int K = min(HUB_K, c.Bmax);  // the draft never needs more than Bmax of them
   const uint32_t nw = *work_n;
@@ -113,9 +116,58 @@ k_hub_refresh(DevCache c, const uint2* __restrict__ work, const uint32_t* work_n
       thr = 0;
       for (int o = 0; o < REFRESH_WARPS; ++o) thr = max(thr, sthr[o]);
     }
-    // pass 2: rank only the children at or above the threshold
+    // pass 2: rank only the children at or above the threshold: each warp
+    // collects its slice's candidates and sorts them by rank (in parallel,
+    // from shared memory) into its top-K list, unless it has more than WCAP
+    // of them (then serial inserts into a sorted warp list)
+    int n = 0;
+    bool over = false;
+    for (uint32_t kb = (uint32_t)w * 32; kb < nch && !over; kb += U4 * STEP) {
+      uint32_t cv[U4], pv[U4];
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * STEP + lane;
+        pv[q] = pos_of(k >= 1 ? k : 1);
+        cv[q] = k == 0 ? c.cnt[r.y] : k < nch ? c.scnt[pv[q]] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * STEP + lane;
+        const bool in = k < nch && cv[q] >= thr;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (!b) continue;
+        if (n + __popc(b) > WCAP) {
+          over = true;
+          break;
+        }
+        if (in) {
+          const int at = n + __popc(b & lanemask_lt());
+          uint32_t id;
+          int32_t tk;
+          if (k == 0) { id = r.y; tk = (int32_t)r.z; }
+          else { id = c.slots[pv[q]]; tk = c.stok[pv[q]]; }
+          cv_id[w][at] = id;
+          ck[w][at] = child_key(cv[q], tk);
+        }
+        n += __popc(b);
+      }
+    }
+    __syncwarp();
+    if (!over) {
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const unsigned long long kj = j < n ? ck[w][j] : 0ull;
+        int rank = 0;
+        for (int i = 0; i < n; ++i) rank += ck[w][i] > kj;
+        if (j < n && rank < K) {
+          sk[w][rank] = kj;
+          sv[w][rank] = cv_id[w][j];
+        }
+      }
+      if (lane == 0) sn[w] = min(n, K);
+    }
     KeyList L{0ull, 0ull, NONE, NONE, 0};
-    for (uint32_t kb = (uint32_t)w * 32; kb < nch; kb += U4 * STEP) {
+    for (uint32_t kb = (uint32_t)w * 32; over && kb < nch; kb += U4 * STEP) {
       uint32_t cv[U4], pv[U4];
 #pragma unroll
       for (int q = 0; q < U4; ++q) {
@@ -138,11 +190,13 @@ k_hub_refresh(DevCache c, const uint2* __restrict__ work, const uint32_t* work_n
         }
       }
     }
-    sk[w][lane] = L.k0;
-    sv[w][lane] = L.v0;
-    sk[w][lane + 32] = L.k1;
-    sv[w][lane + 32] = L.v1;
-    if (lane == 0) sn[w] = L.size;
+    if (over) {
+      sk[w][lane] = L.k0;
+      sv[w][lane] = L.v0;
+      sk[w][lane + 32] = L.k1;
+      sv[w][lane + 32] = L.v1;
+      if (lane == 0) sn[w] = L.size;
+    }
     __syncthreads();
     // Merge the warps' sorted lists in parallel: an entry's place in the union
     // is its index in its own list plus the number of larger keys in each of

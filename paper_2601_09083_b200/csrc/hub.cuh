@@ -64,7 +64,41 @@ struct KeyList {
 // Ordinary loads: the fused step orders them after the acquire of the
 // prompt's release (step.cu).
 // The caller orders it before any reader of p's lists.
-__device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int lane) {
+constexpr int RANK_CAP = 192;  // candidates ranked in shared memory (else serial inserts)
+
+// Write the top K of n candidates (ids cid[], keys key[] in shared memory,
+// distinct nonzero keys) to list slot `slot` by rank, and its header.
+__device__ __forceinline__ void write_ranked(const DevCache& c, uint32_t slot, uint32_t u,
+                                             uint32_t nch, uint32_t csum, const uint32_t* cid,
+                                             const unsigned long long* key, int n, int K,
+                                             int lane) {
+  const size_t e = (size_t)slot * HUB_K;
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int j = j0 + lane;
+    const unsigned long long kj = j < n ? key[j] : 0ull;
+    uint32_t rank = 0;
+    for (int i = 0; i < n; ++i) rank += key[i] > kj;
+    if (j < n && rank < (uint32_t)K) {
+      c.hub_child[e + rank] = cid[j];
+      c.hub_tok[e + rank] = (int32_t)(0xFFFFFFFFu - (uint32_t)kj);
+      c.hub_cnt[e + rank] = (uint32_t)(kj >> 32);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    c.hub_len[slot] = (uint32_t)min(n, K);
+    c.hub_nch[slot] = nch;
+    c.hub_csum[slot] = csum;
+    c.hub_node[slot] = u;
+  }
+  __syncwarp();
+}
+
+// sid: null, or >= RANK_CAP * 3 words of this warp's shared memory (the
+// candidates at or above the threshold are then ranked in parallel there
+// unless there are more than RANK_CAP of them)
+__device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int lane,
+                                 uint32_t* sid = nullptr) {
   if (u >= c.H) return;  // roots are never expanded
   const uint4 r = *rec_of(c, u);
   const uint32_t nch = r.x;
@@ -105,6 +139,47 @@ __device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int l
       thr = __reduce_max_sync(0xffffffffu, t1);
       const unsigned who = __ballot_sync(0xffffffffu, t1 == thr);
       if (lane == __ffs(who) - 1) { t1 = t2; t2 = 0; }
+    }
+  }
+  if (sid) {  // collect the candidates, then rank them
+    uint32_t* cid = sid;
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(sid + RANK_CAP);
+    int n = 0;
+    bool over = false;
+    for (uint32_t kb = 0; kb < nch && !over; kb += U4 * 32) {
+      uint32_t cv[U4], pv[U4];
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * 32 + lane;
+        pv[q] = pos_of(k >= 1 ? k : 1);
+        cv[q] = k == 0 ? c.cnt[r.y] : k < nch ? c.scnt[pv[q]] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < U4; ++q) {
+        const uint32_t k = kb + q * 32 + lane;
+        const bool in = k < nch && cv[q] >= thr;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (!b) continue;
+        if (n + __popc(b) > RANK_CAP) {
+          over = true;
+          break;
+        }
+        if (in) {
+          const int at = n + __popc(b & lanemask_lt());
+          uint32_t id;
+          int32_t tk;
+          if (k == 0) { id = r.y; tk = (int32_t)r.z; }
+          else { id = c.slots[pv[q]]; tk = c.stok[pv[q]]; }
+          cid[at] = id;
+          key[at] = child_key(cv[q], tk);
+        }
+        n += __popc(b);
+      }
+    }
+    __syncwarp();
+    if (!over) {
+      write_ranked(c, slot, u, nch, r.w, cid, key, n, K, lane);
+      return;
     }
   }
   KeyList L{0ull, 0ull, NONE, NONE, 0};
@@ -157,7 +232,7 @@ __device__ void refresh_hub_warp(const DevCache& c, int32_t p, uint32_t u, int l
 // old K-th entry's, which only grew).  Exact only when the touches account
 // for the whole csum change since the build; otherwise (no previous list, a
 // NONE touch = a hub a draft met without a list, lost touches) the full
-// scan of refresh_hub_warp.  sid: >= 384 words (1.5 KB) of this warp's shared memory.
+// scan of refresh_hub_warp.  sid: >= RANK_CAP * 3 words (2.25 KB) of this warp's shared memory.
 __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const uint32_t* kids,
                                  uint32_t m, uint32_t kstride, int lane, uint32_t* sid) {
   if (u >= c.H) return;
@@ -174,7 +249,7 @@ __device__ void refresh_hub_incr(const DevCache& c, int32_t p, uint32_t u, const
   incr = incr && !__any_sync(0xffffffffu, k0 == NONE || k1 == NONE);
   if (lane == 0) atomicAdd(&g_refresh_stats[incr ? 0 : 1], 1ull);
   if (!incr) {
-    refresh_hub_warp(c, p, u, lane);
+    refresh_hub_warp(c, p, u, lane, sid);
     return;
   }
   const size_t e = (size_t)slot * HUB_K;
