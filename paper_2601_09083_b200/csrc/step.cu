@@ -133,10 +133,12 @@ __device__ uint32_t group_touches(const DevCache& c, int32_t p, uint32_t* pdl, u
     key[k] = i < n ? sk[i] : ~0ull;
     rank[k] = 0;
   }
+  const int per = (int)((n + 31) / 32);  // (warp-uniform) key slots in use
   for (uint32_t j = 0; j < n; ++j) {  // rank = smaller keys + equal keys before it
     const unsigned long long kj = sk[j];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
+      if (k >= per) break;
       const uint32_t i = lane + 32 * k;
       rank[k] += kj < key[k] || (kj == key[k] && j < i);
     }
