@@ -552,7 +552,7 @@ SRT_API srt_status srt_row_noise(int32_t vocab_size, uint64_t seed, int32_t n,
  * srt_stream_read — measurement support (not on the path): read the first
  * floor(bytes / chunk) * chunk bytes of the DEVICE buffer `buf` once through
  * shared memory (persistent kernel, ctas_per_sm CTAs per SM, nbuf stages of
- * chunk bytes, 1-D TMA bulk copies, L2 evict_first) and discard them; sink
+ * chunk bytes, 1-D TMA bulk copies; SRT_STREAM_HINT=1 adds an L2 evict_first policy) and discard them; sink
  * is a DEVICE word it may write.  Timed by the caller with CUDA events, it is
  * the read-only HBM stream the verify scan is compared with.
  * SRT_ERR_INVALID_ARG unless chunk is a multiple of 1 KB and the stages fit

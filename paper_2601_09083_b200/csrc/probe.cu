@@ -19,7 +19,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 __global__ void __launch_bounds__(256) k_stream_read(const char* src, int64_t total,
                                                      uint32_t chunk, int nbuf,
-                                                     unsigned long long* sink) {
+                                                     unsigned long long* sink, int hint) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)nbuf * chunk);
   const int64_t nchunks = total / chunk;
@@ -29,19 +29,28 @@ __global__ void __launch_bounds__(256) k_stream_read(const char* src, int64_t to
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // L2 policy of the copies: none (the scan's default since r02 v5, measured
+  // faster in the step) or evict_first (SRT_STREAM_HINT=1)
+  uint64_t pol = 0;
+  if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   auto issue = [&](int b, int64_t ci) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[b])),
                  "r"(chunk)
                  : "memory");
     for (uint32_t off = 0; off < chunk; off += 32768) {
       const uint32_t nb = chunk - off < 32768 ? chunk - off : 32768;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-          "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(sm + (size_t)b * chunk + off)),
-          "l"(src + ci * chunk + off), "r"(nb), "r"(smem_addr(&bar[b])), "l"(pol)
-          : "memory");
+      if (hint)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(sm + (size_t)b * chunk + off)),
+            "l"(src + ci * chunk + off), "r"(nb), "r"(smem_addr(&bar[b])), "l"(pol)
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1], %2, [%3];" ::"r"(smem_addr(sm + (size_t)b * chunk + off)),
+            "l"(src + ci * chunk + off), "r"(nb), "r"(smem_addr(&bar[b]))
+            : "memory");
     }
   };
   const int64_t first = blockIdx.x;
@@ -81,8 +90,13 @@ cudaError_t launch_stream_read(const void* buf, int64_t bytes, int32_t chunk, in
   cudaError_t e = cudaFuncSetAttribute(k_stream_read, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
+  static int hint = -1;
+  if (hint < 0) {
+    const char* h = getenv("SRT_STREAM_HINT");
+    hint = h ? atoi(h) : 0;
+  }
   k_stream_read<<<num_sms() * ctas_per_sm, 256, smem, stream>>>((const char*)buf, bytes,
-                                                                 (uint32_t)chunk, nbuf, sink);
+                                                                 (uint32_t)chunk, nbuf, sink, hint);
   return cudaGetLastError();
 }
 

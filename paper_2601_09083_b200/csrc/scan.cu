@@ -778,7 +778,9 @@ cudaError_t launch_scan_list(const DevCache& c, const VerifyArgs& a, const int2*
   // instantiated pipeline shape (development knob; tools/scan_sweep.sh)
   static int cfg[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
   if (cfg[0] < 0) {
-    int d[8] = {8, 10, 4, 4, 32, 1, 2, 0};
+    // (HINT 0: no L2 policy on the streamed rows -- evict_first was +2-4 % in
+    // the r01 probe but -2 to -4 % in every r02 step configuration)
+    int d[8] = {8, 10, 4, 4, 32, 0, 2, 0};
     if (const char* s = getenv("SRT_SCAN_ROWS")) {
       int x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       const int k = sscanf(s, "%d,%d,%d,%d,%d,%d,%d,%d", &x[0], &x[1], &x[2], &x[3], &x[4], &x[5],
