@@ -294,7 +294,12 @@ __global__ void __launch_bounds__((1 + NSW + NT) * 32, 1) k_scan_rows(DevCache c
     // ===================== producer: the rows' chunks into the ring ========
     if (lane == 0) {
       uint64_t pol = 0;
-      if (a.l2_hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      // (development knob: 1 evict_first, 2 evict_first on half the lines,
+      // 3 evict_unchanged, 4 evict_normal; 0 = no policy, the default)
+      if (a.l2_hint == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      else if (a.l2_hint == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 0.5;" : "=l"(pol));
+      else if (a.l2_hint == 3) asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+      else if (a.l2_hint == 4) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
       // Rows are claimed one at a time from the launch's shared counter
       // (a.sched; else the static sequence blockIdx.x, + gridDim.x, ...), so
       // a CTA that met slow rows takes fewer of them.  The u-th row's id goes
