@@ -91,8 +91,8 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// same, with an L2 cache-policy hint (evict_first: streamed logits should not
-// displace the trees' hash and records from L2)
+// same, with an L2 cache-policy hint (a development knob since r02 v5: no
+// policy on the streamed rows measured fastest in the step)
 __device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes,
                                                  uint64_t* bar, uint64_t pol) {
   asm volatile(
@@ -187,7 +187,7 @@ struct ScanParams {
   uint32_t debug;              // development only (SRT_SCAN_DEBUG: 8 prints the launch; 16 / 32
                                // skip the tail / stream work, timing probes with wrong results;
                                // 64: CTA 0 prints per-warp wait cycles)
-  uint32_t l2_hint;            // 0 = default policy, 1 = evict_first on the streamed rows
+  uint32_t l2_hint;            // 0 = no policy (default); 1-4 = development modes (below)
   uint32_t spin;               // 1 = stream warps poll the ring with test_wait
   uint32_t* sched;             // nullable: [0] next row to claim, [1] CTAs past the end (both 0
                                // between launches); null = static rows blockIdx.x + k gridDim.x
